@@ -1,0 +1,240 @@
+"""Pins of the CPU oracle against values the paper/SPEC and mathematics fix.
+
+Nothing here compares the oracle with a re-typed copy of itself: every
+expected value is a worked example (SPEC/PAPER line cited), a hand-derived
+closed form (tests/golden/), a library routine in a special case that reduces
+to it (torch.nn.GRUCell), or an invariant/brute-force count.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth.model import ModelDims, generate_model, zero_model
+
+pytestmark = pytest.mark.filterwarnings("ignore")
+
+
+def small_cfg(H, E, V=8, log2=10, N=3, **kw):
+    return O.make_config(V, E, H, log2, N, **kw)
+
+
+# ----------------------------------------------------------------------------- compression
+def test_sign_code_spec_S265():
+    # mode=sign, h=[0.3,-0.2,0.0] -> bits [1,0,1] (sign(0)=+, reading 5)
+    code = O.compress([0.3, -0.2, 0.0], O.KEY_SIGN)
+    assert code.tolist() == [0b101]
+
+
+def test_round2_code_spec_S266_fp32_product():
+    # round(2), h=[0.126,-0.005] -> [13,-1].  -0.005f*100 is exactly
+    # -0.5 in fp32 (an fp64 product would give -0.49999998 -> 0): reading 4.
+    code = O.compress([0.126, -0.005], O.KEY_ROUND, 2).view(np.int8)
+    assert code.tolist() == [13, -1]
+
+
+def test_round_half_away_from_zero_and_widths():
+    # 0.125*100 = 12.5 exactly -> 13 (half away; banker's rounding would give 12)
+    assert O.compress([0.125, -0.125, 0.0], O.KEY_ROUND, 2).view(np.int8).tolist() == [13, -13, 0]
+    # k=1: 0.25*10 = 2.5 -> 3 ; -0.05*10 = -0.5 -> -1
+    assert O.compress([0.25, -0.05], O.KEY_ROUND, 1).view(np.int8).tolist() == [3, -1]
+    # k=3 uses little-endian int16 (reading 6): 0.5 -> 500, -0.9994 -> -999.4 -> -999
+    c = O.compress([0.5, -0.9994], O.KEY_ROUND, 3)
+    assert len(c) == 4 and c.view(np.int16).tolist() == [500, -999]
+    # k=4: fp32(0.99995) = 0.99994999170; the fp32 product with 10000 rounds to
+    # 9999.5 exactly -> 10000 (an fp64 product, 9999.4999, would give 9999)
+    assert O.compress([np.float32(0.99995)], O.KEY_ROUND, 4).view(np.int16).tolist() == [10000]
+
+
+def test_sign_zero_negative_zero_and_bit_order():
+    # -0.0 >= 0.0 is true in IEEE: bit 1 (reading 5: never use sign-bit extraction)
+    h = np.array([-0.0, 0.5, -1e-30, 0.0, -0.7, 0.1, 0.2, -0.3, 0.9, -0.9], dtype=np.float32)
+    code = O.compress(h, O.KEY_SIGN)
+    bits = [(int(code[i // 8]) >> (i % 8)) & 1 for i in range(10)]
+    assert bits == [1, 1, 0, 1, 0, 1, 1, 0, 1, 0]
+    assert len(code) == 2
+
+
+def test_off_code_is_bit_pattern():
+    h = np.array([0.0, -0.0, 0.25], dtype=np.float32)
+    c = O.compress(h, O.KEY_OFF)
+    assert c.tobytes() == h.tobytes()
+    assert O.compress([0.0], O.KEY_OFF).tobytes() != O.compress([-0.0], O.KEY_OFF).tobytes()
+
+
+def test_round_idempotent_S267():
+    rng = np.random.default_rng(0)
+    for k, dt in ((1, np.int8), (2, np.int8), (3, np.int16)):
+        h = rng.uniform(-1, 1, 1000).astype(np.float32)
+        q = O.compress(h, O.KEY_ROUND, k).view(dt).astype(np.float32)
+        back = (q / np.float32(10 ** k)).astype(np.float32)
+        assert np.array_equal(O.compress(back, O.KEY_ROUND, k), O.compress(h, O.KEY_ROUND, k))
+
+
+def test_nonfinite_rejected():
+    with pytest.raises(ValueError):
+        O.compress([np.nan, 0.0], O.KEY_SIGN)
+
+
+# ----------------------------------------------------------------------------- MaxEnt hash
+def test_maxent_spec_S182():
+    # M=1000, w=42, ctx=[7]: (42*237967+7+1) mod 1000 = 9,994,622 mod 1000 = 622
+    assert O.maxent_indices([7], 42, 3, 1000) == [42, 622]
+
+
+def test_maxent_empty_context_S183():
+    assert O.maxent_indices([], 123457, 4, 1 << 16) == [123457 % 65536]
+
+
+def test_maxent_context_order_hand():
+    # ctx most recent LAST = [3, 9]: order 2 uses 9, order 3 uses 3.
+    # idx2 = (5*237967 + 9 + 1) mod 2^16 = 1189845 mod 65536 = 10197
+    # idx3 = (10197*237967 + 3 + 1) mod 2^16 = 13567
+    assert O.maxent_indices([3, 9], 5, 3, 1 << 16) == [5, 10197, 13567]
+    # only the last N-1 words matter
+    assert O.maxent_indices([77, 3, 9], 5, 3, 1 << 16) == [5, 10197, 13567]
+    # N caps the order
+    assert O.maxent_indices([3, 9], 5, 2, 1 << 16) == [5, 10197]
+
+
+# ----------------------------------------------------------------------------- score
+def _score_model(H, V, log2):
+    d = ModelDims(V=V, E=1, H=H, maxent_log2=log2, N=2)
+    return d, zero_model(d)
+
+
+def test_nce_score_spec_S173():
+    d, m = _score_model(2, 4, 10)
+    m["nce_w"][3] = [0.5, -0.3]
+    m["nce_b"][3] = 0.1
+    cfg = O.make_config(4, 1, 2, 10, 2)
+    assert O.score(cfg, m, [1.0, 0.0], [], 3) == pytest.approx(0.6, abs=1e-7)
+    # h = 0 -> bias only
+    assert O.score(cfg, m, [0.0, 0.0], [], 3) == pytest.approx(0.1, abs=1e-8)
+
+
+def test_maxent_score_power_of_two_analogue_of_S192():
+    # M=1024, w=42, ctx=[7]: idx = [42, (42*237967+8) mod 1024 = 382]
+    d, m = _score_model(2, 64, 10)
+    m["maxent"][42] = 0.25
+    m["maxent"][382] = 0.5
+    cfg = O.make_config(64, 1, 2, 10, 2)
+    assert O.score(cfg, m, [0.3, 0.7], [7], 42) == 0.75          # NCE part zero
+    m["nce_w"][42] = [1.0, 2.0]
+    m["nce_b"][42] = 0.125
+    # ensemble is additive (reading 13): 0.3 + 1.4 + 0.125 + 0.75
+    assert O.score(cfg, m, [0.3, 0.7], [7], 42) == pytest.approx(2.575, abs=1e-6)
+
+
+def test_score_linear_in_h_S213():
+    d = ModelDims(V=50, E=4, H=16, maxent_log2=10, N=3)
+    m = generate_model(d, seed=3)
+    cfg = O.make_config(50, 4, 16, 10, 3)
+    rng = np.random.default_rng(1)
+    h1, h2 = rng.uniform(-1, 1, (2, 16)).astype(np.float32)
+    a = np.float32(0.5)
+    z = np.zeros(16, np.float32)
+    base = O.score(cfg, m, z, [1, 2], 7)
+    lhs = O.score(cfg, m, (a * h1 + h2).astype(np.float32), [1, 2], 7) - base
+    rhs = a * (O.score(cfg, m, h1, [1, 2], 7) - base) + (O.score(cfg, m, h2, [1, 2], 7) - base)
+    assert lhs == pytest.approx(rhs, abs=1e-6)
+
+
+# ----------------------------------------------------------------------------- GRU
+def _gru_from_case(c):
+    E, H = c["E"], c["H"]
+    m = {k: np.array(c[k], dtype=np.float32) for k in
+         ("Wz", "Uz", "bz", "Wr", "Ur", "br", "Wh", "Uh", "bh")}
+    m.update(emb=np.zeros((2, E), np.float32), nce_w=np.zeros((2, H), np.float32),
+             nce_b=np.zeros(2, np.float32), maxent=np.zeros(2, np.float32))
+    cfg = O.make_config(2, E, H, 1, 1)
+    return cfg, m
+
+
+def test_gru_hand_cases(golden_dir):
+    cases = json.load(open(os.path.join(golden_dir, "gru_hand_cases.json")))["cases"]
+    for c in cases:
+        cfg, m = _gru_from_case(c)
+        out = O.gru(cfg, m, c["x"], c["h"], fp64=True)
+        exact_inputs = c["name"] == "spec_S116_scalar"
+        tol = 1e-12 if exact_inputs else 1e-7      # ln 3 is not an fp32 number
+        np.testing.assert_allclose(out, c["expected"], atol=tol, rtol=0, err_msg=c["name"])
+        for wrong in c.get("wrong", {}).values():
+            assert np.max(np.abs(out - np.array(wrong))) > 1e-3, c["name"]
+
+
+def test_gru_zero_weights_halves_state_S115():
+    d = ModelDims(V=4, E=8, H=16, maxent_log2=4, N=2)
+    m = zero_model(d)
+    cfg = O.make_config(4, 8, 16, 4, 2)
+    h = np.random.default_rng(2).uniform(-1, 1, 16).astype(np.float32)
+    out = O.gru(cfg, m, np.ones(8, np.float32), h)
+    assert np.array_equal(out, (np.float32(0.5) * h))
+
+
+def test_gru_matches_torch_grucell_when_reset_is_one():
+    """Special case r == 1 reduces the Chung GRU to a library routine.
+
+    With Wr=Ur=0 and br=40, sigma(40) rounds to 1.0 in fp64, so both
+    formulations give tanh(Wh x + Uh h + bh).  torch.nn.GRUCell uses
+    h' = (1-z_t) n + z_t h, i.e. z_t = 1 - z = sigma(-(...)): its update-gate
+    weights are the negated ones.  This pins W/U orientation (E != H), the
+    update-gate orientation, tanh and the biases.
+    """
+    E, H = 5, 3
+    rng = np.random.default_rng(4)
+    m = {k: rng.uniform(-1, 1, s).astype(np.float32) for k, s in
+         dict(Wz=(H, E), Uz=(H, H), bz=(H,), Wh=(H, E), Uh=(H, H), bh=(H,)).items()}
+    m.update(Wr=np.zeros((H, E), np.float32), Ur=np.zeros((H, H), np.float32),
+             br=np.full(H, 40.0, np.float32), emb=np.zeros((2, E), np.float32),
+             nce_w=np.zeros((2, H), np.float32), nce_b=np.zeros(2, np.float32),
+             maxent=np.zeros(2, np.float32))
+    x = rng.uniform(-1, 1, E).astype(np.float32)
+    h = rng.uniform(-1, 1, H).astype(np.float32)
+    cfg = O.make_config(2, E, H, 1, 1)
+    ours = O.gru(cfg, m, x, h, fp64=True)
+
+    cell = torch.nn.GRUCell(E, H).double()
+    t = lambda a: torch.tensor(a, dtype=torch.float64)
+    with torch.no_grad():
+        # torch gate order in weight_ih / weight_hh: (r, z, n)
+        cell.weight_ih.copy_(torch.cat([t(np.zeros((H, E))), -t(m["Wz"]), t(m["Wh"])]))
+        cell.weight_hh.copy_(torch.cat([t(np.zeros((H, H))), -t(m["Uz"]), t(m["Uh"])]))
+        cell.bias_ih.copy_(torch.cat([t(np.full(H, 40.0)), -t(m["bz"]), t(m["bh"])]))
+        cell.bias_hh.zero_()
+        ref = cell(t(x)[None], t(h)[None])[0].numpy()
+    np.testing.assert_allclose(ours, ref, atol=1e-13, rtol=0)
+
+
+def test_gru_zero_history_special_case_S117():
+    # h = 0: r*h = 0, so h' = z * tanh(Wh x + bh) with z = sigma(Wz x + bz)
+    E, H = 3, 4
+    rng = np.random.default_rng(5)
+    m = generate_model(ModelDims(V=2, E=E, H=H, maxent_log2=1, N=1), seed=5, scale=1.0,
+                       bf16_grid=False)
+    cfg = O.make_config(2, E, H, 1, 1)
+    x = rng.uniform(-1, 1, E).astype(np.float32)
+    out = O.gru(cfg, m, x, np.zeros(H, np.float32), fp64=True)
+    X = torch.tensor(x, dtype=torch.float64)
+    lin = lambda W, b: torch.nn.functional.linear(X, torch.tensor(W, dtype=torch.float64),
+                                                  torch.tensor(b, dtype=torch.float64))
+    ref = torch.sigmoid(lin(m["Wz"], m["bz"])) * torch.tanh(lin(m["Wh"], m["bh"]))
+    np.testing.assert_allclose(out, ref.numpy(), atol=1e-13, rtol=0)
+
+
+def test_gru_bounded_state_S129():
+    # h' is a convex combination of h in (-1,1) and tanh(.) in (-1,1)
+    d = ModelDims(V=2, E=6, H=12, maxent_log2=1, N=1)
+    cfg = O.make_config(2, 6, 12, 1, 1)
+    rng = np.random.default_rng(6)
+    for seed in range(3):
+        m = generate_model(d, seed=seed, scale=0.5, bf16_grid=False)
+        h = np.zeros(12, np.float32)
+        for _ in range(100):
+            h64 = O.gru(cfg, m, rng.uniform(-1, 1, 6).astype(np.float32), h, fp64=True)
+            assert np.all(np.abs(h64) < 1.0)
+            h = h64.astype(np.float32)
