@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark of the frame-batched GRU-RNNLM query step (BASELINE.json metric).
+
+    python bench.py --gpus N --steps K --warmup W [--workload multi] [--math bf16]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...        (the CPU oracle arm)
+
+A step = one decoder frame of every session this rank owns: one
+rnnlm_query_batch call that runs the whole hot path (keys, both caches,
+compaction, gather + GRU, NCE + MaxEnt scoring, result write) over that
+frame's queries.  Workload: BASELINE.json configs[4] ("multi": 64 utterance
+streams x 2,048 queries/frame on the large model, V=200k, H=E=1024, 2^27
+4-gram MaxEnt) per GPU (weak scaling: sessions are independent units,
+DESIGN.md "Multi-GPU"); synthetic, seeded (synth/).  The per-query results
+(score, child) of every step are all-gathered over NCCL on a side stream when
+N > 1.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, generate_model, generate_workload, model_dims  # noqa: E402
+
+METRIC = "RNNLM queries/sec (frame-batched, cache on)"
+UNIT = "queries/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="multi", choices=list(CONFIGS))
+    ap.add_argument("--sessions", type=int, default=None, help="sessions per rank (default: config)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--math", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--key", default="sign", help="off | sign | round:K")
+    ap.add_argument("--no-cache", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--uniform-words", action="store_true", help="(ncu evidence) no Zipf reuse")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def sessions_for(args, world):
+    S = args.sessions or CONFIGS[args.workload]["S"]
+    if args.scaling == "strong":
+        assert S % world == 0, "strong scaling needs sessions divisible by world size"
+        return S // world
+    return S
+
+
+def key_mode(name):
+    from paper_1801_09866_b200 import KEY_MODES
+    return KEY_MODES[name]
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def time_oracle(dims, model, wl, mode, k, cache, budget_s, max_steps=None):
+    """The CPU oracle as it stands (single thread), on a bounded prefix of the
+    workload's first session.  Returns (queries, seconds, frames)."""
+    import oracle as O
+    one = wl.select_sessions(0, 1)
+    cfg = O.make_config(dims.V, dims.E, dims.H, dims.maxent_log2, dims.N, mode, k,
+                        1 if cache else 0, 1, one.max_histories_hint())
+    orc = O.Oracle(cfg, model)
+    child = np.zeros(one.n_total, np.uint32)
+    done_q, t_total, f = 0, 0.0, 0
+    per_step = []
+    while f < one.frames and t_total < budget_s and (max_steps is None or f < max_steps):
+        sl = one.frame_slice(f)
+        par = O.resolve_parents(one.parent_ref[sl], child)
+        t0 = time.perf_counter()
+        _, ch, _ = orc.query_frame(one.session[sl], par, one.word[sl])
+        dt = time.perf_counter() - t0
+        child[sl] = ch
+        done_q += len(par)
+        t_total += dt
+        per_step.append(dt)
+        f += 1
+    return done_q, t_total, f, per_step
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    c = CONFIGS[args.workload]
+    dims = model_dims(args.workload)
+    model = generate_model(dims, seed=1234)
+    mode, k = key_mode(args.key)
+    steps = args.warmup + args.steps
+    wl = generate_workload(1, steps, c["B_s"], dims.V, seed=7)
+    # each step = one frame of one utterance stream (bounded sample of the workload)
+    q, secs, frames, per = time_oracle(dims, model, wl, mode, k, not args.no_cache, 1e30,
+                                       max_steps=steps)
+    timed = per[args.warmup:]
+    tq = c["B_s"] * len(timed)
+    value = tq / sum(timed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(timed) / len(timed), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "key": args.key,
+                   "sample": f"1 session x {c['B_s']} queries per step (frames {args.warmup}.."
+                             f"{steps - 1} of utterance 0)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{len(timed)} frames x {c['B_s']} queries, session 0",
+                         "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1801_09866_b200 as R
+
+    rank, world, local = dist_env()
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = CONFIGS[args.workload]
+    dims = model_dims(args.workload)
+    S = sessions_for(args, world)
+    B_s = c["B_s"]
+    frames = args.warmup + args.steps
+    model = generate_model(dims, seed=1234)
+    V_draw = dims.V
+    wl = generate_workload(S, frames, B_s, V_draw, seed=7 + rank * S,
+                           zipf_s=0.0 if args.uniform_words else 1.0)
+    mode, k = key_mode(args.key)
+    math = R.MATH_BF16 if args.math == "bf16" else R.MATH_FP32
+    n = wl.n_per_frame
+    cap = wl.max_histories_hint()
+    eng = R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math,
+                            cache_enabled=not args.no_cache, num_sessions=S,
+                            max_queries_per_call=n, max_histories_per_session=cap, device=local)
+
+    as_dev = lambda a, dt: torch.as_tensor(a.view(dt) if a.dtype.itemsize == 4 else a, device=dev)
+    d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
+    d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
+    d_ref = torch.as_tensor(wl.parent_ref, device=dev)
+    d_child = torch.zeros(wl.n_total, dtype=torch.int32, device=dev)
+    d_score = torch.zeros(wl.n_total, dtype=torch.float32, device=dev)
+    d_par = torch.zeros(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)        # > 126 MB L2
+    side = torch.cuda.Stream(device=dev)
+    gathered = torch.empty((world * n, 2), dtype=torch.int32, device=dev) if world > 1 else None
+    main = torch.cuda.current_stream()
+
+    def step(t, timed_events=None):
+        sl = wl.frame_slice(t)
+        R.resolve_parents(d_ref[sl], d_child, d_par)
+        if timed_events is not None:
+            timed_events[0].record()
+        eng.query_batch(d_sess[sl], d_par, d_word[sl], score=d_score[sl], child=d_child[sl],
+                        want_outcome=False)
+        if timed_events is not None:
+            timed_events[1].record()
+        if world > 1:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                pair = torch.stack([d_score[sl].view(torch.int32), d_child[sl]], dim=1)
+                dist.all_gather_into_tensor(gathered, pair)
+
+    # ---- warm-up
+    for t in range(args.warmup):
+        step(t)
+    torch.cuda.synchronize()
+    st0 = eng.cache_stats()
+    eng.set_timing(True)
+    eng.get_timing(reset=True)
+    l0 = eng.launch_count()
+    clocks = ClockSampler(local)
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    # the resolve kernel + the step are inside each event pair; the L2 flush is between pairs
+    for i, t in enumerate(range(args.warmup, frames)):
+        flush.zero_()
+        sl = wl.frame_slice(t)
+        evs[i][0].record()
+        R.resolve_parents(d_ref[sl], d_child, d_par)
+        eng.query_batch(d_sess[sl], d_par, d_word[sl], score=d_score[sl], child=d_child[sl],
+                        want_outcome=False)
+        if world > 1:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                pair = torch.stack([d_score[sl].view(torch.int32), d_child[sl]], dim=1)
+                dist.all_gather_into_tensor(gathered, pair)
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    timing = eng.get_timing(reset=True)
+    launches = eng.launch_count() - l0 + args.steps          # + resolve_parents kernels
+    st1 = eng.cache_stats()
+    ms_steps = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(ms_steps))
+    gru_ms = timing["ms_gru"]
+    if world > 1:
+        tt = torch.tensor([total_ms, gru_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, gru_ms_max = float(tt[0]), float(tt[1])
+    queries_rank = n * args.steps
+    total_queries = queries_rank * world
+    value = total_queries / (total_ms / 1e3)
+    d_stats = {kk: st1[kk] - st0[kk] for kk in ("total_queries", "query_hits", "hidden_lookups",
+                                                "hidden_hits", "gru_computations")}
+    rows = d_stats["gru_computations"]
+    flops = 6.0 * dims.H * (dims.E + dims.H) * rows       # [Q, E+H] x [E+H, 3H], 2 flop/MAC
+    gru_s = timing["ms_gru"] / 1e3
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    if math == R.MATH_BF16:
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        bound, peak_src = "tensor", ("measured bf16_tflops_sustained" if peaks else "fallback")
+    else:
+        sm_max = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # FP32 FFMA lanes x 2 flop x clock
+        bound, peak_src = "alu", "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz"
+    achieved = flops / gru_s / 1e12 if gru_s > 0 else 0.0
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get(args.workload, {}).get(args.math, {}).get("gru_dram_bytes_per_step")
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "bf16" if math == R.MATH_BF16 else "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "sessions_per_gpu": S, "queries_per_session_frame": B_s,
+                   "queries_per_step": total_queries // args.steps, "V": dims.V, "E": dims.E,
+                   "H": dims.H, "maxent": f"2^{dims.maxent_log2} {dims.N}-gram", "key": args.key,
+                   "cache": not args.no_cache, "math": args.math,
+                   "l2": "flushed between timed steps (256 MiB write outside the event pair)",
+                   "parallelism": f"dp{world} (sessions sharded, weights replicated, NCCL all-gather of (score, child))"},
+        "roofline": {"kernel": "GRU gate contraction (both phases, per step)", "bound": bound,
+                     "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic": f"6*H*(E+H) flop x {rows} GRU rows over {args.steps} steps",
+                     "gru_ms_per_step": timing["ms_gru"] / args.steps,
+                     "share_of_step": (timing["ms_gru"] / total_ms) if total_ms else None},
+        "kernel_ms_per_step": {kk: timing[kk] / args.steps for kk in
+                               ("ms_cache", "ms_score", "ms_gru", "ms_encode", "ms_final")},
+        "hit_rates": {"query_cache": d_stats["query_hits"] / max(1, d_stats["total_queries"]),
+                      "hidden_cache": d_stats["hidden_hits"] / max(1, d_stats["hidden_lookups"]),
+                      "gru_rows_per_step": rows / args.steps},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    # ---- e2e: same metric through the C ABI with host buffers, copies inside the timed region
+    if not args.no_e2e:
+        e2e = run_e2e(args, eng, wl, dev, world)
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        q, secs, f, _ = time_oracle(dims, model, wl, mode, k, not args.no_cache, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": q / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"session 0, frames 0..{f - 1} ({q} queries, {secs:.1f} s)",
+                                "cpu": cpu_model(), "host_cores": host_cores()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, eng, wl, dev, world):
+    """Host-buffer path: per step H2D of (session, parent, word) from pinned
+    memory, rnnlm_query_batch, D2H of (score, child); parents of the next frame
+    are resolved on the host from the returned handles (as a decoder would)."""
+    import torch
+    import torch.distributed as dist
+    n = wl.n_per_frame
+    eng.reset_session()
+    h_in = torch.empty((3, n), dtype=torch.int32).pin_memory()
+    h_score = torch.empty(n, dtype=torch.float32).pin_memory()
+    h_child = torch.empty(n, dtype=torch.int32).pin_memory()
+    d_in = torch.empty((3, n), dtype=torch.int32, device=dev)
+    d_score = torch.empty(n, dtype=torch.float32, device=dev)
+    d_child = torch.empty(n, dtype=torch.int32, device=dev)
+    child_log = np.zeros(wl.n_total, np.uint32)
+
+    def host_step(t):
+        sl = wl.frame_slice(t)
+        ref = wl.parent_ref[sl]
+        par = np.where(ref >= 0, child_log[np.maximum(ref, 0)], 0).astype(np.uint32)
+        h_in[0].numpy()[:] = wl.session[sl].view(np.int32)
+        h_in[1].numpy()[:] = par.view(np.int32)
+        h_in[2].numpy()[:] = wl.word[sl].view(np.int32)
+        d_in.copy_(h_in, non_blocking=True)
+        eng.query_batch(d_in[0], d_in[1], d_in[2], score=d_score, child=d_child, want_outcome=False)
+        h_score.copy_(d_score, non_blocking=True)
+        h_child.copy_(d_child, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        child_log[sl] = h_child.numpy().view(np.uint32)
+
+    for t in range(args.warmup):
+        host_step(t)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for t in range(args.warmup, args.warmup + args.steps):
+        host_step(t)
+    torch.cuda.synchronize()
+    secs = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([secs], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        secs = float(tt[0])
+    return {"value": n * args.steps * world / secs, "unit": UNIT,
+            "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 8 * n,
+            "note": "wall clock incl. host-side parent resolution; per rank, max over ranks"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

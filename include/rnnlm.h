@@ -1,0 +1,193 @@
+/* rnnlm.h -- C ABI of the B200-native frame-batched GRU-RNNLM query step.
+ *
+ * The operation (PAPER.md, arXiv 1801.09866; P:n = line n of PAPER.md):
+ *   An online ASR decoder emits, at every 10 ms frame, LM queries
+ *   (history, next word) for the hypotheses that reached a word boundary
+ *   (P:45-47).  Each query is answered with an unnormalised log-score
+ *   (NCE inner product of the history's GRU output with the word's output row
+ *   plus bias, plus the hashed n-gram MaxEnt bypass) and a
+ *   handle for the extended history, whose state is the GRU update
+ *   h' = GRU(x_word, h).  Redundant work is removed by an exact
+ *   LM-query cache on (history, word) (Fig. 1) and by a cache of GRU
+ *   outputs keyed on (word, lossily compressed history vector), where the
+ *   compression rounds each element to k decimals or keeps only its sign
+ *   (Table 1).  All queries of one decoder frame are one batch
+ *   (frame-wise batching).
+ *
+ *   On B200 the whole step stays resident in HBM: one rnnlm_query_batch call
+ *   = one frame for any number of sessions, executed as a short sequence of
+ *   sm_100a kernels on the caller's stream.  Semantics
+ *   are those of SURVEY.md 8(c) / DESIGN.md "Readings", which the CPU oracle
+ *   (oracle/, test infrastructure) implements one query at a time.
+ *
+ * Conventions
+ *   - One rnnlm_t per CUDA device; one host thread per handle at a time.
+ *   - Every call that takes a cudaStream_t is stream-ordered and asynchronous
+ *     and allocates nothing (so a caller may capture it in a CUDA graph).
+ *     rnnlm_cache_stats, rnnlm_get_timing and rnnlm_create/destroy synchronise.
+ *   - Pointers named d_* are DEVICE pointers owned by the caller; they must
+ *     stay valid until the work on the given stream completes.  Pointers
+ *     without the prefix are host pointers, read/written before return.
+ *   - History handles are dense u32 per session.  Handle 0 is the utterance
+ *     root: zero state, word context [0] (<s>).  A query's parent must be a
+ *     handle created by an EARLIER rnnlm_query_batch call of that session
+ *     (reading 17).  New handles are numbered densely, in stream
+ *     (index) order, over the non-QHIT queries of the session; state slots
+ *     densely over the MISS queries (reading 20).
+ *   - Errors: argument errors are returned synchronously.  Per-query errors
+ *     (session >= num_sessions, word >= V, unknown/unborn parent, batch not
+ *     sorted by session, capacity exhausted) are detected on the device: the
+ *     query gets score = NaN, child = 0xFFFFFFFF, outcome = RNNLM_INVALID, the
+ *     rest of the batch proceeds, and the first such error is latched into a
+ *     sticky word returned by rnnlm_cache_stats.  After RNNLM_E_CAPACITY the
+ *     affected session must be reset.
+ */
+#ifndef RNNLM_H
+#define RNNLM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RNNLM_ABI_VERSION 1
+
+typedef struct rnnlm rnnlm_t;          /* opaque; one per CUDA device */
+typedef struct CUstream_st *rnnlm_stream_t;   /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  RNNLM_OK = 0,
+  RNNLM_E_INVALID_ARG = 1,  /* null pointer, bad enum, n > max_queries_per_call, unsorted batch */
+  RNNLM_E_DIMENSION = 2,    /* V < 2, E/H not multiples of 8, N outside 1..8, ... */
+  RNNLM_E_NONFINITE = 3,    /* a weight is NaN or Inf */
+  RNNLM_E_VOCAB = 4,        /* query word >= V (per query, sticky) */
+  RNNLM_E_HISTORY = 5,      /* parent handle not created in an earlier call (per query, sticky) */
+  RNNLM_E_CAPACITY = 6,     /* session ran out of history handles (per query, sticky) */
+  RNNLM_E_CUDA = 7,         /* a CUDA runtime call failed */
+  RNNLM_E_OOM = 8           /* device allocation failed at create */
+} rnnlm_status;
+
+/* History-vector compression used as the hidden-state cache key. */
+typedef enum {
+  RNNLM_KEY_OFF = 0,        /* exact fp32 bit pattern */
+  RNNLM_KEY_ROUND = 1,      /* q_i = roundf(h_i * 10^k) (fp32 product, half away from zero), k = round_digits */
+  RNNLM_KEY_SIGN = 2        /* bit_i = (h_i >= 0.0f) */
+} rnnlm_key_mode;
+
+/* Arithmetic of the GRU gate contraction (a5).  States are always fp32. */
+typedef enum {
+  RNNLM_MATH_FP32 = 0,      /* FP32 FFMA (SIMT) */
+  RNNLM_MATH_TF32 = 1,      /* reserved (rnnlm_create returns RNNLM_E_INVALID_ARG in ABI v1) */
+  RNNLM_MATH_BF16 = 2       /* bf16 operands, fp32 accumulation on tcgen05 tensor cores */
+} rnnlm_math;
+
+typedef enum { RNNLM_QHIT = 0, RNNLM_SHIT = 1, RNNLM_MISS = 2, RNNLM_INVALID = 255 } rnnlm_outcome;
+
+typedef struct {
+  uint32_t vocab, embed, hidden;        /* V >= 2 (word 0 = <s>), E, H; E and H multiples of 8 */
+  uint32_t maxent_log2, maxent_order;   /* MaxEnt table M = 2^maxent_log2 floats (<= 2^31); order N in 1..8 */
+  uint32_t key_mode, round_digits;      /* rnnlm_key_mode; round_digits in 1..4 when ROUND */
+  uint32_t math;                        /* rnnlm_math */
+  uint32_t cache_enabled;               /* 0: no cache at all, every valid query is a MISS */
+  uint32_t num_sessions;                /* utterance streams owned by this handle */
+  uint32_t max_queries_per_call;        /* B_max: fixes scratch sizes */
+  uint32_t max_histories_per_session;   /* handle/state capacity per session (>= 2); no eviction */
+  int32_t device;                       /* CUDA device ordinal */
+} rnnlm_config;
+
+/* Host fp32 row-major weights, copied at create (caller may free on return).
+ * Shapes: emb V x E; Wz, Wr, Wh H x E; Uz, Ur, Uh H x H; bz, br, bh H;
+ * nce_w V x H (row per word, the paper's H x V matrix transposed);
+ * nce_b V; maxent 2^maxent_log2. */
+typedef struct {
+  const float *emb;
+  const float *Wz, *Uz, *bz, *Wr, *Ur, *br, *Wh, *Uh, *bh;
+  const float *nce_w, *nce_b;
+  const float *maxent;
+} rnnlm_weights;
+
+typedef struct {
+  uint64_t total_queries, query_hits, hidden_lookups, hidden_hits, gru_computations;
+  int32_t sticky_error;                 /* rnnlm_status of the first per-query error, else 0 */
+  int32_t pad_;
+} rnnlm_stats;
+
+/* Per-kernel-group device time accumulated while timing is enabled
+ * (CUDA events on the caller's stream around each group). */
+typedef struct {
+  double ms_cache;      /* key/probe/claim/scan/commit kernels (a1-a4) */
+  double ms_score;      /* NCE + MaxEnt scoring (a6) */
+  double ms_gru;        /* gather + gate contraction + gates, both phases (a5) */
+  double ms_encode;     /* code + code hash of new states (a1, at state creation) */
+  double ms_final;      /* result write + counters (a7) */
+  uint64_t calls;       /* timed query_batch calls */
+  uint64_t launches;    /* kernels launched by those calls */
+} rnnlm_timing;
+
+/* Create an engine on cfg->device: validates dims and weights, copies the
+ * weights into kernel layouts, allocates every pool once, resets all
+ * sessions.  On failure *out = NULL and the status says why. */
+rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm_t **out);
+void rnnlm_destroy(rnnlm_t *h);
+
+/* Utterance start for one session (UINT32_MAX = all): clears both caches,
+ * counters, histories; handle 0 becomes the root again. */
+rnnlm_status rnnlm_reset_session(rnnlm_t *h, uint32_t session, rnnlm_stream_t stream);
+
+/* One decoder frame of n LM queries (frame-wise batching).
+ *   d_session, d_parent, d_word: n u32 each.  Queries must be sorted by
+ *     session (non-decreasing); within a session, index order is stream order.
+ *   d_score (n f32), d_child (n u32): results; d_outcome (n u8) may be NULL.
+ * Steps: (a1) key of the parent state, (a2) LM-query cache,
+ * (a3) hidden-state cache, (a4) miss compaction + handle/slot allocation,
+ * (a5) embedding gather + GRU for the misses, (a6) NCE + MaxEnt score of every
+ * non-QHIT query, (a7) result write + cache inserts + counters. */
+rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
+                               const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
+                               uint32_t *d_child, uint8_t *d_outcome, rnnlm_stream_t stream);
+
+/* Counters of one session (UINT32_MAX = sum over all).  Synchronises the
+ * device.  Returns the sticky error (also stored in out->sticky_error). */
+rnnlm_status rnnlm_cache_stats(rnnlm_t *h, uint32_t session, rnnlm_stats *out);
+
+/* States (n x H fp32) of n handles of one session; unknown handles -> NaN rows. */
+rnnlm_status rnnlm_read_states(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
+                               float *d_states, rnnlm_stream_t stream);
+/* State slot of each handle (0xFFFFFFFF if unknown). */
+rnnlm_status rnnlm_read_slots(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
+                              uint32_t *d_slots, rnnlm_stream_t stream);
+/* Stored compression code of each handle's state, rnnlm_code_bytes() bytes per
+ * row (sign: bit i in byte i/8 at bit i%8; round: int8 (k<=2) / LE int16;
+ * off: the fp32 bit patterns).  Unknown handles -> 0xFF bytes. */
+rnnlm_status rnnlm_read_codes(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
+                              uint8_t *d_codes, rnnlm_stream_t stream);
+/* The same compression applied to n arbitrary fp32 rows d_states (n x H),
+ * with the handle's key mode (inspection/testing of step a1). */
+rnnlm_status rnnlm_encode_states(rnnlm_t *h, uint32_t n, const float *d_states, uint8_t *d_codes,
+                                 rnnlm_stream_t stream);
+/* MaxEnt feature indices of queries (session, parent, word), n x maxent_order
+ * u64, unused orders = UINT64_MAX (inspection/testing of step a6). */
+rnnlm_status rnnlm_maxent_indices(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
+                                  const uint32_t *d_parent, const uint32_t *d_word, uint64_t *d_idx,
+                                  rnnlm_stream_t stream);
+uint32_t rnnlm_code_bytes(const rnnlm_t *h);
+
+/* Workload plumbing (not part of the method): d_parent[i] = d_ref[i] < 0 ? 0
+ * : d_log[d_ref[i]], i.e. map "child of earlier query j" references to the
+ * handles the engine returned for those queries. */
+rnnlm_status rnnlm_resolve_parents(uint32_t n, const int64_t *d_ref, const uint32_t *d_log,
+                                   uint32_t *d_parent, rnnlm_stream_t stream);
+
+rnnlm_status rnnlm_set_timing(rnnlm_t *h, int enable);
+rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset);
+/* Kernels launched by this handle since create (host-side count). */
+uint64_t rnnlm_launch_count(const rnnlm_t *h);
+const char *rnnlm_status_string(rnnlm_status s);
+int rnnlm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RNNLM_H */

@@ -1,0 +1,12 @@
+"""B200-native frame-batched GRU-RNNLM query step (arXiv 1801.09866 hot path).
+
+The product is librnnlm.so (hand-written sm_100a kernels behind the C ABI of
+include/rnnlm.h); this package is its thin binding plus host-side reporting.
+"""
+from .engine import (ALL, INVALID, KEY_MODES, KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32,
+                     MISS, QHIT, RNNLM, SHIT, as_u32, resolve_parents)
+from .stats import hit_ratio, redundancy_rate
+
+__all__ = ["RNNLM", "KEY_OFF", "KEY_ROUND", "KEY_SIGN", "KEY_MODES", "MATH_FP32", "MATH_BF16",
+           "QHIT", "SHIT", "MISS", "INVALID", "ALL", "resolve_parents", "as_u32",
+           "redundancy_rate", "hit_ratio"]

@@ -1,0 +1,461 @@
+// api.cu -- the C ABI (include/rnnlm.h): engine creation, pools, weight
+// layouts, and the per-frame orchestration of rnnlm_query_batch.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "rnnlm_impl.cuh"
+
+using namespace rnnlm_dev;
+
+namespace rnnlm_host {
+// Tensor-core path (k_gru_tc.cu).  Returns kernels launched, or -1 if the
+// configuration is not supported by it.
+int gru_tc_supported(uint32_t E, uint32_t H);
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_out);
+void gru_tc_release(void *state);
+int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax);
+int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s);
+}  // namespace rnnlm_host
+
+struct rnnlm {
+  rnnlm_config cfg{};
+  Params P{};
+  int num_sms = 148;
+  std::vector<void *> allocs;
+  void *tc = nullptr;                 // tensor-core GRU state (descriptors, weights)
+  uint32_t epoch = 0;
+  uint64_t launches = 0;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::vector<cudaEvent_t>> ev_pending;   // 6 events per timed call
+  rnnlm_timing acc{};
+};
+
+namespace {
+
+constexpr int NEV = 6;
+
+rnnlm_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return RNNLM_OK;
+  return e == cudaErrorMemoryAllocation ? RNNLM_E_OOM : RNNLM_E_CUDA;
+}
+
+template <typename T>
+rnnlm_status dalloc(rnnlm *h, T **p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return RNNLM_OK;
+  void *v = nullptr;
+  cudaError_t e = cudaMalloc(&v, count * sizeof(T));
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return RNNLM_E_OOM;
+  }
+  h->allocs.push_back(v);
+  *p = static_cast<T *>(v);
+  return RNNLM_OK;
+}
+
+uint32_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return (uint32_t)p;
+}
+
+bool all_finite(const float *p, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+bool all_bf16_exact(const float *p, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    uint32_t u;
+    std::memcpy(&u, &p[i], 4);
+    if (u & 0xFFFFu) return false;
+  }
+  return true;
+}
+
+uint32_t code_bytes_of(uint32_t mode, uint32_t k, uint32_t H) {
+  if (mode == RNNLM_KEY_SIGN) return (H + 7) / 8;
+  if (mode == RNNLM_KEY_ROUND) return k <= 2 ? H : 2 * H;
+  return 4 * H;
+}
+
+template <typename T>
+rnnlm_status upload(rnnlm *h, T **dst, const T *src, size_t count) {
+  rnnlm_status st = dalloc(h, dst, count);
+  if (st != RNNLM_OK) return st;
+  return cuda_status(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+rnnlm_status upload_bf16(rnnlm *h, __nv_bfloat16 **dst, const float *src, size_t count) {
+  std::vector<__nv_bfloat16> tmp(count);
+  for (size_t i = 0; i < count; ++i) tmp[i] = __float2bfloat16_rn(src[i]);
+  return upload(h, dst, tmp.data(), count);
+}
+
+void free_all(rnnlm *h) {
+  if (h->tc) rnnlm_host::gru_tc_release(h->tc);
+  h->tc = nullptr;
+  for (void *p : h->allocs) cudaFree(p);
+  h->allocs.clear();
+  for (auto &v : h->ev_pending)
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  h->ev_pending.clear();
+  h->ev_pool.clear();
+}
+
+cudaEvent_t take_event(rnnlm *h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rnnlm_abi_version(void) { return RNNLM_ABI_VERSION; }
+
+const char *rnnlm_status_string(rnnlm_status s) {
+  switch (s) {
+    case RNNLM_OK: return "ok";
+    case RNNLM_E_INVALID_ARG: return "invalid argument";
+    case RNNLM_E_DIMENSION: return "invalid dimension";
+    case RNNLM_E_NONFINITE: return "non-finite weight";
+    case RNNLM_E_VOCAB: return "word id >= vocab";
+    case RNNLM_E_HISTORY: return "unknown or unborn parent history";
+    case RNNLM_E_CAPACITY: return "history capacity exhausted";
+    case RNNLM_E_CUDA: return "CUDA error";
+    case RNNLM_E_OOM: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+uint32_t rnnlm_code_bytes(const rnnlm_t *h) { return h ? h->P.code_bytes : 0; }
+uint64_t rnnlm_launch_count(const rnnlm_t *h) { return h ? h->launches : 0; }
+
+rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm_t **out) {
+  if (!out) return RNNLM_E_INVALID_ARG;
+  *out = nullptr;
+  if (!cfg || !w) return RNNLM_E_INVALID_ARG;
+  const rnnlm_config c = *cfg;
+  if (c.vocab < 2 || c.embed == 0 || c.hidden == 0 || c.embed % 8 || c.hidden % 8 ||
+      c.maxent_order < 1 || c.maxent_order > 8 || c.maxent_log2 > 31 || c.num_sessions == 0 ||
+      c.max_queries_per_call == 0 || c.max_histories_per_session < 2 ||
+      c.max_histories_per_session > 0x7FFFFFFFu || c.max_queries_per_call > 0x7FFFFFFFu)
+    return RNNLM_E_DIMENSION;
+  if (c.key_mode > RNNLM_KEY_SIGN) return RNNLM_E_INVALID_ARG;
+  if (c.key_mode == RNNLM_KEY_ROUND && (c.round_digits < 1 || c.round_digits > 4))
+    return RNNLM_E_INVALID_ARG;
+  if (c.math != RNNLM_MATH_FP32 && c.math != RNNLM_MATH_BF16) return RNNLM_E_INVALID_ARG;
+  if (c.math == RNNLM_MATH_BF16 && !rnnlm_host::gru_tc_supported(c.embed, c.hidden))
+    return RNNLM_E_DIMENSION;
+  const size_t V = c.vocab, E = c.embed, H = c.hidden, M = (size_t)1 << c.maxent_log2;
+  const float *arrs[] = {w->emb, w->Wz, w->Uz, w->bz, w->Wr, w->Ur, w->br,
+                         w->Wh, w->Uh, w->bh, w->nce_w, w->nce_b, w->maxent};
+  const size_t lens[] = {V * E, H * E, H * H, H, H * E, H * H, H, H * E, H * H, H, V * H, V, M};
+  for (int i = 0; i < 13; ++i)
+    if (!arrs[i]) return RNNLM_E_INVALID_ARG;
+  for (int i = 0; i < 13; ++i)
+    if (!all_finite(arrs[i], lens[i])) return RNNLM_E_NONFINITE;
+
+  if (cudaSetDevice(c.device) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return RNNLM_E_CUDA;
+  }
+  rnnlm *h = new (std::nothrow) rnnlm;
+  if (!h) return RNNLM_E_OOM;
+  h->cfg = c;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+  Params &P = h->P;
+  P.V = c.vocab; P.E = c.embed; P.H = c.hidden; P.N = c.maxent_order; P.S = c.num_sessions;
+  P.cap = c.max_histories_per_session;
+  const uint32_t tcap = next_pow2(2ull * P.cap);
+  P.qmask = tcap - 1;
+  P.hmask = tcap - 1;
+  P.key_mode = c.key_mode; P.round_digits = c.round_digits; P.cache = c.cache_enabled ? 1 : 0;
+  P.math = c.math;
+  P.M_mask = (unsigned long long)M - 1;
+  P.code_bytes = code_bytes_of(c.key_mode, c.round_digits, P.H);
+  P.code_words = (P.code_bytes + 3) / 4;
+  P.cstride = c.key_mode == RNNLM_KEY_OFF ? 0 : (P.code_bytes + 15) / 16 * 16;
+  P.Hp = (P.H + 63) / 64 * 64;
+  const float scales[5] = {1.0f, 10.0f, 100.0f, 1000.0f, 10000.0f};
+  P.round_scale = c.key_mode == RNNLM_KEY_ROUND ? scales[c.round_digits] : 1.0f;
+
+  rnnlm_status st = RNNLM_OK;
+  const size_t S = c.num_sessions, cap = P.cap, B = c.max_queries_per_call;
+  const size_t Hp = P.Hp, nub = Hp / 64;
+  auto chk = [&](rnnlm_status s2) { if (st == RNNLM_OK) st = s2; };
+  // ---- weights
+  chk(upload(h, const_cast<float **>(&P.emb), w->emb, V * E));
+  chk(upload(h, const_cast<float **>(&P.nce_b), w->nce_b, V));
+  chk(upload(h, const_cast<float **>(&P.maxent), w->maxent, M));
+  if (c.math == RNNLM_MATH_BF16 && all_bf16_exact(w->nce_w, V * H))
+    chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.nce_w16), w->nce_w, V * H));
+  else
+    chk(upload(h, const_cast<float **>(&P.nce_w), w->nce_w, V * H));
+  if (c.math == RNNLM_MATH_FP32) {
+    std::vector<float> w1x(E * nub * 192, 0.0f), w1h(H * nub * 128, 0.0f), b1(nub * 192, 0.0f),
+        w2(H * Hp, 0.0f);
+    const float *Wg[3] = {w->Wz, w->Wr, w->Wh};
+    const float *Ug[2] = {w->Uz, w->Ur};
+    const float *bg[3] = {w->bz, w->br, w->bh};
+    for (size_t u = 0; u < H; ++u) {
+      const size_t ub = u / 64, uu = u % 64;
+      for (int g = 0; g < 3; ++g) {
+        for (size_t k = 0; k < E; ++k) w1x[(k * nub + ub) * 192 + g * 64 + uu] = Wg[g][u * E + k];
+        b1[ub * 192 + g * 64 + uu] = bg[g][u];
+      }
+      for (int g = 0; g < 2; ++g)
+        for (size_t k = 0; k < H; ++k) w1h[(k * nub + ub) * 128 + g * 64 + uu] = Ug[g][u * H + k];
+      for (size_t k = 0; k < H; ++k) w2[k * Hp + u] = w->Uh[u * H + k];
+    }
+    chk(upload(h, const_cast<float **>(&P.w1x), w1x.data(), w1x.size()));
+    chk(upload(h, const_cast<float **>(&P.w1h), w1h.data(), w1h.size()));
+    chk(upload(h, const_cast<float **>(&P.b1), b1.data(), b1.size()));
+    chk(upload(h, const_cast<float **>(&P.w2), w2.data(), w2.size()));
+  } else {
+    chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.emb16), w->emb, V * E));
+    if (st == RNNLM_OK && rnnlm_host::gru_tc_prepare(w, c.embed, c.hidden, &h->tc) != 0)
+      st = RNNLM_E_OOM;
+  }
+  // ---- pools
+  chk(dalloc(h, &P.rec, S * cap));
+  chk(dalloc(h, &P.state, S * cap * H));
+  if (c.math == RNNLM_MATH_BF16) chk(dalloc(h, &P.state16, S * cap * H));
+  if (P.cache) {
+    if (c.key_mode != RNNLM_KEY_OFF) chk(dalloc(h, &P.codes, S * cap * P.cstride));
+    chk(dalloc(h, &P.codehash, S * cap));
+    chk(dalloc(h, &P.qtab, S * tcap));
+    chk(dalloc(h, &P.qowner, S * tcap));
+    chk(dalloc(h, &P.htab, S * tcap));
+    chk(dalloc(h, &P.howner, S * tcap));
+  }
+  chk(dalloc(h, &P.ctr, S));
+  chk(dalloc(h, &P.sticky, 1));
+  // ---- scratch
+  uint32_t **u32s[] = {&P.st, &P.qent, &P.aux, &P.hent, &P.pslot, &P.cslot, &P.excl_nonq,
+                       &P.excl_miss, &P.nonq_list, &P.row_src, &P.row_dst, &P.row_word};
+  for (uint32_t **p : u32s) chk(dalloc(h, p, B));
+  uint32_t **segs[] = {&P.seg_excl_nonq, &P.seg_excl_miss, &P.seg_cnt_nonq, &P.seg_cnt_miss};
+  for (uint32_t **p : segs) chk(dalloc(h, p, S));
+  chk(dalloc(h, &P.tile_status, (B + rnnlm_host::SCAN_TILE - 1) / rnnlm_host::SCAN_TILE));
+  chk(dalloc(h, &P.tile_ticket, 1));
+  chk(dalloc(h, &P.counts, 4));
+  chk(dalloc(h, &P.g_z, B * H));
+  chk(dalloc(h, &P.g_wxb, B * H));
+  if (c.math == RNNLM_MATH_FP32) chk(dalloc(h, &P.g_rh, B * H));
+  else chk(dalloc(h, &P.g_rh16, B * H));
+  if (st == RNNLM_OK && c.math == RNNLM_MATH_BF16 && rnnlm_host::gru_tc_bind(h->tc, P.g_rh16, (uint32_t)B) != 0)
+    st = RNNLM_E_CUDA;
+  if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.sticky, 0, sizeof(int))));
+  if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.counts, 0, 4 * sizeof(uint32_t))));
+  if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.row_dst, 0xFF, B * sizeof(uint32_t))));
+  if (st == RNNLM_OK) {
+    st = rnnlm_reset_session(h, 0xFFFFFFFFu, nullptr);
+    if (st == RNNLM_OK) st = cuda_status(cudaDeviceSynchronize());
+  }
+  if (st != RNNLM_OK) {
+    free_all(h);
+    delete h;
+    (void)cudaGetLastError();
+    return st;
+  }
+  *out = h;
+  return RNNLM_OK;
+}
+
+void rnnlm_destroy(rnnlm_t *h) {
+  if (!h) return;
+  cudaSetDevice(h->cfg.device);
+  cudaDeviceSynchronize();
+  free_all(h);
+  delete h;
+}
+
+rnnlm_status rnnlm_reset_session(rnnlm_t *h, uint32_t session, rnnlm_stream_t stream) {
+  if (!h) return RNNLM_E_INVALID_ARG;
+  const Params &P = h->P;
+  uint32_t lo = session, hi = session + 1;
+  if (session == 0xFFFFFFFFu) { lo = 0; hi = P.S; }
+  else if (session >= P.S) return RNNLM_E_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t n = hi - lo, tcap = (size_t)P.qmask + 1;
+  cudaError_t e = cudaSuccess;
+  if (P.cache) {
+    e = cudaMemsetAsync(P.qtab + lo * tcap, 0xFF, n * tcap * sizeof(QEntry), s);
+    if (!e) e = cudaMemsetAsync(P.qowner + lo * tcap, 0xFF, n * tcap * sizeof(uint32_t), s);
+    if (!e) e = cudaMemsetAsync(P.htab + lo * tcap, 0xFF, n * tcap * sizeof(HEntry), s);
+    if (!e) e = cudaMemsetAsync(P.howner + lo * tcap, 0xFF, n * tcap * sizeof(uint32_t), s);
+  }
+  if (!e) e = cudaMemsetAsync(P.ctr + lo, 0, n * sizeof(SessCtr), s);
+  if (e) return cuda_status(e);
+  h->launches += rnnlm_host::launch_reset_root(P, lo, hi, s);
+  // the root is handle 0 / slot 0: cursors start at 1
+  std::vector<SessCtr> init(n);
+  for (auto &c : init) { std::memset(&c, 0, sizeof c); c.next_handle = 1; c.next_slot = 1; }
+  e = cudaMemcpyAsync(P.ctr + lo, init.data(), n * sizeof(SessCtr), cudaMemcpyHostToDevice, s);
+  if (!e) e = cudaStreamSynchronize(s);     // init lives on the host stack
+  return cuda_status(e);
+}
+
+rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
+                               const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
+                               uint32_t *d_child, uint8_t *d_outcome, rnnlm_stream_t stream) {
+  if (!h) return RNNLM_E_INVALID_ARG;
+  if (n == 0) return RNNLM_OK;
+  if (n > h->cfg.max_queries_per_call) return RNNLM_E_INVALID_ARG;
+  if (!d_session || !d_parent || !d_word || !d_score || !d_child) return RNNLM_E_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CallArgs A;
+  A.n = n;
+  A.epoch = ++h->epoch;
+  if (A.epoch == 0) A.epoch = ++h->epoch;
+  A.session = d_session; A.parent = d_parent; A.word = d_word;
+  A.score = d_score; A.child = d_child; A.outcome = d_outcome;
+  const Params &P = h->P;
+  std::vector<cudaEvent_t> ev;
+  if (h->timing) {
+    for (int i = 0; i < NEV; ++i) ev.push_back(take_event(h));
+    cudaEventRecord(ev[0], s);
+  }
+  int k = 0;
+  k += rnnlm_host::launch_cache_front(P, A, s);
+  k += rnnlm_host::launch_commit(P, A, s);
+  if (h->timing) cudaEventRecord(ev[1], s);
+  k += rnnlm_host::launch_score(P, A, h->num_sms, s);
+  if (h->timing) cudaEventRecord(ev[2], s);
+  if (P.math == RNNLM_MATH_BF16) k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s);
+  else k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
+  if (h->timing) cudaEventRecord(ev[3], s);
+  k += rnnlm_host::launch_encode_rows(P, n, h->num_sms, s);
+  if (h->timing) cudaEventRecord(ev[4], s);
+  k += rnnlm_host::launch_final(P, A, s);
+  if (h->timing) {
+    cudaEventRecord(ev[5], s);
+    h->ev_pending.push_back(ev);
+    h->acc.calls += 1;
+    h->acc.launches += (uint64_t)k;
+  }
+  h->launches += (uint64_t)k;
+  return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_cache_stats(rnnlm_t *h, uint32_t session, rnnlm_stats *out) {
+  if (!h || !out) return RNNLM_E_INVALID_ARG;
+  const Params &P = h->P;
+  if (session != 0xFFFFFFFFu && session >= P.S) return RNNLM_E_INVALID_ARG;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e) return cuda_status(e);
+  std::vector<SessCtr> c(P.S);
+  e = cudaMemcpy(c.data(), P.ctr, P.S * sizeof(SessCtr), cudaMemcpyDeviceToHost);
+  int sticky = 0;
+  if (!e) e = cudaMemcpy(&sticky, P.sticky, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e) return cuda_status(e);
+  std::memset(out, 0, sizeof *out);
+  for (uint32_t i = 0; i < P.S; ++i) {
+    if (session != 0xFFFFFFFFu && session != i) continue;
+    out->total_queries += c[i].total;
+    out->query_hits += c[i].qhits;
+    out->hidden_lookups += c[i].hlookups;
+    out->hidden_hits += c[i].hhits;
+    out->gru_computations += c[i].gru;
+  }
+  out->sticky_error = sticky;
+  return (rnnlm_status)sticky;
+}
+
+rnnlm_status rnnlm_read_states(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
+                               float *d_states, rnnlm_stream_t stream) {
+  if (!h || (n && (!d_handles || !d_states))) return RNNLM_E_INVALID_ARG;
+  h->launches += rnnlm_host::launch_read_states(h->P, session, n, d_handles, d_states,
+                                                reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_read_slots(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
+                              uint32_t *d_slots, rnnlm_stream_t stream) {
+  if (!h || (n && (!d_handles || !d_slots))) return RNNLM_E_INVALID_ARG;
+  h->launches += rnnlm_host::launch_read_slots(h->P, session, n, d_handles, d_slots,
+                                               reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_read_codes(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
+                              uint8_t *d_codes, rnnlm_stream_t stream) {
+  if (!h || (n && (!d_handles || !d_codes))) return RNNLM_E_INVALID_ARG;
+  if (!h->P.cache && h->P.key_mode != RNNLM_KEY_OFF) return RNNLM_E_INVALID_ARG;  // no arena
+  h->launches += rnnlm_host::launch_read_codes(h->P, session, n, d_handles, d_codes,
+                                               reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_encode_states(rnnlm_t *h, uint32_t n, const float *d_states, uint8_t *d_codes,
+                                 rnnlm_stream_t stream) {
+  if (!h || (n && (!d_states || !d_codes))) return RNNLM_E_INVALID_ARG;
+  Params P = h->P;
+  if (P.key_mode != RNNLM_KEY_OFF && P.cstride == 0) return RNNLM_E_INVALID_ARG;
+  h->launches += rnnlm_host::launch_encode_states(P, n, d_states, d_codes,
+                                                  reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_maxent_indices(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
+                                  const uint32_t *d_parent, const uint32_t *d_word, uint64_t *d_idx,
+                                  rnnlm_stream_t stream) {
+  if (!h || (n && (!d_session || !d_parent || !d_word || !d_idx))) return RNNLM_E_INVALID_ARG;
+  h->launches += rnnlm_host::launch_maxent_indices(
+      h->P, n, d_session, d_parent, d_word, reinterpret_cast<unsigned long long *>(d_idx),
+      reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_resolve_parents(uint32_t n, const int64_t *d_ref, const uint32_t *d_log,
+                                   uint32_t *d_parent, rnnlm_stream_t stream) {
+  if (n && (!d_ref || !d_log || !d_parent)) return RNNLM_E_INVALID_ARG;
+  rnnlm_host::launch_resolve_parents(n, d_ref, d_log, d_parent,
+                                     reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_set_timing(rnnlm_t *h, int enable) {
+  if (!h) return RNNLM_E_INVALID_ARG;
+  h->timing = enable != 0;
+  return RNNLM_OK;
+}
+
+rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset) {
+  if (!h || !out) return RNNLM_E_INVALID_ARG;
+  for (auto &ev : h->ev_pending) {
+    cudaError_t e = cudaEventSynchronize(ev[NEV - 1]);
+    if (e) return cuda_status(e);
+    float ms[NEV - 1];
+    for (int i = 0; i + 1 < NEV; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
+    h->acc.ms_cache += ms[0];
+    h->acc.ms_score += ms[1];
+    h->acc.ms_gru += ms[2];
+    h->acc.ms_encode += ms[3];
+    h->acc.ms_final += ms[4];
+    for (cudaEvent_t e2 : ev) h->ev_pool.push_back(e2);
+  }
+  h->ev_pending.clear();
+  *out = h->acc;
+  if (reset) h->acc = rnnlm_timing{};
+  return RNNLM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,468 @@
+// k_cache.cu -- steps (a2) LM-query cache, (a3) hidden-state cache,
+// (a4) miss compaction + handle/slot allocation, (a7) result write + counters.
+//
+// Paper: "The LM queries with same history as well as following words are
+// deduplicated by applying a cache strategy at the start of the rescoring
+// procedure"; "we created another cache for that vectors just before
+// computing RNNLMs ... The key of the cache is the GRU input which is a pair
+// of a word embedding and a history vector, and the value of the cache is a
+// GRU hidden layer output"; the frame's surviving rows form one
+// contiguous block.  Semantics: the oracle's stream-order loop
+// (SURVEY 8(c)); the GPU reproduces it bit-exactly with a deterministic
+// "first occupant = lowest query index" rule:
+//
+//   k_qprobe  read-only probe of the LM-query cache (entries from earlier
+//             calls only: nothing is inserted yet) + validation
+//   k_qclaim  not-found keys: CAS-insert (or find the concurrent insert),
+//             atomicMin(owner, q)
+//   k_hprobe  owner == q -> first occurrence (non-QHIT); else duplicate.
+//             First occurrences probe the hidden cache read-only
+//   k_hclaim  not-found hidden keys: CAS-insert / find + atomicMin(owner, q)
+//   k_scan    owner == q -> MISS else SHIT; one decoupled look-back scan
+//             over (non-QHIT, MISS) flags -> dense handles and slots
+//   k_commit  records, cache values, GRU row list, scoring list
+//   k_final   QHIT results, outcomes, counters, allocation cursors
+//
+// Kernel boundaries separate "claim" from "read owner", which is what makes
+// the outcome independent of thread scheduling.
+#include "rnnlm_impl.cuh"
+
+namespace rnnlm_dev {
+
+__device__ __forceinline__ unsigned long long vload64(const unsigned long long *p) {
+  return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+
+__device__ __forceinline__ uint32_t hhome(unsigned long long codehash, uint32_t w, uint32_t mask) {
+  return (uint32_t)(mix64(codehash ^ ((unsigned long long)w * 0x9E3779B97F4A7C15ull)) & mask);
+}
+
+// Full code equality of the states in global rows a and b (never a hash).
+__device__ bool code_equal(const Params &P, size_t a, size_t b) {
+  if (a == b) return true;
+  const uint4 *pa, *pb;
+  uint32_t n16;
+  if (P.key_mode == RNNLM_KEY_OFF) {
+    pa = reinterpret_cast<const uint4 *>(P.state + a * P.H);
+    pb = reinterpret_cast<const uint4 *>(P.state + b * P.H);
+    n16 = P.H / 4;
+  } else {
+    pa = reinterpret_cast<const uint4 *>(P.codes + a * P.cstride);
+    pb = reinterpret_cast<const uint4 *>(P.codes + b * P.cstride);
+    n16 = P.cstride / 16;
+  }
+  for (uint32_t i = 0; i < n16; ++i) {
+    const uint4 x = pa[i], y = pb[i];
+    if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w) return false;
+  }
+  return true;
+}
+
+// Hidden-cache key match: same word and equal code of the reference state.
+__device__ __forceinline__ bool hkey_match(const Params &P, unsigned long long tag, uint32_t s,
+                                           uint32_t w, uint32_t ps, unsigned long long hh) {
+  if ((uint32_t)tag != w) return false;
+  const size_t base = (size_t)s * P.cap;
+  const uint32_t ref = (uint32_t)(tag >> 32);
+  if (P.codehash[base + ref] != hh) return false;
+  return code_equal(P, base + ref, base + ps);
+}
+
+// ---- (a2) probe -------------------------------------------------------------
+__global__ void k_qprobe(Params P, CallArgs A, uint32_t ntiles) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < ntiles) P.tile_status[q] = 0ull;
+  if (q == 0) *P.tile_ticket = 0u;
+  if (q >= A.n) return;
+  const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
+  int err = 0;
+  if (s >= P.S) err = RNNLM_E_INVALID_ARG;
+  else if (q > 0 && A.session[q - 1] > s) err = RNNLM_E_INVALID_ARG;
+  else if (w >= P.V) err = RNNLM_E_VOCAB;
+  else if (p >= P.ctr[s].next_handle) err = RNNLM_E_HISTORY;
+  if (q > 0 && A.session[q - 1] > s) P.counts[2] = A.epoch;   // batch not sorted by session
+  if (err) {
+    P.st[q] = ST_INVALID;
+    latch(P.sticky, err);
+    return;
+  }
+  if (!P.cache) {
+    P.st[q] = ST_MISS_NC;
+    P.pslot[q] = P.rec[(size_t)s * P.cap + p].slot;
+    return;
+  }
+  const unsigned long long key = ((unsigned long long)p << 32) | w;
+  const size_t base = (size_t)s * (P.qmask + 1);
+  uint32_t idx = (uint32_t)(mix64(key) & P.qmask);
+  for (;;) {
+    const unsigned long long t = P.qtab[base + idx].tag;
+    if (t == key) { P.st[q] = ST_QHIT_OLD; P.qent[q] = idx; return; }
+    if (t == TAG_EMPTY) { P.st[q] = ST_QNEED; P.qent[q] = idx; return; }
+    idx = (idx + 1) & P.qmask;
+  }
+}
+
+// ---- (a2) claim -------------------------------------------------------------
+__global__ void k_qclaim(Params P, CallArgs A) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= A.n || P.st[q] != ST_QNEED || P.counts[2] == A.epoch) return;
+  const uint32_t s = A.session[q];
+  const unsigned long long key = ((unsigned long long)A.parent[q] << 32) | A.word[q];
+  const size_t base = (size_t)s * (P.qmask + 1);
+  uint32_t idx = P.qent[q];                 // slots before the hint hold other keys
+  for (;;) {
+    unsigned long long t = vload64(&P.qtab[base + idx].tag);
+    if (t == TAG_EMPTY) t = atomicCAS(&P.qtab[base + idx].tag, TAG_EMPTY, key);
+    if (t == TAG_EMPTY || t == key) break;
+    idx = (idx + 1) & P.qmask;
+  }
+  atomicMin(&P.qowner[base + idx], q);
+  P.qent[q] = idx;
+}
+
+// ---- (a3) probe ------------------------------------------------------------
+__global__ void k_hprobe(Params P, CallArgs A) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= A.n || P.st[q] != ST_QNEED || P.counts[2] == A.epoch) return;
+  const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
+  const uint32_t o = P.qowner[(size_t)s * (P.qmask + 1) + P.qent[q]];
+  if (o != q) { P.st[q] = ST_QHIT_NEW; P.aux[q] = o; return; }
+  const size_t cb = (size_t)s * P.cap;
+  const uint32_t ps = P.rec[cb + p].slot;
+  P.pslot[q] = ps;
+  const unsigned long long hh = P.codehash[cb + ps];
+  const size_t base = (size_t)s * (P.hmask + 1);
+  uint32_t idx = hhome(hh, w, P.hmask);
+  for (;;) {
+    const unsigned long long t = P.htab[base + idx].tag;
+    if (t == TAG_EMPTY) { P.st[q] = ST_HNEED; P.hent[q] = idx; return; }
+    if (hkey_match(P, t, s, w, ps, hh)) {
+      P.st[q] = ST_SHIT_OLD;
+      P.hent[q] = idx;
+      P.cslot[q] = P.htab[base + idx].slot;
+      return;
+    }
+    idx = (idx + 1) & P.hmask;
+  }
+}
+
+// ---- (a3) claim ------------------------------------------------------------
+__global__ void k_hclaim(Params P, CallArgs A) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= A.n || P.st[q] != ST_HNEED || P.counts[2] == A.epoch) return;
+  const uint32_t s = A.session[q], w = A.word[q];
+  const uint32_t ps = P.pslot[q];
+  const unsigned long long hh = P.codehash[(size_t)s * P.cap + ps];
+  const unsigned long long mine = ((unsigned long long)ps << 32) | w;
+  const size_t base = (size_t)s * (P.hmask + 1);
+  uint32_t idx = P.hent[q];
+  for (;;) {
+    unsigned long long t = vload64(&P.htab[base + idx].tag);
+    if (t == TAG_EMPTY) {
+      t = atomicCAS(&P.htab[base + idx].tag, TAG_EMPTY, mine);
+      if (t == TAG_EMPTY) break;
+    }
+    if (hkey_match(P, t, s, w, ps, hh)) break;
+    idx = (idx + 1) & P.hmask;
+  }
+  atomicMin(&P.howner[base + idx], q);
+  P.hent[q] = idx;
+}
+
+// ---- (a4) decoupled look-back scan over (non-QHIT, MISS) ------------------
+constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 4;
+static_assert(SCAN_THREADS * SCAN_ITEMS == rnnlm_host::SCAN_TILE, "tile");
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62;
+
+__device__ __forceinline__ unsigned long long to_status(unsigned long long v, unsigned long long f) {
+  // v = (nonq << 32 | miss) -> f | nonq << 31 | miss (31-bit fields)
+  return f | ((v >> 32) << 31) | (v & 0x7FFFFFFFull);
+}
+__device__ __forceinline__ unsigned long long from_status(unsigned long long x) {
+  return (((x >> 31) & 0x7FFFFFFFull) << 32) | (x & 0x7FFFFFFFull);
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_warp[SCAN_THREADS / 32];
+  __shared__ unsigned long long s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(P.tile_ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const bool bad = P.counts[2] == A.epoch;
+  const uint32_t q0 = tile * rnnlm_host::SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  unsigned long long v[SCAN_ITEMS];
+  unsigned long long tsum = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    const uint32_t q = q0 + i;
+    uint32_t nonq = 0, miss = 0;
+    if (q < A.n) {
+      uint32_t st = P.st[q];
+      if (bad) {
+        if (st != ST_INVALID) latch(P.sticky, RNNLM_E_INVALID_ARG);
+        st = ST_INVALID;
+      } else if (st == ST_HNEED) {
+        const uint32_t o = P.howner[(size_t)A.session[q] * (P.hmask + 1) + P.hent[q]];
+        st = (o == q) ? ST_MISS : ST_SHIT_NEW;
+        P.aux[q] = o;
+      }
+      P.st[q] = st;
+      nonq = (st == ST_SHIT_OLD || st == ST_SHIT_NEW || st == ST_MISS || st == ST_MISS_NC);
+      miss = (st == ST_MISS || st == ST_MISS_NC);
+    }
+    v[i] = ((unsigned long long)nonq << 32) | miss;
+    tsum += v[i];
+  }
+  // block-exclusive prefix of tsum
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long inc = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    for (int i = 0; i < SCAN_THREADS / 32; ++i) {
+      const unsigned long long t = s_warp[i];
+      s_warp[i] = run;
+      run += t;
+    }
+    const unsigned long long agg = run;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      atomicExch(&P.tile_status[0], to_status(agg, ST_INC));
+    } else {
+      atomicExch(&P.tile_status[tile], to_status(agg, ST_AGG));
+      int j = (int)tile - 1;
+      for (;;) {
+        unsigned long long x;
+        do { x = vload64(&P.tile_status[j]); } while ((x >> 62) == 0);
+        excl += from_status(x);
+        if ((x >> 62) == 2) break;
+        --j;
+      }
+      atomicExch(&P.tile_status[tile], to_status(excl + agg, ST_INC));
+    }
+    s_prefix = excl;
+  }
+  __syncthreads();
+  unsigned long long run = s_prefix + s_warp[wid] + (inc - tsum);
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    const uint32_t q = q0 + i;
+    if (q < A.n) {
+      P.excl_nonq[q] = (uint32_t)(run >> 32);
+      P.excl_miss[q] = (uint32_t)run;
+      const uint32_t s = A.session[q];
+      if (!bad && s < P.S && (q == 0 || A.session[q - 1] != s)) {
+        P.seg_excl_nonq[s] = (uint32_t)(run >> 32);
+        P.seg_excl_miss[s] = (uint32_t)run;
+      }
+      if (q == A.n - 1) {
+        const unsigned long long tot = run + v[i];
+        P.counts[0] = (uint32_t)(tot >> 32);
+        P.counts[1] = (uint32_t)tot;
+      }
+    }
+    run += v[i];
+  }
+}
+
+// ---- (a4) commit: handles, slots, records, cache values, work lists -------
+__global__ void k_commit(Params P, CallArgs A) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= A.n) return;
+  const uint32_t st = P.st[q];
+  const uint32_t s = A.session[q];
+  const bool bad = P.counts[2] == A.epoch;
+  const bool nonq = (st == ST_SHIT_OLD || st == ST_SHIT_NEW || st == ST_MISS || st == ST_MISS_NC);
+  const bool miss = (st == ST_MISS || st == ST_MISS_NC);
+  if (!bad && s < P.S && (q == A.n - 1 || A.session[q + 1] != s)) {   // last of the session
+    P.seg_cnt_nonq[s] = P.excl_nonq[q] + (nonq ? 1u : 0u) - P.seg_excl_nonq[s];
+    P.seg_cnt_miss[s] = P.excl_miss[q] + (miss ? 1u : 0u) - P.seg_excl_miss[s];
+  }
+  if (!nonq) return;
+  const uint32_t w = A.word[q], p = A.parent[q];
+  const size_t cb = (size_t)s * P.cap;
+  const uint32_t h = P.ctr[s].next_handle + (P.excl_nonq[q] - P.seg_excl_nonq[s]);
+  const size_t qb = (size_t)s * (P.qmask + 1);
+  const uint32_t r = P.excl_miss[q];
+  P.nonq_list[P.excl_nonq[q]] = q;
+  if (h >= P.cap) {                                    // out of history handles
+    P.st[q] = ST_INVALID;
+    latch(P.sticky, RNNLM_E_CAPACITY);
+    A.score[q] = __int_as_float(0x7fc00000);
+    A.child[q] = NONE;
+    if (P.cache) { P.qtab[qb + P.qent[q]].child = NONE; P.qtab[qb + P.qent[q]].score = __int_as_float(0x7fc00000); }
+    if (miss) P.row_dst[r] = NONE;
+    return;
+  }
+  uint32_t sl;
+  if (miss) {
+    sl = P.ctr[s].next_slot + (r - P.seg_excl_miss[s]);
+    P.row_src[r] = (uint32_t)(cb + P.pslot[q]);
+    P.row_dst[r] = (uint32_t)(cb + sl);
+    P.row_word[r] = w;
+    if (P.cache) P.htab[(size_t)s * (P.hmask + 1) + P.hent[q]].slot = sl;
+  } else if (st == ST_SHIT_OLD) {
+    sl = P.cslot[q];
+  } else {                                             // SHIT_NEW: the owner's new slot
+    const uint32_t o = P.aux[q];
+    sl = P.ctr[s].next_slot + (P.excl_miss[o] - P.seg_excl_miss[s]);
+  }
+  P.cslot[q] = sl;
+  const Rec pr = P.rec[cb + p];
+  Rec nr;
+  nr.slot = sl;
+  for (int j = 0; j < MAX_CTX; ++j) nr.ctx[j] = NONE;
+  if (P.N > 1) {                                       // last N-1 words of (ctx o w)
+    nr.ctx[0] = w;
+    for (uint32_t j = 1; j + 1 < P.N; ++j) nr.ctx[j] = pr.ctx[j - 1];
+  }
+  P.rec[cb + h] = nr;
+  A.child[q] = h;
+  if (P.cache) P.qtab[qb + P.qent[q]].child = h;
+}
+
+// ---- (a7) final: QHIT results, outcomes, counters, cursors -----------------
+__global__ void k_final(Params P, CallArgs A) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = q < A.n;
+  uint32_t st = active ? P.st[q] : ST_INVALID;
+  const uint32_t s = active ? A.session[q] : NONE;
+  uint8_t oc = RNNLM_INVALID;
+  if (active) {
+    if (st == ST_QHIT_OLD) {
+      const rnnlm_dev::QEntry e = P.qtab[(size_t)s * (P.qmask + 1) + P.qent[q]];
+      A.score[q] = e.score;
+      A.child[q] = e.child;
+      if (e.child == NONE) st = ST_INVALID; else oc = RNNLM_QHIT;   // entry of a failed query
+    } else if (st == ST_QHIT_NEW) {
+      const uint32_t o = P.aux[q];
+      const uint32_t c = A.child[o];
+      A.score[q] = A.score[o];
+      A.child[q] = c;
+      if (c == NONE) st = ST_INVALID; else oc = RNNLM_QHIT;
+    } else if (st == ST_SHIT_OLD || st == ST_SHIT_NEW) {
+      oc = RNNLM_SHIT;
+    } else if (st == ST_MISS || st == ST_MISS_NC) {
+      oc = RNNLM_MISS;
+    }
+    if (st == ST_INVALID) {
+      A.score[q] = __int_as_float(0x7fc00000);
+      A.child[q] = NONE;
+    }
+    if (A.outcome) A.outcome[q] = oc;
+  }
+  const bool valid = st != ST_INVALID;
+  const uint32_t key = valid ? s : NONE;
+  const uint32_t mask = __match_any_sync(0xffffffffu, key);
+  const uint32_t c_tot = valid;
+  const uint32_t c_qh = valid && (st == ST_QHIT_OLD || st == ST_QHIT_NEW);
+  const uint32_t c_hl = valid && P.cache && !c_qh;
+  const uint32_t c_hh = valid && (st == ST_SHIT_OLD || st == ST_SHIT_NEW);
+  const uint32_t c_gru = valid && (st == ST_MISS || st == ST_MISS_NC);
+  const uint32_t t_tot = __reduce_add_sync(mask, c_tot), t_qh = __reduce_add_sync(mask, c_qh);
+  const uint32_t t_hl = __reduce_add_sync(mask, c_hl), t_hh = __reduce_add_sync(mask, c_hh);
+  const uint32_t t_gru = __reduce_add_sync(mask, c_gru);
+  if (key != NONE && (threadIdx.x & 31) == (uint32_t)(__ffs(mask) - 1)) {
+    SessCtr *c = &P.ctr[key];
+    if (t_tot) atomicAdd(&c->total, (unsigned long long)t_tot);
+    if (t_qh) atomicAdd(&c->qhits, (unsigned long long)t_qh);
+    if (t_hl) atomicAdd(&c->hlookups, (unsigned long long)t_hl);
+    if (t_hh) atomicAdd(&c->hhits, (unsigned long long)t_hh);
+    if (t_gru) atomicAdd(&c->gru, (unsigned long long)t_gru);
+  }
+  if (active && P.counts[2] != A.epoch && s < P.S && (q == A.n - 1 || A.session[q + 1] != s)) {
+    SessCtr *c = &P.ctr[s];
+    const uint32_t nh = c->next_handle + P.seg_cnt_nonq[s];
+    const uint32_t ns = c->next_slot + P.seg_cnt_miss[s];
+    c->next_handle = nh < P.cap ? nh : P.cap;
+    c->next_slot = ns < P.cap ? ns : P.cap;
+  }
+}
+
+// ---- inspection / plumbing -------------------------------------------------
+__global__ void k_read_states(Params P, uint32_t sess, uint32_t n, const uint32_t *__restrict__ h,
+                              float *__restrict__ out) {
+  const uint32_t i = blockIdx.x;
+  if (i >= n) return;
+  const uint32_t hd = h[i];
+  const bool ok = sess < P.S && hd < P.ctr[sess].next_handle;
+  const size_t row = ok ? (size_t)sess * P.cap + P.rec[(size_t)sess * P.cap + hd].slot : 0;
+  for (uint32_t j = threadIdx.x; j < P.H; j += blockDim.x)
+    out[(size_t)i * P.H + j] = ok ? P.state[row * P.H + j] : __int_as_float(0x7fc00000);
+}
+
+__global__ void k_read_slots(Params P, uint32_t sess, uint32_t n, const uint32_t *__restrict__ h,
+                             uint32_t *__restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t hd = h[i];
+  const bool ok = sess < P.S && hd < P.ctr[sess].next_handle;
+  out[i] = ok ? P.rec[(size_t)sess * P.cap + hd].slot : NONE;
+}
+
+__global__ void k_resolve_parents(uint32_t n, const int64_t *__restrict__ ref,
+                                  const uint32_t *__restrict__ log, uint32_t *__restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = ref[i];
+  out[i] = r < 0 ? 0u : log[r];
+}
+
+}  // namespace rnnlm_dev
+
+namespace rnnlm_host {
+using namespace rnnlm_dev;
+
+static inline uint32_t nblk(uint32_t n, uint32_t t) { return (n + t - 1) / t; }
+
+int launch_cache_front(const Params &P, const CallArgs &A, cudaStream_t s) {
+  const uint32_t ntiles = nblk(A.n, SCAN_TILE);
+  int k = 0;
+  k_qprobe<<<nblk(A.n, 256), 256, 0, s>>>(P, A, ntiles); ++k;
+  if (P.cache) {
+    k_qclaim<<<nblk(A.n, 256), 256, 0, s>>>(P, A); ++k;
+    k_hprobe<<<nblk(A.n, 256), 256, 0, s>>>(P, A); ++k;
+    k_hclaim<<<nblk(A.n, 256), 256, 0, s>>>(P, A); ++k;
+  }
+  k_scan<<<ntiles, SCAN_THREADS, 0, s>>>(P, A); ++k;
+  return k;
+}
+
+int launch_commit(const Params &P, const CallArgs &A, cudaStream_t s) {
+  k_commit<<<nblk(A.n, 256), 256, 0, s>>>(P, A);
+  return 1;
+}
+
+int launch_final(const Params &P, const CallArgs &A, cudaStream_t s) {
+  k_final<<<nblk(A.n, 256), 256, 0, s>>>(P, A);
+  return 1;
+}
+
+int launch_read_states(const Params &P, uint32_t sess, uint32_t n, const uint32_t *h, float *out,
+                       cudaStream_t s) {
+  if (!n) return 0;
+  k_read_states<<<n, 128, 0, s>>>(P, sess, n, h, out);
+  return 1;
+}
+
+int launch_read_slots(const Params &P, uint32_t sess, uint32_t n, const uint32_t *h, uint32_t *out,
+                      cudaStream_t s) {
+  if (!n) return 0;
+  k_read_slots<<<nblk(n, 256), 256, 0, s>>>(P, sess, n, h, out);
+  return 1;
+}
+
+int launch_resolve_parents(uint32_t n, const int64_t *ref, const uint32_t *log, uint32_t *out,
+                           cudaStream_t s) {
+  if (!n) return 0;
+  k_resolve_parents<<<nblk(n, 256), 256, 0, s>>>(n, ref, log, out);
+  return 1;
+}
+}  // namespace rnnlm_host

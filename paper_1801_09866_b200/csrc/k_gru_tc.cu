@@ -1,0 +1,589 @@
+// k_gru_tc.cu -- step (a5), BF16 tensor-core path on sm_100a (tcgen05 + TMEM + TMA).
+//
+// The GRU gate contraction of the frame's MISS rows (the
+// frame's (h || x) rows form one block) is a real dense contraction:
+// [Q, E+H] x [E+H, 3H] for Q misses (Chung form, reading 1), executed as
+//
+//   phase 1  A = [x | h] rows GATHERED on the fly (x = E[word] bf16, h = bf16
+//            shadow of the parent state) by 4 producer warps with cp.async
+//            16-byte copies straight into the 128B-swizzled UMMA layout;
+//            B = gate-interleaved weights W1 [H/64 x 192 rows][E+H] bf16 via
+//            TMA (per 64-unit block: 64 rows z, 64 rows r, 64 rows h; the h
+//            rows are zero on the recurrent half, so those K chunks issue
+//            N = 128 MMAs and load only the z/r rows).  Tile 128 x 192, fp32
+//            accumulators in TMEM (two buffers of 256 columns: the epilogue of
+//            tile i overlaps the MMAs of tile i+1).  Epilogue: z = s(.+bz),
+//            r = s(.+br) -> r.h (bf16, phase-2 A operand), Wh x + bh (fp32).
+//   phase 2  A = r.h rows via TMA, B = Uh [H][H] bf16 via TMA, tile 128 x 256;
+//            epilogue: c = tanh(Wh x + bh + Uh(r.h)), h' = (1-z) h + z c, the
+//            new fp32 state and its bf16 shadow.
+//
+// Both kernels are persistent (grid <= #SMs), warp-specialised: producer(s),
+// one MMA-issuing thread (tcgen05.mma.cta_group::1.kind::f16, M = 128), four
+// epilogue warps (tcgen05.ld.32x32b, one TMEM lane = one row per thread).
+// Pipelines are mbarrier rings (full / empty per smem stage, full / empty per
+// TMEM accumulator).  Rows >= Q are zero-filled / discarded.
+#include <cuda.h>
+
+#include <cstring>
+#include <vector>
+
+#include "rnnlm_impl.cuh"
+
+namespace rnnlm_tc {
+using namespace rnnlm_dev;
+
+constexpr int BM = 128;          // UMMA M (rows per tile)
+constexpr int BK = 64;           // K elements per smem stage (= one 128-byte swizzle atom)
+constexpr int N1 = 192;          // phase-1 tile N (z, r, h of 64 units)
+constexpr int N1H = 128;         // phase-1 N on recurrent K chunks (z, r only)
+constexpr int N2 = 256;          // phase-2 tile N (units)
+constexpr int ST1 = 4;           // phase-1 smem stages
+constexpr int ST2 = 4;           // phase-2 smem stages
+constexpr int A_BYTES = BM * BK * 2;          // 16 KB
+constexpr int B1_BYTES = N1 * BK * 2;         // 24 KB
+constexpr int B2_BYTES = N2 * BK * 2;         // 32 KB
+constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 columns
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *b) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+// D[tmem] (+)= A[smem] . B[smem]^T, both K-major, bf16 -> fp32, M = 128.
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// 16 consecutive fp32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row atoms of
+// 1024 bytes (SBO), version 1 (sm100).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// Instruction descriptor: kind::f16, A = B = BF16, D = F32, K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float sigm(float a) { return 1.0f / (1.0f + __expf(-a)); }
+
+struct TcArgs {
+  uint32_t E, H, nub;
+  const __nv_bfloat16 *emb16;
+  const __nv_bfloat16 *state16;
+  const float *state;
+  const float *b1;                 // [nub][3][64]
+  __nv_bfloat16 *state16_out;
+  float *state_out;
+  const uint32_t *row_src, *row_dst, *row_word, *counts;
+  float *g_z, *g_wxb;
+  __nv_bfloat16 *g_rh16;
+};
+
+// =============================================================== phase 1
+// warps 0-3: A gather producers (warp 0 lane 0 also issues the B TMA)
+// warp 4:    TMEM allocation + MMA issue
+// warps 5-8: epilogue (TMEM lane quarter = warp % 4)
+constexpr int P1_THREADS = 9 * 32;
+
+__global__ void __launch_bounds__(P1_THREADS, 1)
+    k_gru1_tc(const __grid_constant__ CUtensorMap map_w1x, const __grid_constant__ CUtensorMap map_w1h,
+              TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = smem;                                   // ST1 x 16 KB
+  uint8_t *sB = smem + ST1 * A_BYTES;                   // ST1 x 24 KB
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + ST1 * B1_BYTES);
+  uint64_t *empty = full + ST1;
+  uint64_t *tfull = empty + ST1;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_base_sm = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t Q = a.counts[1];
+  const uint32_t mt = (Q + BM - 1) / BM;
+  const uint32_t ntiles = mt * a.nub;
+  const uint32_t kx = a.E / BK, kh = a.H / BK, KC = kx + kh;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST1; ++s) { mbar_init(&full[s], 128 + 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&map_w1x);
+    prefetch_map(&map_w1h);
+  }
+  if (warp == 4) tmem_alloc(tmem_base_sm, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_sm;
+
+  if (warp < 4) {
+    // ------------------------------------------------ producers
+    const int p = threadIdx.x;                          // row within the tile
+    uint32_t stage = 0, phase = 0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const uint32_t m0 = (tile / a.nub) * BM, ub = tile % a.nub;
+      const uint32_t row = m0 + p;
+      const bool valid = row < Q;
+      const __nv_bfloat16 *xrow = valid ? a.emb16 + (size_t)a.row_word[row] * a.E : a.emb16;
+      const __nv_bfloat16 *hrow = valid ? a.state16 + (size_t)a.row_src[row] * a.H : a.state16;
+      const uint32_t nbytes = valid ? 16u : 0u;
+      for (uint32_t kc = 0; kc < KC; ++kc) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (p == 0) {
+          const uint32_t dstB = smem_u32(sB + stage * B1_BYTES);
+          if (kc < kx) {
+            mbar_expect_tx(&full[stage], N1 * BK * 2);
+            tma_load_2d(dstB, &map_w1x, &full[stage], (int)(kc * BK), (int)(ub * N1));
+          } else {
+            mbar_expect_tx(&full[stage], N1H * BK * 2);
+            tma_load_2d(dstB, &map_w1h, &full[stage], (int)(kc * BK), (int)(ub * N1));
+          }
+        }
+        const __nv_bfloat16 *src = kc < kx ? xrow + kc * BK : hrow + (kc - kx) * BK;
+        const uint32_t dst = smem_u32(sA + stage * A_BYTES) + p * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) cp_async16(dst + ((c ^ (p & 7)) << 4), src + c * 8, nbytes);
+        cp_async_mbar_arrive(&full[stage]);
+        mbar_arrive(&full[stage]);
+        if (++stage == ST1) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------------ MMA issuer
+    uint32_t stage = 0, phase = 0, it = 0;
+    const uint32_t id_x = idesc_bf16(BM, N1), id_h = idesc_bf16(BM, N1H);
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const uint32_t acc = it & 1;
+      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t tm = tmem_base + acc * 256;
+      for (uint32_t kc = 0; kc < KC; ++kc) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        fence_proxy_async();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B1_BYTES);
+          const uint32_t id = kc < kx ? id_x : id_h;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+          umma_commit(&empty[stage]);
+          if (kc == KC - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == ST1) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue
+    const int q = warp & 3;                             // TMEM lane quarter
+    const int r_in = q * 32 + lane;
+    uint32_t it = 0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const uint32_t acc = it & 1;
+      const uint32_t m0 = (tile / a.nub) * BM, ub = tile % a.nub;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t row = m0 + r_in;
+      const bool valid = row < Q;
+      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * 64;
+      const float *bb = a.b1 + (size_t)ub * 192;
+      const size_t o = (size_t)row * a.H + ub * 64;
+#pragma unroll 1
+      for (int g = 0; g < 4; ++g) {
+        float vz[16], vr[16], vx[16];
+        tmem_ld16(tbase + g * 16, vz);
+        tmem_ld16(tbase + 64 + g * 16, vr);
+        tmem_ld16(tbase + 128 + g * 16, vx);
+        tmem_ld_wait();
+        if (g == 3) {                                   // accumulator drained
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        if (!valid) continue;
+        float z[16], rh[16], wx[16];
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+          const float4 hv = *reinterpret_cast<const float4 *>(hp + g * 16 + j);
+          const float hh[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int u = g * 16 + j + t;
+            z[j + t] = sigm(vz[j + t] + bb[u]);
+            rh[j + t] = sigm(vr[j + t] + bb[64 + u]) * hh[t];
+            wx[j + t] = vx[j + t] + bb[128 + u];
+          }
+        }
+        float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
+        float4 *gw = reinterpret_cast<float4 *>(a.g_wxb + o + g * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          gz[j] = make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
+          gw[j] = make_float4(wx[4 * j], wx[4 * j + 1], wx[4 * j + 2], wx[4 * j + 3]);
+        }
+        uint4 pk[2];
+        uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162 t2 = __floats2bfloat162_rn(rh[2 * j], rh[2 * j + 1]);
+          pw[j] = *reinterpret_cast<uint32_t *>(&t2);
+        }
+        uint4 *gr = reinterpret_cast<uint4 *>(a.g_rh16 + o + g * 16);
+        gr[0] = pk[0];
+        gr[1] = pk[1];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// =============================================================== phase 2
+// warp 0: TMA producer; warp 1: TMEM alloc + MMA; warps 2-5: epilogue
+constexpr int P2_THREADS = 6 * 32;
+
+__global__ void __launch_bounds__(P2_THREADS, 1)
+    k_gru2_tc(const __grid_constant__ CUtensorMap map_a2, const __grid_constant__ CUtensorMap map_w2,
+              TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + ST2 * A_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + ST2 * B2_BYTES);
+  uint64_t *empty = full + ST2;
+  uint64_t *tfull = empty + ST2;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_base_sm = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t Q = a.counts[1];
+  const uint32_t mt = (Q + BM - 1) / BM;
+  const uint32_t nt = a.H / N2;
+  const uint32_t ntiles = mt * nt;
+  const uint32_t KC = a.H / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&map_a2);
+    prefetch_map(&map_w2);
+  }
+  if (warp == 1) tmem_alloc(tmem_base_sm, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_sm;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t m0 = (tile / nt) * BM, n0 = (tile % nt) * N2;
+        for (uint32_t kc = 0; kc < KC; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], A_BYTES + B2_BYTES);
+          tma_load_2d(smem_u32(sA + stage * A_BYTES), &map_a2, &full[stage], (int)(kc * BK), (int)m0);
+          tma_load_2d(smem_u32(sB + stage * B2_BYTES), &map_w2, &full[stage], (int)(kc * BK), (int)n0);
+          if (++stage == ST2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    uint32_t stage = 0, phase = 0, it = 0;
+    const uint32_t id = idesc_bf16(BM, N2);
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const uint32_t acc = it & 1;
+      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t tm = tmem_base + acc * 256;
+      for (uint32_t kc = 0; kc < KC; ++kc) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B2_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+          umma_commit(&empty[stage]);
+          if (kc == KC - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == ST2) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int r_in = q * 32 + lane;
+    uint32_t it = 0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const uint32_t acc = it & 1;
+      const uint32_t m0 = (tile / nt) * BM, n0 = (tile % nt) * N2;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t row = m0 + r_in;
+      const bool valid = row < Q;
+      const uint32_t dst = valid ? a.row_dst[row] : NONE;
+      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + n0;
+      const size_t o = (size_t)row * a.H + n0;
+#pragma unroll 1
+      for (int g = 0; g < N2 / 16; ++g) {
+        float vu[16];
+        tmem_ld16(tbase + g * 16, vu);
+        tmem_ld_wait();
+        if (g == N2 / 16 - 1) {
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        if (dst == NONE) continue;
+        float hn[16];
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+          const float4 z4 = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + j);
+          const float4 w4 = *reinterpret_cast<const float4 *>(a.g_wxb + o + g * 16 + j);
+          const float4 h4 = *reinterpret_cast<const float4 *>(hp + g * 16 + j);
+          const float zz[4] = {z4.x, z4.y, z4.z, z4.w}, ww[4] = {w4.x, w4.y, w4.z, w4.w};
+          const float hh[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float c = tanhf(ww[t] + vu[j + t]);
+            hn[j + t] = (1.0f - zz[t]) * hh[t] + zz[t] * c;
+          }
+        }
+        float4 *so = reinterpret_cast<float4 *>(a.state_out + (size_t)dst * a.H + n0 + g * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) so[j] = make_float4(hn[4 * j], hn[4 * j + 1], hn[4 * j + 2], hn[4 * j + 3]);
+        uint4 pk[2];
+        uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162 t2 = __floats2bfloat162_rn(hn[2 * j], hn[2 * j + 1]);
+          pw[j] = *reinterpret_cast<uint32_t *>(&t2);
+        }
+        uint4 *s16 = reinterpret_cast<uint4 *>(a.state16_out + (size_t)dst * a.H + n0 + g * 16);
+        s16[0] = pk[0];
+        s16[1] = pk[1];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+constexpr size_t SMEM1 = 1024 + ST1 * (A_BYTES + B1_BYTES) + 256;
+constexpr size_t SMEM2 = 1024 + ST2 * (A_BYTES + B2_BYTES) + 256;
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct TcState {
+  uint32_t E = 0, H = 0, nub = 0, bmax = 0;
+  __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr;
+  float *b1 = nullptr;
+  CUtensorMap map_w1x, map_w1h, map_w2, map_a2;
+  bool bound = false;
+};
+
+static EncodeTiled get_encode() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap *m, void *base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+  EncodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace rnnlm_tc
+
+namespace rnnlm_host {
+using namespace rnnlm_tc;
+
+int gru_tc_supported(uint32_t E, uint32_t H) {
+  return E % 64 == 0 && H % N2 == 0 && E >= 64 && H >= N2;
+}
+
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_out) {
+  *state_out = nullptr;
+  TcState *t = new TcState;
+  t->E = E; t->H = H; t->nub = H / 64;
+  const size_t K1 = E + H, R1 = (size_t)t->nub * N1;
+  std::vector<__nv_bfloat16> w1(R1 * K1, __float2bfloat16_rn(0.0f)), w2((size_t)H * H);
+  std::vector<float> b1((size_t)t->nub * 192);
+  const float *Wg[3] = {w->Wz, w->Wr, w->Wh};
+  const float *Ug[2] = {w->Uz, w->Ur};
+  const float *bg[3] = {w->bz, w->br, w->bh};
+  for (size_t u = 0; u < H; ++u) {
+    const size_t ub = u / 64, uu = u % 64;
+    for (int g = 0; g < 3; ++g) {
+      __nv_bfloat16 *row = w1.data() + (ub * N1 + g * 64 + uu) * K1;
+      for (size_t k = 0; k < E; ++k) row[k] = __float2bfloat16_rn(Wg[g][u * E + k]);
+      if (g < 2)
+        for (size_t k = 0; k < H; ++k) row[E + k] = __float2bfloat16_rn(Ug[g][u * H + k]);
+      b1[ub * 192 + g * 64 + uu] = bg[g][u];
+    }
+    for (size_t k = 0; k < H; ++k) w2[u * H + k] = __float2bfloat16_rn(w->Uh[u * H + k]);
+  }
+  bool ok = cudaMalloc(&t->w1, w1.size() * 2) == cudaSuccess &&
+            cudaMalloc(&t->w2, w2.size() * 2) == cudaSuccess &&
+            cudaMalloc(&t->b1, b1.size() * 4) == cudaSuccess;
+  ok = ok && cudaMemcpy(t->w1, w1.data(), w1.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && cudaMemcpy(t->w2, w2.data(), w2.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && cudaMemcpy(t->b1, b1.data(), b1.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && make_map(&t->map_w1x, t->w1, K1, R1, N1) && make_map(&t->map_w1h, t->w1, K1, R1, N1H) &&
+       make_map(&t->map_w2, t->w2, H, H, N2);
+  ok = ok && cudaFuncSetAttribute(k_gru1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM1) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2) == cudaSuccess;
+  *state_out = t;
+  if (!ok) {
+    (void)cudaGetLastError();
+    return -1;
+  }
+  return 0;
+}
+
+// The phase-2 A operand map needs the r.h scratch; bound once per engine.
+int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax) {
+  TcState *t = static_cast<TcState *>(state);
+  t->rh16 = rh16;
+  t->bmax = bmax;
+  t->bound = make_map(&t->map_a2, rh16, t->H, bmax, BM);
+  return t->bound ? 0 : -1;
+}
+
+void gru_tc_release(void *state) {
+  TcState *t = static_cast<TcState *>(state);
+  if (!t) return;
+  cudaFree(t->w1);
+  cudaFree(t->w2);
+  cudaFree(t->b1);
+  delete t;
+}
+
+int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, cudaStream_t s) {
+  TcState *t = static_cast<TcState *>(state);
+  if (!max_rows || !t || !t->bound) return 0;
+  TcArgs a;
+  a.E = P.E; a.H = P.H; a.nub = t->nub;
+  a.emb16 = P.emb16; a.state16 = P.state16; a.state = P.state; a.b1 = t->b1;
+  a.state16_out = P.state16; a.state_out = P.state;
+  a.row_src = P.row_src; a.row_dst = P.row_dst; a.row_word = P.row_word; a.counts = P.counts;
+  a.g_z = P.g_z; a.g_wxb = P.g_wxb; a.g_rh16 = P.g_rh16;
+  const uint32_t mt = (max_rows + BM - 1) / BM;
+  uint32_t g1 = mt * t->nub, g2 = mt * (P.H / N2);
+  if (g1 > (uint32_t)num_sms) g1 = num_sms;
+  if (g2 > (uint32_t)num_sms) g2 = num_sms;
+  k_gru1_tc<<<g1, P1_THREADS, SMEM1, s>>>(t->map_w1x, t->map_w1h, a);
+  k_gru2_tc<<<g2, P2_THREADS, SMEM2, s>>>(t->map_a2, t->map_w2, a);
+  return 2;
+}
+}  // namespace rnnlm_host

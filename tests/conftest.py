@@ -16,3 +16,11 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_sessionstart(session):
+    # build in-tree artefacts if missing or stale (no-op when up to date)
+    from paper_1801_09866_b200 import build as _b
+    _b.build()
+    import oracle
+    oracle.build()

@@ -1,0 +1,91 @@
+"""Replay-protocol parity driver: CUDA path vs CPU oracle.
+
+Per frame: both sides get the same queries (parents resolved from their own
+returned handles), then
+  * outcomes, child handles and state slots must be bit-exact,
+  * scores within ``tol_score`` (absolute),
+  * every new state (MISS) within ``tol_state`` of the oracle's fp64 GRU,
+  * the stored compression codes of new states bit-exact vs the oracle's
+    compress() of the SAME (GPU) vector,
+and finally the oracle's new states are overwritten with the GPU's, so the
+next frame's keys on both sides are computed from identical vectors
+("computed from identical input vectors", BASELINE.json north_star).
+
+Used by tests/ and by __graft_entry__.smoke() only.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle as O
+
+
+def _dev(a, device="cuda"):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32), device=device)
+
+
+def replay_compare(eng, orc, wl, frames=None, tol_score=1e-5, tol_state=1e-5, check_codes=True):
+    F = wl.frames if frames is None else frames
+    child_g = np.zeros(wl.n_total, np.uint32)
+    child_o = np.zeros(wl.n_total, np.uint32)
+    rep = dict(max_score_err=0.0, max_state_err=0.0, frames=F, queries=0, miss=0, shit=0, qhit=0,
+               invalid=0)
+    for t in range(F):
+        sl = wl.frame_slice(t)
+        pg = O.resolve_parents(wl.parent_ref[sl], child_g)
+        po = O.resolve_parents(wl.parent_ref[sl], child_o)
+        assert np.array_equal(pg, po), f"frame {t}: parent handles diverged"
+        sess = wl.session[sl]
+        sc, ch, oc = eng.query_batch(_dev(sess), _dev(pg), _dev(wl.word[sl]))
+        osc, och, ooc = orc.query_frame(sess, po, wl.word[sl])
+        gsc = sc.cpu().numpy()
+        gch = ch.cpu().numpy().view(np.uint32)
+        goc = oc.cpu().numpy()
+        bad = np.nonzero(goc != ooc)[0]
+        assert len(bad) == 0, (f"frame {t}: outcome mismatch at {bad[:8]}: gpu {goc[bad[:8]]} "
+                               f"oracle {ooc[bad[:8]]}")
+        assert np.array_equal(gch, och), f"frame {t}: child handles differ"
+        valid = ooc != O.INVALID
+        assert np.array_equal(np.isnan(gsc), np.isnan(osc))
+        if valid.any():
+            err = float(np.max(np.abs(gsc[valid] - osc[valid])))
+            rep["max_score_err"] = max(rep["max_score_err"], err)
+            assert err <= tol_score, f"frame {t}: score error {err}"
+        child_g[sl] = gch
+        child_o[sl] = och
+        rep["queries"] += len(sess)
+        rep["miss"] += int(np.sum(ooc == O.MISS))
+        rep["shit"] += int(np.sum(ooc == O.SHIT))
+        rep["qhit"] += int(np.sum(ooc == O.QHIT))
+        rep["invalid"] += int(np.sum(ooc == O.INVALID))
+        for s in np.unique(sess):
+            m = (sess == s) & valid & (ooc != O.QHIT)
+            if not m.any():
+                continue
+            hs = gch[m]
+            gs = eng.read_slots(int(s), hs).cpu().numpy().view(np.uint32)
+            assert np.array_equal(gs, orc.read_slots(int(s), hs)), f"frame {t}: slots differ"
+            mm = (sess == s) & (ooc == O.MISS)
+            if not mm.any():
+                continue
+            hm = gch[mm]
+            gst = eng.read_states(int(s), hm).cpu().numpy()
+            ost = orc.read_states(int(s), hm)
+            err = float(np.max(np.abs(gst - ost)))
+            rep["max_state_err"] = max(rep["max_state_err"], err)
+            assert err <= tol_state, f"frame {t}: state error {err}"
+            if check_codes and eng.cfg.cache_enabled:
+                gcode = eng.read_codes(int(s), hm).cpu().numpy()
+                for i in range(len(hm)):
+                    ref = O.compress(gst[i], eng.cfg.key_mode, eng.cfg.round_digits)
+                    assert np.array_equal(gcode[i], ref), f"frame {t}: code of handle {hm[i]} differs"
+            for i, hd in enumerate(hm):
+                orc.overwrite_state(int(s), int(hd), gst[i])
+    gst = eng.cache_stats()
+    ost = orc.stats()
+    for k in ("total_queries", "query_hits", "hidden_lookups", "hidden_hits", "gru_computations",
+              "sticky_error"):
+        assert gst[k] == ost[k], f"stat {k}: gpu {gst[k]} oracle {ost[k]}"
+    rep["stats"] = gst
+    return rep

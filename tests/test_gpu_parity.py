@@ -1,0 +1,268 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle.
+
+Bar (BASELINE.json north_star): bit-exact keys, MaxEnt indices, outcomes,
+handles, slots, stats; scores and states within 1e-5 (FP32 path) / 1e-3
+(BF16 tensor-core path).  Inputs: seeded synth/ generators with the shapes of
+the BASELINE.json configs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_1801_09866_b200 import (KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, RNNLM,
+                                   INVALID, MISS, QHIT, SHIT)
+from synth import generate_model, generate_workload, model_dims
+from synth.model import ModelDims
+from tests.parity_util import _dev, replay_compare
+
+pytestmark = pytest.mark.gpu
+
+TOL = {MATH_FP32: 1e-5, MATH_BF16: 1e-3}
+_models = {}
+
+
+def model(name_or_dims, seed=1234, scale=None):
+    key = (name_or_dims, seed, scale)
+    if key not in _models:
+        d = model_dims(name_or_dims) if isinstance(name_or_dims, str) else name_or_dims
+        _models[key] = (d, generate_model(d, seed=seed, scale=scale))
+    return _models[key]
+
+
+def pair(d, m, wl, mode=KEY_OFF, k=0, math=MATH_FP32, cache=True, B=None, cap=None):
+    cap = cap or wl.max_histories_hint()
+    B = B or wl.n_per_frame
+    eng = RNNLM.from_dims(d, m, key_mode=mode, round_digits=k, math=math, cache_enabled=cache,
+                          num_sessions=wl.S, max_queries_per_call=B, max_histories_per_session=cap)
+    orc = O.Oracle(O.make_config(d.V, d.E, d.H, d.maxent_log2, d.N, mode, k, 1 if cache else 0,
+                                 wl.S, cap), m)
+    return eng, orc
+
+
+@pytest.mark.parametrize("mode,k", [(KEY_SIGN, 0), (KEY_ROUND, 2), (KEY_OFF, 0)])
+def test_tiny_config_all_frames(mode, k):
+    """configs[0]: V 1k, E=H=64, 2^16 3-gram, 32 queries x 100 frames, fp32."""
+    d, m = model("tiny")
+    wl = generate_workload(1, 100, 32, d.V, seed=7)
+    eng, orc = pair(d, m, wl, mode, k)
+    rep = replay_compare(eng, orc, wl, tol_score=1e-5, tol_state=1e-5)
+    assert rep["miss"] > 100 and rep["qhit"] > 1000
+
+
+def test_tiny_cache_disabled():
+    d, m = model("tiny")
+    wl = generate_workload(1, 30, 32, d.V, seed=8)
+    eng, orc = pair(d, m, wl, KEY_SIGN, 0, cache=False)
+    rep = replay_compare(eng, orc, wl)
+    assert rep["miss"] == wl.n_total
+
+
+@pytest.mark.parametrize("mode,k", [(KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 3)])
+def test_small_hidden_many_lossy_hits_multisession(mode, k):
+    """H=16 with a large weight scale: lossy keys collide often, so the hidden
+    cache's SHIT path (old and same-frame owners) is exercised; 3 sessions."""
+    d, m = model(ModelDims(V=64, E=16, H=16, maxent_log2=10, N=4), seed=5, scale=1.5)
+    wl = generate_workload(3, 40, 96, d.V, seed=21)
+    eng, orc = pair(d, m, wl, mode, k)
+    rep = replay_compare(eng, orc, wl)
+    assert rep["shit"] > 50, rep
+
+
+def test_moderate_config_prefix():
+    """configs[1]: V 100k, H 256, 2^22 4-gram, 256 queries/frame (first 60 frames)."""
+    d, m = model("moderate")
+    wl = generate_workload(1, 60, 256, d.V, seed=7)
+    for mode in (KEY_OFF, KEY_SIGN):
+        eng, orc = pair(d, m, wl, mode)
+        rep = replay_compare(eng, orc, wl)
+        assert rep["miss"] > 500
+
+
+def test_large_config_fp32_prefix():
+    """configs[2] shapes: V 200k, H 1024, 2^27 4-gram, 2,048 queries/frame, fp32 path."""
+    d, m = model("large")
+    wl = generate_workload(1, 3, 2048, d.V, seed=7)
+    eng, orc = pair(d, m, wl, KEY_SIGN)
+    replay_compare(eng, orc, wl)
+
+
+def test_multisession_config_sample():
+    """configs[4] shapes: 4 of the 64 sessions x 2,048 queries/frame, large model."""
+    d, m = model("large")
+    wl = generate_workload(4, 2, 2048, d.V, seed=7)
+    eng, orc = pair(d, m, wl, KEY_SIGN)
+    replay_compare(eng, orc, wl)
+
+
+def test_edge_cases_invalid_and_ragged():
+    d, m = model("tiny")
+    eng = RNNLM.from_dims(d, m, key_mode=KEY_SIGN, num_sessions=2, max_queries_per_call=1000,
+                          max_histories_per_session=64)
+    orc = O.Oracle(O.make_config(d.V, d.E, d.H, d.maxent_log2, d.N, O.KEY_SIGN, 0, 1, 2, 64), m)
+    # empty batch
+    e = torch.empty(0, dtype=torch.int32, device="cuda")
+    eng.query_batch(e, e, e)
+    frames = [
+        # session, parent, word: dup pairs, word >= V, parent unborn, session >= S
+        ([0, 0, 0, 0, 1, 1, 1, 2], [0, 0, 0, 5, 0, 0, 0, 0], [3, 3, 1000, 4, 7, 7, 2, 1]),
+        ([0] * 5 + [1] * 3, [1, 2, 1, 1, 2, 1, 2, 2], [9, 9, 9, 8, 9, 3, 4, 4]),
+    ]
+    for sess, par, wrd in frames:
+        sc, ch, oc = eng.query_batch(_dev(sess), _dev(par), _dev(wrd))
+        osc, och, ooc = orc.query_frame(sess, par, wrd)
+        assert np.array_equal(oc.cpu().numpy(), ooc)
+        assert np.array_equal(ch.cpu().numpy().view(np.uint32), och)
+        v = ooc != O.INVALID
+        assert np.max(np.abs(sc.cpu().numpy()[v] - osc[v])) <= 1e-5
+        assert np.all(np.isnan(sc.cpu().numpy()[~v]))
+    st = eng.cache_stats()
+    ost = orc.stats()
+    for kk in ("total_queries", "query_hits", "hidden_lookups", "hidden_hits", "gru_computations"):
+        assert st[kk] == ost[kk]
+    assert st["sticky_error"] != 0
+    # a ragged batch of 1000 queries (not a multiple of the 1024-query scan tile / 256 threads)
+    rng = np.random.default_rng(3)
+    sess = np.sort(rng.integers(0, 2, 1000))
+    par = np.zeros(1000)
+    wrd = rng.integers(0, d.V, 1000)
+    sc, ch, oc = eng.query_batch(_dev(sess), _dev(par), _dev(wrd))
+    osc, och, ooc = orc.query_frame(sess, par, wrd)
+    assert np.array_equal(oc.cpu().numpy(), ooc)
+    assert np.array_equal(ch.cpu().numpy().view(np.uint32), och)   # includes capacity overflow
+
+
+def test_unsorted_batch_rejected():
+    d, m = model("tiny")
+    eng = RNNLM.from_dims(d, m, num_sessions=2, max_queries_per_call=8, max_histories_per_session=64)
+    sc, ch, oc = eng.query_batch(_dev([1, 0]), _dev([0, 0]), _dev([1, 2]))
+    assert set(oc.cpu().numpy().tolist()) == {INVALID}
+    assert eng.cache_stats()["sticky_error"] == 1
+    assert eng.cache_stats()["total_queries"] == 0
+
+
+def test_mode_off_equals_cache_disabled_bitwise():
+    """Cache-hit equivalence on the GPU: with a lossless key the cached run
+    returns exactly what direct evaluation returns (BASELINE north_star)."""
+    d, m = model("tiny")
+    wl = generate_workload(2, 40, 32, d.V, seed=9)
+    outs = []
+    for cache in (True, False):
+        eng = RNNLM.from_dims(d, m, key_mode=KEY_OFF, cache_enabled=cache, num_sessions=2,
+                              max_queries_per_call=64, max_histories_per_session=4096)
+        child = np.zeros(wl.n_total, np.uint32)
+        scores = np.zeros(wl.n_total, np.float32)
+        for t in range(wl.frames):
+            sl = wl.frame_slice(t)
+            par = O.resolve_parents(wl.parent_ref[sl], child)
+            sc, ch, _ = eng.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]))
+            child[sl] = ch.cpu().numpy().view(np.uint32)
+            scores[sl] = sc.cpu().numpy()
+        states = [eng.read_states(s, child[wl.session == s]).cpu().numpy() for s in range(2)]
+        outs.append((scores, states))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("mode,k", [(KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 2), (KEY_ROUND, 3),
+                                    (KEY_ROUND, 4), (KEY_OFF, 0)])
+def test_compression_kernel_bit_exact(mode, k):
+    """(a1) keys bit-exact vs the oracle on random and adversarial vectors."""
+    H = 64
+    d = ModelDims(V=4, E=8, H=H, maxent_log2=4, N=2)
+    _, m = model(d, seed=3)
+    eng = RNNLM.from_dims(d, m, key_mode=mode, round_digits=k, max_queries_per_call=4,
+                          max_histories_per_session=8)
+    rng = np.random.default_rng(k + 10 * mode)
+    rows = [rng.uniform(-1, 1, (4000, H)), rng.uniform(-1e-3, 1e-3, (500, H))]
+    # ties n.5 / 10^k on exactly representable values, zeros of both signs, near +-1
+    ties = np.array([0.125, -0.125, 0.375, -0.375, 0.5, -0.5, 0.0, -0.0, 0.25, -0.25, 0.05,
+                     -0.005, 0.0005, -0.00005, 0.99995, -0.99995], dtype=np.float32)
+    rows.append(np.tile(ties, (8, H // len(ties))))
+    rows.append(rng.choice([-1, 1], (100, H)) * np.nextafter(np.float32(1), np.float32(0)))
+    X = np.concatenate(rows).astype(np.float32)
+    got = eng.encode_states(torch.from_numpy(X)).cpu().numpy()
+    for i in range(len(X)):
+        assert np.array_equal(got[i], O.compress(X[i], mode, k)), (i, X[i][:4])
+
+
+def test_maxent_indices_bit_exact():
+    d, m = model("moderate")
+    wl = generate_workload(1, 30, 256, d.V, seed=4)
+    eng, orc = pair(d, m, wl, KEY_SIGN)
+    replay_compare(eng, orc, wl, check_codes=False)
+    rng = np.random.default_rng(0)
+    h, _ = orc.num_handles(0)
+    par = rng.integers(0, h, 3000).astype(np.uint32)
+    wrd = rng.integers(0, d.V, 3000).astype(np.uint32)
+    got = eng.maxent_indices(_dev(np.zeros(3000)), _dev(par), _dev(wrd)).cpu().numpy().view(np.uint64)
+    ctxs = orc.read_ctx(0, par)
+    for i in range(3000):
+        ref = O.maxent_indices(ctxs[i], int(wrd[i]), d.N, d.M)
+        assert got[i][:len(ref)].tolist() == ref
+        assert all(x == 2 ** 64 - 1 for x in got[i][len(ref):])
+
+
+def test_deterministic_rerun():
+    d, m = model(ModelDims(V=64, E=16, H=16, maxent_log2=10, N=4), seed=5, scale=1.5)
+    wl = generate_workload(3, 25, 96, d.V, seed=22)
+    runs = []
+    for _ in range(2):
+        eng = RNNLM.from_dims(d, m, key_mode=KEY_SIGN, num_sessions=3, max_queries_per_call=wl.n_per_frame,
+                              max_histories_per_session=wl.max_histories_hint())
+        child = np.zeros(wl.n_total, np.uint32)
+        out = []
+        for t in range(wl.frames):
+            sl = wl.frame_slice(t)
+            par = O.resolve_parents(wl.parent_ref[sl], child)
+            sc, ch, oc = eng.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]))
+            child[sl] = ch.cpu().numpy().view(np.uint32)
+            out.append((sc.cpu().numpy().view(np.uint32), child[sl].copy(), oc.cpu().numpy()))
+        runs.append(out)
+    for a, b in zip(*runs):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
+def test_resolve_parents_kernel():
+    from paper_1801_09866_b200 import resolve_parents
+    ref = torch.tensor([-1, 0, 2, 1], dtype=torch.int64, device="cuda")
+    log = torch.tensor([7, 8, 9], dtype=torch.int32, device="cuda")
+    out = torch.empty(4, dtype=torch.int32, device="cuda")
+    resolve_parents(ref, log, out)
+    assert out.cpu().tolist() == [0, 7, 9, 8]
+
+
+# ---------------------------------------------------------------- BF16 tensor-core path (tcgen05)
+@pytest.mark.parametrize("mode", [KEY_OFF, KEY_SIGN])
+def test_moderate_bf16_tensor_core(mode):
+    d, m = model("moderate")
+    wl = generate_workload(1, 40, 256, d.V, seed=17)
+    eng, orc = pair(d, m, wl, mode, math=MATH_BF16)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_BF16], tol_state=TOL[MATH_BF16])
+    assert rep["miss"] > 300
+
+
+def test_large_bf16_cache_off_full_tiles():
+    """All-miss stress: 2,048 GRU rows per frame = 16 full M-tiles + ragged frames."""
+    d, m = model("large")
+    wl = generate_workload(1, 2, 2048, d.V, seed=5)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16, cache=False)
+    rep = replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+    assert rep["miss"] == wl.n_total
+
+
+def test_large_bf16_ragged_rows():
+    """Q not a multiple of 128 (ragged last M-tile) on the large model."""
+    d, m = model("large")
+    wl = generate_workload(1, 2, 300, d.V, seed=6)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16, cache=False)
+    replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+
+
+def test_multisession_bf16_sample():
+    d, m = model("large")
+    wl = generate_workload(4, 3, 2048, d.V, seed=7)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16)
+    replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
