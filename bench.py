@@ -200,6 +200,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1801_09866_b200 as R
+    from paper_1801_09866_b200.parallel import all_gather_results
 
     rank, world, local = dist_env()
     if args.gpus != world and world > 1:
@@ -225,7 +226,6 @@ def run_ours(args):
                             cache_enabled=not args.no_cache, num_sessions=S,
                             max_queries_per_call=n, max_histories_per_session=cap, device=local)
 
-    as_dev = lambda a, dt: torch.as_tensor(a.view(dt) if a.dtype.itemsize == 4 else a, device=dev)
     d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
     d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
     d_ref = torch.as_tensor(wl.parent_ref, device=dev)
@@ -251,8 +251,7 @@ def run_ours(args):
             ev.record(main)
             side.wait_event(ev)
             with torch.cuda.stream(side):
-                pair = torch.stack([d_score[sl].view(torch.int32), d_child[sl]], dim=1)
-                dist.all_gather_into_tensor(gathered, pair)
+                all_gather_results(d_score[sl], d_child[sl], out=gathered)
 
     # ---- warm-up
     for t in range(args.warmup):
@@ -282,8 +281,7 @@ def run_ours(args):
             ev.record(main)
             side.wait_event(ev)
             with torch.cuda.stream(side):
-                pair = torch.stack([d_score[sl].view(torch.int32), d_child[sl]], dim=1)
-                dist.all_gather_into_tensor(gathered, pair)
+                all_gather_results(d_score[sl], d_child[sl], out=gathered)
         evs[i][1].record()
     torch.cuda.synchronize()
     if world > 1:

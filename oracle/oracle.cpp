@@ -32,6 +32,7 @@ struct Session {
   std::map<std::pair<uint32_t, std::string>, uint32_t> hcache;
   uint64_t total = 0, query_hits = 0, hidden_lookups = 0, hidden_hits = 0, gru = 0;
   int sticky = 0;
+  bool poisoned = false;        // ran out of handles: later frames are rejected until reset
 };
 
 struct Pending {                // a GRU evaluation owed at the end of the frame
@@ -239,7 +240,11 @@ int orc_query_frame(orc_t *o, uint32_t n, const uint32_t *session, const uint32_
   if (!o || (n && (!session || !parent || !word || !score || !child))) return ORC_E_INVALID_ARG;
   const orc_config &c = o->cfg;
   std::vector<uint32_t> limit(c.num_sessions);
-  for (uint32_t s = 0; s < c.num_sessions; ++s) limit[s] = (uint32_t)o->sess[s].rec.size();
+  std::vector<char> dead(c.num_sessions);
+  for (uint32_t s = 0; s < c.num_sessions; ++s) {
+    limit[s] = (uint32_t)o->sess[s].rec.size();
+    dead[s] = o->sess[s].poisoned;
+  }
   std::vector<Pending> pending;
   const uint32_t cb = orc_code_bytes(c.key_mode, c.round_digits, c.H);
   std::string code(cb, '\0');
@@ -249,6 +254,7 @@ int orc_query_frame(orc_t *o, uint32_t n, const uint32_t *session, const uint32_
     int err = ORC_OK;
     if (s >= c.num_sessions) err = ORC_E_INVALID_ARG;
     else if (w >= c.V) err = ORC_E_VOCAB;
+    else if (dead[s]) err = ORC_E_CAPACITY;                    // reading 9: reset required
     else if (p >= limit[s]) err = ORC_E_HISTORY;               // S:272, reading 17
     else if (!(c.cache_enabled && o->sess[s].qcache.count({p, w})) &&
              o->sess[s].rec.size() >= c.max_histories)
@@ -258,6 +264,7 @@ int orc_query_frame(orc_t *o, uint32_t n, const uint32_t *session, const uint32_
       child[q] = 0xFFFFFFFFu;
       if (outcome) outcome[q] = ORC_INVALID;
       if (s < c.num_sessions && o->sess[s].sticky == ORC_OK) o->sess[s].sticky = err;
+      if (err == ORC_E_CAPACITY) o->sess[s].poisoned = true;
       if (first_err == ORC_OK) first_err = err;
       continue;
     }

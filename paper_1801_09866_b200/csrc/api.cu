@@ -183,7 +183,10 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   Params &P = h->P;
   P.V = c.vocab; P.E = c.embed; P.H = c.hidden; P.N = c.maxent_order; P.S = c.num_sessions;
   P.cap = c.max_histories_per_session;
-  const uint32_t tcap = next_pow2(2ull * P.cap);
+  // Tables hold >= cap + B_max keys at load <= 0.5: the keys claimed before a
+  // session's first capacity failure (< cap) plus one call's worth of claims
+  // (<= B_max) always fit, so claiming never depends on thread order.
+  const uint32_t tcap = next_pow2(2ull * ((uint64_t)P.cap + c.max_queries_per_call));
   P.qmask = tcap - 1;
   P.hmask = tcap - 1;
   P.key_mode = c.key_mode; P.round_digits = c.round_digits; P.cache = c.cache_enabled ? 1 : 0;

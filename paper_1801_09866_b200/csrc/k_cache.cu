@@ -79,6 +79,7 @@ __global__ void k_qprobe(Params P, CallArgs A, uint32_t ntiles) {
   if (s >= P.S) err = RNNLM_E_INVALID_ARG;
   else if (q > 0 && A.session[q - 1] > s) err = RNNLM_E_INVALID_ARG;
   else if (w >= P.V) err = RNNLM_E_VOCAB;
+  else if (P.ctr[s].poisoned) err = RNNLM_E_CAPACITY;
   else if (p >= P.ctr[s].next_handle) err = RNNLM_E_HISTORY;
   if (q > 0 && A.session[q - 1] > s) P.counts[2] = A.epoch;   // batch not sorted by session
   if (err) {
@@ -94,12 +95,16 @@ __global__ void k_qprobe(Params P, CallArgs A, uint32_t ntiles) {
   const unsigned long long key = ((unsigned long long)p << 32) | w;
   const size_t base = (size_t)s * (P.qmask + 1);
   uint32_t idx = (uint32_t)(mix64(key) & P.qmask);
-  for (;;) {
+  for (uint32_t probes = 0; probes <= P.qmask; ++probes) {
     const unsigned long long t = P.qtab[base + idx].tag;
     if (t == key) { P.st[q] = ST_QHIT_OLD; P.qent[q] = idx; return; }
     if (t == TAG_EMPTY) { P.st[q] = ST_QNEED; P.qent[q] = idx; return; }
     idx = (idx + 1) & P.qmask;
   }
+  // table full: only possible once the session's handles are exhausted (tables
+  // hold >= 2 x capacity entries), so this is a capacity failure
+  P.st[q] = ST_INVALID;
+  latch(P.sticky, RNNLM_E_CAPACITY);
 }
 
 // ---- (a2) claim -------------------------------------------------------------
@@ -110,7 +115,13 @@ __global__ void k_qclaim(Params P, CallArgs A) {
   const unsigned long long key = ((unsigned long long)A.parent[q] << 32) | A.word[q];
   const size_t base = (size_t)s * (P.qmask + 1);
   uint32_t idx = P.qent[q];                 // slots before the hint hold other keys
-  for (;;) {
+  uint32_t probes = 0;
+  for (;; ++probes) {
+    if (probes > P.qmask) {                 // table full -> capacity failure
+      P.st[q] = ST_INVALID;
+      latch(P.sticky, RNNLM_E_CAPACITY);
+      return;
+    }
     unsigned long long t = vload64(&P.qtab[base + idx].tag);
     if (t == TAG_EMPTY) t = atomicCAS(&P.qtab[base + idx].tag, TAG_EMPTY, key);
     if (t == TAG_EMPTY || t == key) break;
@@ -133,7 +144,7 @@ __global__ void k_hprobe(Params P, CallArgs A) {
   const unsigned long long hh = P.codehash[cb + ps];
   const size_t base = (size_t)s * (P.hmask + 1);
   uint32_t idx = hhome(hh, w, P.hmask);
-  for (;;) {
+  for (uint32_t probes = 0; probes <= P.hmask; ++probes) {
     const unsigned long long t = P.htab[base + idx].tag;
     if (t == TAG_EMPTY) { P.st[q] = ST_HNEED; P.hent[q] = idx; return; }
     if (hkey_match(P, t, s, w, ps, hh)) {
@@ -144,6 +155,8 @@ __global__ void k_hprobe(Params P, CallArgs A) {
     }
     idx = (idx + 1) & P.hmask;
   }
+  P.st[q] = ST_INVALID;                     // table full -> capacity failure
+  latch(P.sticky, RNNLM_E_CAPACITY);
 }
 
 // ---- (a3) claim ------------------------------------------------------------
@@ -156,7 +169,12 @@ __global__ void k_hclaim(Params P, CallArgs A) {
   const unsigned long long mine = ((unsigned long long)ps << 32) | w;
   const size_t base = (size_t)s * (P.hmask + 1);
   uint32_t idx = P.hent[q];
-  for (;;) {
+  for (uint32_t probes = 0;; ++probes) {
+    if (probes > P.hmask) {                 // table full -> capacity failure
+      P.st[q] = ST_INVALID;
+      latch(P.sticky, RNNLM_E_CAPACITY);
+      return;
+    }
     unsigned long long t = vload64(&P.htab[base + idx].tag);
     if (t == TAG_EMPTY) {
       t = atomicCAS(&P.htab[base + idx].tag, TAG_EMPTY, mine);
@@ -295,6 +313,7 @@ __global__ void k_commit(Params P, CallArgs A) {
   if (h >= P.cap) {                                    // out of history handles
     P.st[q] = ST_INVALID;
     latch(P.sticky, RNNLM_E_CAPACITY);
+    P.ctr[s].poisoned = 1u;                            // read from the next call on
     A.score[q] = __int_as_float(0x7fc00000);
     A.child[q] = NONE;
     if (P.cache) { P.qtab[qb + P.qent[q]].child = NONE; P.qtab[qb + P.qent[q]].score = __int_as_float(0x7fc00000); }

@@ -36,7 +36,9 @@ struct __align__(32) Rec {
 };
 // Per-session counters and allocation cursors.
 struct __align__(64) SessCtr {
-  uint32_t next_handle, next_slot, pad0, pad1;
+  uint32_t next_handle, next_slot;
+  uint32_t poisoned;                // a capacity failure happened: every later query is INVALID
+  uint32_t pad1;
   unsigned long long total, qhits, hlookups, hhits, gru;
   unsigned long long pad2[1];
 };

@@ -31,7 +31,7 @@ def model(name_or_dims, seed=1234, scale=None):
 
 
 def pair(d, m, wl, mode=KEY_OFF, k=0, math=MATH_FP32, cache=True, B=None, cap=None):
-    cap = cap or wl.max_histories_hint()
+    cap = cap or (wl.max_histories_hint() if cache else wl.n_total // wl.S + 2)
     B = B or wl.n_per_frame
     eng = RNNLM.from_dims(d, m, key_mode=mode, round_digits=k, math=math, cache_enabled=cache,
                           num_sessions=wl.S, max_queries_per_call=B, max_histories_per_session=cap)
@@ -58,15 +58,26 @@ def test_tiny_cache_disabled():
     assert rep["miss"] == wl.n_total
 
 
-@pytest.mark.parametrize("mode,k", [(KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 3)])
-def test_small_hidden_many_lossy_hits_multisession(mode, k):
-    """H=16 with a large weight scale: lossy keys collide often, so the hidden
-    cache's SHIT path (old and same-frame owners) is exercised; 3 sessions."""
-    d, m = model(ModelDims(V=64, E=16, H=16, maxent_log2=10, N=4), seed=5, scale=1.5)
-    wl = generate_workload(3, 40, 96, d.V, seed=21)
+def forgetful_model(H=16, E=16, V=64, seed=5):
+    """Input-dominated GRU (z ~ 0.98, tiny recurrent weights): a state is almost
+    a function of its last word, so histories that end in the same word get
+    equal lossy keys and the hidden cache's SHIT paths are exercised."""
+    d = ModelDims(V=V, E=E, H=H, maxent_log2=10, N=4)
+    m = generate_model(d, seed=seed, scale=1.0, bf16_grid=False)
+    for k in ("Uz", "Ur", "Uh"):
+        m[k] = (m[k] * 0.02).astype(np.float32)
+    m["bz"] = np.full(H, 4.0, np.float32)
+    return d, m
+
+
+@pytest.mark.parametrize("mode,k", [(KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 2), (KEY_OFF, 0)])
+def test_lossy_hidden_hits_multisession(mode, k):
+    """Many SHITs (earlier-call and same-call owners), 3 sessions, fp32 path."""
+    d, m = forgetful_model()
+    wl = generate_workload(3, 40, 96, d.V, seed=21, dur=(2, 6))
     eng, orc = pair(d, m, wl, mode, k)
     rep = replay_compare(eng, orc, wl)
-    assert rep["shit"] > 50, rep
+    assert rep["shit"] >= {KEY_SIGN: 100, KEY_ROUND: 20, KEY_OFF: 0}[mode], rep
 
 
 def test_moderate_config_prefix():
@@ -205,8 +216,8 @@ def test_maxent_indices_bit_exact():
 
 
 def test_deterministic_rerun():
-    d, m = model(ModelDims(V=64, E=16, H=16, maxent_log2=10, N=4), seed=5, scale=1.5)
-    wl = generate_workload(3, 25, 96, d.V, seed=22)
+    d, m = forgetful_model()
+    wl = generate_workload(3, 25, 96, d.V, seed=22, dur=(2, 6))
     runs = []
     for _ in range(2):
         eng = RNNLM.from_dims(d, m, key_mode=KEY_SIGN, num_sessions=3, max_queries_per_call=wl.n_per_frame,
