@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--prefill", type=int, default=40,
+                    help="untimed frames run before warm-up so timed frames are mid-utterance")
     ap.add_argument("--uniform-words", action="store_true", help="(ncu evidence) no Zipf reuse")
     return ap.parse_args()
 
@@ -213,7 +215,8 @@ def run_ours(args):
     dims = model_dims(args.workload)
     S = sessions_for(args, world)
     B_s = c["B_s"]
-    frames = args.warmup + args.steps
+    F0 = args.prefill
+    frames = F0 + args.warmup + args.steps
     model = generate_model(dims, seed=1234)
     V_draw = dims.V
     wl = generate_workload(S, frames, B_s, V_draw, seed=7 + rank * S,
@@ -253,8 +256,8 @@ def run_ours(args):
             with torch.cuda.stream(side):
                 all_gather_results(d_score[sl], d_child[sl], out=gathered)
 
-    # ---- warm-up
-    for t in range(args.warmup):
+    # ---- prefill (utterance start, untimed) + warm-up
+    for t in range(F0 + args.warmup):
         step(t)
     torch.cuda.synchronize()
     st0 = eng.cache_stats()
@@ -269,7 +272,7 @@ def run_ours(args):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     # the resolve kernel + the step are inside each event pair; the L2 flush is between pairs
-    for i, t in enumerate(range(args.warmup, frames)):
+    for i, t in enumerate(range(F0 + args.warmup, frames)):
         flush.zero_()
         sl = wl.frame_slice(t)
         evs[i][0].record()
@@ -335,6 +338,7 @@ def run_ours(args):
                    "H": dims.H, "maxent": f"2^{dims.maxent_log2} {dims.N}-gram", "key": args.key,
                    "cache": not args.no_cache, "math": args.math,
                    "l2": "flushed between timed steps (256 MiB write outside the event pair)",
+                   "timed_frames": f"{F0 + args.warmup}..{frames - 1} of each utterance ({F0} prefill + {args.warmup} warm-up frames untimed)",
                    "parallelism": f"dp{world} (sessions sharded, weights replicated, NCCL all-gather of (score, child))"},
         "roofline": {"kernel": "GRU gate contraction (both phases, per step)", "bound": bound,
                      "achieved": achieved, "peak": peak,
@@ -397,13 +401,14 @@ def run_e2e(args, eng, wl, dev, world):
         torch.cuda.current_stream().synchronize()
         child_log[sl] = h_child.numpy().view(np.uint32)
 
-    for t in range(args.warmup):
+    F0 = args.prefill
+    for t in range(F0 + args.warmup):
         host_step(t)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for t in range(args.warmup, args.warmup + args.steps):
+    for t in range(F0 + args.warmup, F0 + args.warmup + args.steps):
         host_step(t)
     torch.cuda.synchronize()
     secs = time.perf_counter() - t0

@@ -345,7 +345,8 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
   if (P.math == RNNLM_MATH_BF16) k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s);
   else k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
   if (h->timing) cudaEventRecord(ev[3], s);
-  k += rnnlm_host::launch_encode_rows(P, n, h->num_sms, s);
+  if (P.math != RNNLM_MATH_BF16)                      // the tcgen05 epilogue encodes in place
+    k += rnnlm_host::launch_encode_rows(P, n, h->num_sms, s);
   if (h->timing) cudaEventRecord(ev[4], s);
   k += rnnlm_host::launch_final(P, A, s);
   if (h->timing) {

@@ -326,7 +326,10 @@ __global__ void k_commit(Params P, CallArgs A) {
     P.row_src[r] = (uint32_t)(cb + P.pslot[q]);
     P.row_dst[r] = (uint32_t)(cb + sl);
     P.row_word[r] = w;
-    if (P.cache) P.htab[(size_t)s * (P.hmask + 1) + P.hent[q]].slot = sl;
+    if (P.cache) {
+      P.htab[(size_t)s * (P.hmask + 1) + P.hent[q]].slot = sl;
+      P.codehash[cb + sl] = 0ull;                      // accumulated by the GRU epilogue
+    }
   } else if (st == ST_SHIT_OLD) {
     sl = P.cslot[q];
   } else {                                             // SHIT_NEW: the owner's new slot

@@ -4,25 +4,27 @@
 // frame's (h || x) rows form one block) is a real dense contraction:
 // [Q, E+H] x [E+H, 3H] for Q misses (Chung form, reading 1), executed as
 //
-//   phase 1  A = [x | h] rows GATHERED on the fly (x = E[word] bf16, h = bf16
-//            shadow of the parent state) by 4 producer warps with cp.async
-//            16-byte copies straight into the 128B-swizzled UMMA layout;
-//            B = gate-interleaved weights W1 [H/64 x 192 rows][E+H] bf16 via
-//            TMA (per 64-unit block: 64 rows z, 64 rows r, 64 rows h; the h
-//            rows are zero on the recurrent half, so those K chunks issue
-//            N = 128 MMAs and load only the z/r rows).  Tile 128 x 192, fp32
-//            accumulators in TMEM (two buffers of 256 columns: the epilogue of
-//            tile i overlaps the MMAs of tile i+1).  Epilogue: z = s(.+bz),
-//            r = s(.+br) -> r.h (bf16, phase-2 A operand), Wh x + bh (fp32).
+//   gather   A1[r] = [x | h] (x = E[word] bf16, h = bf16 shadow of the parent
+//            state), one warp per row, 16-byte vector copies (k_gather_a1).
+//   phase 1  A = A1 via TMA, B = gate-interleaved weights W1 [H/64 x 192
+//            rows][E+H] bf16 via TMA (per 64-unit block: 64 rows z, 64 rows r,
+//            64 rows h; the h rows are zero on the recurrent half, so those K
+//            chunks issue N = 128 MMAs and load only the z/r rows).  Tile
+//            128 x 192, fp32 accumulators in TMEM (two buffers of 256 columns:
+//            the epilogue of tile i overlaps the MMAs of tile i+1).  Epilogue:
+//            z = s(.+bz), r = s(.+br) -> r.h (bf16, phase-2 A), Wh x + bh (fp32).
 //   phase 2  A = r.h rows via TMA, B = Uh [H][H] bf16 via TMA, tile 128 x 256;
 //            epilogue: c = tanh(Wh x + bh + Uh(r.h)), h' = (1-z) h + z c, the
-//            new fp32 state and its bf16 shadow.
+//            new fp32 state, its bf16 shadow, and (a1) its compression code +
+//            code-hash contribution (hash terms add, so the four N-tiles of a
+//            row combine with one 64-bit atomicAdd each, order-independent).
 //
-// Both kernels are persistent (grid <= #SMs), warp-specialised: producer(s),
-// one MMA-issuing thread (tcgen05.mma.cta_group::1.kind::f16, M = 128), four
-// epilogue warps (tcgen05.ld.32x32b, one TMEM lane = one row per thread).
-// Pipelines are mbarrier rings (full / empty per smem stage, full / empty per
-// TMEM accumulator).  Rows >= Q are zero-filled / discarded.
+// Both GEMM kernels are persistent (grid <= #SMs), warp-specialised: one TMA
+// producer thread, one MMA-issuing thread (tcgen05.mma.cta_group::1.kind::f16,
+// M = 128), eight epilogue warps (tcgen05.ld.32x32b: TMEM lane quarter =
+// warp % 4, two warps per quarter split the columns).  Pipelines are mbarrier
+// rings (full / empty per smem stage, full / empty per TMEM accumulator).
+// Rows >= Q read stale A rows and are discarded.
 #include <cuda.h>
 
 #include <cstring>
@@ -158,17 +160,44 @@ struct TcArgs {
   const uint32_t *row_src, *row_dst, *row_word, *counts;
   float *g_z, *g_wxb;
   __nv_bfloat16 *g_rh16;
+  __nv_bfloat16 *a1;               // [B_max][E+H] gathered phase-1 A operand
+  // (a1) compression of the new state, fused into the phase-2 epilogue
+  uint32_t cache, key_mode, round_digits, cstride;
+  float round_scale;
+  uint8_t *codes;
+  unsigned long long *codehash;
 };
 
+// ---------------------------------------------------------------- A gather
+// Phase-1 A operand: row r = [E[word_r] | h16[src_r]] (bf16, K-major, dense),
+// one warp per row, 16-byte loads/stores (the paper's per-frame (h || x)
+// block, built in HBM instead of host memory).
+__global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
+  const uint32_t Q = a.counts[1];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t K1 = a.E + a.H;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Q; r += nw) {
+    const uint4 *x = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)a.row_word[r] * a.E);
+    const uint4 *h = reinterpret_cast<const uint4 *>(a.state16 + (size_t)a.row_src[r] * a.H);
+    uint4 *dst = reinterpret_cast<uint4 *>(a.a1 + (size_t)r * K1);
+    const uint32_t nx = a.E / 8, nh = a.H / 8;
+    for (uint32_t i = lane; i < nx; i += 32) dst[i] = __ldg(x + i);
+    for (uint32_t i = lane; i < nh; i += 32) dst[nx + i] = h[i];
+  }
+}
+
 // =============================================================== phase 1
-// warps 0-3: A gather producers (warp 0 lane 0 also issues the B TMA)
-// warp 4:    TMEM allocation + MMA issue
-// warps 5-8: epilogue (TMEM lane quarter = warp % 4)
-constexpr int P1_THREADS = 9 * 32;
+// warp 0: TMA producer (A rows + gate-interleaved weights)
+// warp 1: TMEM allocation + MMA issue
+// warps 2-9: epilogue; TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
+constexpr int EPI_WARPS = 8;
+constexpr int P1_THREADS = (2 + EPI_WARPS) * 32;
+constexpr int P2_THREADS = (2 + EPI_WARPS) * 32;
 
 __global__ void __launch_bounds__(P1_THREADS, 1)
-    k_gru1_tc(const __grid_constant__ CUtensorMap map_w1x, const __grid_constant__ CUtensorMap map_w1h,
-              TcArgs a) {
+    k_gru1_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1x,
+              const __grid_constant__ CUtensorMap map_w1h, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;                                   // ST1 x 16 KB
@@ -186,51 +215,40 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
   const uint32_t kx = a.E / BK, kh = a.H / BK, KC = kx + kh;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST1; ++s) { mbar_init(&full[s], 128 + 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    for (int s = 0; s < ST1; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS * 32); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&map_a1);
     prefetch_map(&map_w1x);
     prefetch_map(&map_w1h);
   }
-  if (warp == 4) tmem_alloc(tmem_base_sm, TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_base_sm, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_sm;
 
-  if (warp < 4) {
-    // ------------------------------------------------ producers
-    const int p = threadIdx.x;                          // row within the tile
-    uint32_t stage = 0, phase = 0;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const uint32_t m0 = (tile / a.nub) * BM, ub = tile % a.nub;
-      const uint32_t row = m0 + p;
-      const bool valid = row < Q;
-      const __nv_bfloat16 *xrow = valid ? a.emb16 + (size_t)a.row_word[row] * a.E : a.emb16;
-      const __nv_bfloat16 *hrow = valid ? a.state16 + (size_t)a.row_src[row] * a.H : a.state16;
-      const uint32_t nbytes = valid ? 16u : 0u;
-      for (uint32_t kc = 0; kc < KC; ++kc) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (p == 0) {
-          const uint32_t dstB = smem_u32(sB + stage * B1_BYTES);
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t m0 = (tile / a.nub) * BM, ub = tile % a.nub;
+        for (uint32_t kc = 0; kc < KC; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t dA = smem_u32(sA + stage * A_BYTES), dB = smem_u32(sB + stage * B1_BYTES);
           if (kc < kx) {
-            mbar_expect_tx(&full[stage], N1 * BK * 2);
-            tma_load_2d(dstB, &map_w1x, &full[stage], (int)(kc * BK), (int)(ub * N1));
+            mbar_expect_tx(&full[stage], A_BYTES + N1 * BK * 2);
+            tma_load_2d(dB, &map_w1x, &full[stage], (int)(kc * BK), (int)(ub * N1));
           } else {
-            mbar_expect_tx(&full[stage], N1H * BK * 2);
-            tma_load_2d(dstB, &map_w1h, &full[stage], (int)(kc * BK), (int)(ub * N1));
+            mbar_expect_tx(&full[stage], A_BYTES + N1H * BK * 2);
+            tma_load_2d(dB, &map_w1h, &full[stage], (int)(kc * BK), (int)(ub * N1));
           }
+          tma_load_2d(dA, &map_a1, &full[stage], (int)(kc * BK), (int)m0);
+          if (++stage == ST1) { stage = 0; phase ^= 1; }
         }
-        const __nv_bfloat16 *src = kc < kx ? xrow + kc * BK : hrow + (kc - kx) * BK;
-        const uint32_t dst = smem_u32(sA + stage * A_BYTES) + p * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) cp_async16(dst + ((c ^ (p & 7)) << 4), src + c * 8, nbytes);
-        cp_async_mbar_arrive(&full[stage]);
-        mbar_arrive(&full[stage]);
-        if (++stage == ST1) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     uint32_t stage = 0, phase = 0, it = 0;
     const uint32_t id_x = idesc_bf16(BM, N1), id_h = idesc_bf16(BM, N1H);
@@ -242,7 +260,6 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
       for (uint32_t kc = 0; kc < KC; ++kc) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        fence_proxy_async();
         if (lane == 0) {
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B1_BYTES);
           const uint32_t id = kc < kx ? id_x : id_h;
@@ -259,6 +276,7 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
   } else {
     // ------------------------------------------------ epilogue
     const int q = warp & 3;                             // TMEM lane quarter
+    const int half = (warp - 2) >> 2;                   // 32-unit half of the 64-unit block
     const int r_in = q * 32 + lane;
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -268,22 +286,23 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
       tc_fence_after();
       const uint32_t row = m0 + r_in;
       const bool valid = row < Q;
-      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
-      const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * 64;
-      const float *bb = a.b1 + (size_t)ub * 192;
-      const size_t o = (size_t)row * a.H + ub * 64;
-#pragma unroll 1
-      for (int g = 0; g < 4; ++g) {
-        float vz[16], vr[16], vx[16];
-        tmem_ld16(tbase + g * 16, vz);
-        tmem_ld16(tbase + 64 + g * 16, vr);
-        tmem_ld16(tbase + 128 + g * 16, vx);
-        tmem_ld_wait();
-        if (g == 3) {                                   // accumulator drained
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
-        }
-        if (!valid) continue;
+      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16) + half * 32;
+      const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * 64 + half * 32;
+      const float *bb = a.b1 + (size_t)ub * 192 + half * 32;
+      const size_t o = (size_t)row * a.H + ub * 64 + half * 32;
+      float vz[2][16], vr[2][16], vx[2][16];
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        tmem_ld16(tbase + g * 16, vz[g]);
+        tmem_ld16(tbase + 64 + g * 16, vr[g]);
+        tmem_ld16(tbase + 128 + g * 16, vx[g]);
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);                        // accumulator drained
+      if (!valid) continue;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
         float z[16], rh[16], wx[16];
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
@@ -292,9 +311,9 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const int u = g * 16 + j + t;
-            z[j + t] = sigm(vz[j + t] + bb[u]);
-            rh[j + t] = sigm(vr[j + t] + bb[64 + u]) * hh[t];
-            wx[j + t] = vx[j + t] + bb[128 + u];
+            z[j + t] = sigm(vz[g][j + t] + __ldg(bb + u));
+            rh[j + t] = sigm(vr[g][j + t] + __ldg(bb + 64 + u)) * hh[t];
+            wx[j + t] = vx[g][j + t] + __ldg(bb + 128 + u);
           }
         }
         float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
@@ -319,16 +338,68 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
-// =============================================================== phase 2
-// warp 0: TMA producer; warp 1: TMEM alloc + MMA; warps 2-5: epilogue
-constexpr int P2_THREADS = 6 * 32;
+// Compression code words of 16 consecutive new-state elements starting at
+// unit u0 (same packing and hash terms as k_encode.cu's encode_row_warp):
+// sign: bits of a 32-bit word (two calls fill one word), round: int8 / int16
+// codes, off: the fp32 bit patterns.  Returns the hash contribution.
+__device__ __forceinline__ unsigned long long encode16(const TcArgs &a, const float *hn, uint32_t u0,
+                                                       uint8_t *code, uint32_t &signacc) {
+  unsigned long long hs = 0;
+  if (a.key_mode == RNNLM_KEY_SIGN) {
+    uint32_t b = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) b |= (hn[j] >= 0.0f ? 1u : 0u) << j;
+    if ((u0 & 31) == 0) {
+      signacc = b;
+    } else {
+      const uint32_t word = signacc | (b << 16);
+      const uint32_t wi = u0 >> 5;
+      reinterpret_cast<uint32_t *>(code)[wi] = word;
+      hs += mix64(((unsigned long long)wi << 32) | word);
+    }
+  } else if (a.key_mode == RNNLM_KEY_ROUND) {
+    if (a.round_digits <= 2) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          word |= ((uint32_t)(uint8_t)(int8_t)(int)roundf(__fmul_rn(hn[4 * i + j], a.round_scale))) << (8 * j);
+        w[i] = word;
+        hs += mix64(((unsigned long long)(u0 / 4 + i) << 32) | word);
+      }
+      *reinterpret_cast<uint4 *>(code + u0) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      uint32_t w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          word |= ((uint32_t)(uint16_t)(int16_t)(int)roundf(__fmul_rn(hn[2 * i + j], a.round_scale))) << (16 * j);
+        w[i] = word;
+        hs += mix64(((unsigned long long)(u0 / 2 + i) << 32) | word);
+      }
+      *reinterpret_cast<uint4 *>(code + 2 * u0) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4 *>(code + 2 * u0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      hs += mix64(((unsigned long long)(u0 + j) << 32) | __float_as_uint(hn[j]));
+  }
+  return hs;
+}
 
+// =============================================================== phase 2
+// warp 0: TMA producer; warp 1: TMEM alloc + MMA; warps 2-9: epilogue
 __global__ void __launch_bounds__(P2_THREADS, 1)
     k_gru2_tc(const __grid_constant__ CUtensorMap map_a2, const __grid_constant__ CUtensorMap map_w2,
               TcArgs a) {
@@ -351,7 +422,7 @@ __global__ void __launch_bounds__(P2_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS * 32); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&map_a2);
     prefetch_map(&map_w2);
@@ -401,41 +472,54 @@ __global__ void __launch_bounds__(P2_THREADS, 1)
     }
   } else {
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;                   // 128-unit half of the 256-unit tile
     const int r_in = q * 32 + lane;
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
-      const uint32_t m0 = (tile / nt) * BM, n0 = (tile % nt) * N2;
+      const uint32_t m0 = (tile / nt) * BM;
+      const uint32_t n0 = (tile % nt) * N2 + half * (N2 / 2);
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t row = m0 + r_in;
       const bool valid = row < Q;
       const uint32_t dst = valid ? a.row_dst[row] : NONE;
-      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16) + half * (N2 / 2);
       const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + n0;
-      const size_t o = (size_t)row * a.H + n0;
+      const size_t o = (size_t)(valid ? row : 0) * a.H + n0;
+      uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && dst != NONE)
+                          ? a.codes + (size_t)dst * a.cstride : nullptr;
+      unsigned long long hs = 0;
+      uint32_t signacc = 0;
 #pragma unroll 1
-      for (int g = 0; g < N2 / 16; ++g) {
+      for (int g = 0; g < N2 / 32; ++g) {
         float vu[16];
         tmem_ld16(tbase + g * 16, vu);
+        float4 z4[4], w4[4], h4[4];
+        if (dst != NONE) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            z4[j] = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + 4 * j);
+            w4[j] = *reinterpret_cast<const float4 *>(a.g_wxb + o + g * 16 + 4 * j);
+            h4[j] = *reinterpret_cast<const float4 *>(hp + g * 16 + 4 * j);
+          }
+        }
         tmem_ld_wait();
-        if (g == N2 / 16 - 1) {
+        if (g == N2 / 32 - 1) {
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
         }
         if (dst == NONE) continue;
         float hn[16];
 #pragma unroll
-        for (int j = 0; j < 16; j += 4) {
-          const float4 z4 = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + j);
-          const float4 w4 = *reinterpret_cast<const float4 *>(a.g_wxb + o + g * 16 + j);
-          const float4 h4 = *reinterpret_cast<const float4 *>(hp + g * 16 + j);
-          const float zz[4] = {z4.x, z4.y, z4.z, z4.w}, ww[4] = {w4.x, w4.y, w4.z, w4.w};
-          const float hh[4] = {h4.x, h4.y, h4.z, h4.w};
+        for (int j = 0; j < 4; ++j) {
+          const float zz[4] = {z4[j].x, z4[j].y, z4[j].z, z4[j].w};
+          const float ww[4] = {w4[j].x, w4[j].y, w4[j].z, w4[j].w};
+          const float hh[4] = {h4[j].x, h4[j].y, h4[j].z, h4[j].w};
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const float c = tanhf(ww[t] + vu[j + t]);
-            hn[j + t] = (1.0f - zz[t]) * hh[t] + zz[t] * c;
+            const float c = tanhf(ww[t] + vu[4 * j + t]);
+            hn[4 * j + t] = (1.0f - zz[t]) * hh[t] + zz[t] * c;
           }
         }
         float4 *so = reinterpret_cast<float4 *>(a.state_out + (size_t)dst * a.H + n0 + g * 16);
@@ -451,7 +535,9 @@ __global__ void __launch_bounds__(P2_THREADS, 1)
         uint4 *s16 = reinterpret_cast<uint4 *>(a.state16_out + (size_t)dst * a.H + n0 + g * 16);
         s16[0] = pk[0];
         s16[1] = pk[1];
+        if (a.cache) hs += encode16(a, hn, n0 + g * 16, code, signacc);
       }
+      if (a.cache && dst != NONE) atomicAdd(&a.codehash[dst], hs);
     }
   }
   tc_fence_before();
@@ -473,9 +559,9 @@ typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, 
 
 struct TcState {
   uint32_t E = 0, H = 0, nub = 0, bmax = 0;
-  __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr;
+  __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr, *a1 = nullptr;
   float *b1 = nullptr;
-  CUtensorMap map_w1x, map_w1h, map_w2, map_a2;
+  CUtensorMap map_w1x, map_w1h, map_w2, map_a2, map_a1;
   bool bound = false;
 };
 
@@ -556,7 +642,12 @@ int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax) {
   TcState *t = static_cast<TcState *>(state);
   t->rh16 = rh16;
   t->bmax = bmax;
-  t->bound = make_map(&t->map_a2, rh16, t->H, bmax, BM);
+  if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * 2) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -1;
+  }
+  t->bound = make_map(&t->map_a2, rh16, t->H, bmax, BM) &&
+             make_map(&t->map_a1, t->a1, t->E + t->H, bmax, BM);
   return t->bound ? 0 : -1;
 }
 
@@ -565,6 +656,7 @@ void gru_tc_release(void *state) {
   if (!t) return;
   cudaFree(t->w1);
   cudaFree(t->w2);
+  cudaFree(t->a1);
   cudaFree(t->b1);
   delete t;
 }
@@ -577,13 +669,18 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.emb16 = P.emb16; a.state16 = P.state16; a.state = P.state; a.b1 = t->b1;
   a.state16_out = P.state16; a.state_out = P.state;
   a.row_src = P.row_src; a.row_dst = P.row_dst; a.row_word = P.row_word; a.counts = P.counts;
-  a.g_z = P.g_z; a.g_wxb = P.g_wxb; a.g_rh16 = P.g_rh16;
+  a.g_z = P.g_z; a.g_wxb = P.g_wxb; a.g_rh16 = P.g_rh16; a.a1 = t->a1;
+  a.cache = P.cache; a.key_mode = P.key_mode; a.round_digits = P.round_digits;
+  a.cstride = P.cstride; a.round_scale = P.round_scale; a.codes = P.codes; a.codehash = P.codehash;
   const uint32_t mt = (max_rows + BM - 1) / BM;
   uint32_t g1 = mt * t->nub, g2 = mt * (P.H / N2);
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
   if (g2 > (uint32_t)num_sms) g2 = num_sms;
-  k_gru1_tc<<<g1, P1_THREADS, SMEM1, s>>>(t->map_w1x, t->map_w1h, a);
+  uint32_t gg = (max_rows + 7) / 8;
+  if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
+  k_gather_a1<<<gg, 256, 0, s>>>(a);
+  k_gru1_tc<<<g1, P1_THREADS, SMEM1, s>>>(t->map_a1, t->map_w1x, t->map_w1h, a);
   k_gru2_tc<<<g2, P2_THREADS, SMEM2, s>>>(t->map_a2, t->map_w2, a);
-  return 2;
+  return 3;
 }
 }  // namespace rnnlm_host

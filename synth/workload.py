@@ -15,9 +15,11 @@ hypotheses at word boundaries during frame-synchronous Viterbi search
   frames (word-end-time ambiguity), which is what the paper's LM-query cache
   removes (~89% hits).  Re-emissions fill each frame up to exactly
   B_s queries per session, so the hit ratio is ~ 1 - P*K/(mean_dur*B_s);
-* shared recent pasts: all paths of an utterance follow the same transcript
-  with independent substitutions, so histories that differ in an older word
-  share their recent words (what lossy history keys merge).
+* shared recent pasts: every path starts with ``private`` words of its own
+  (hypotheses that differ in earlier context), then all paths of an
+  utterance follow the same transcript with independent substitutions, so
+  histories that differ in an older word share their recent words (what
+  lossy history keys merge).
 
 Parents are expressed as *references to earlier queries* (``parent_ref`` =
 flat index of the query whose returned child handle is the parent history,
@@ -89,7 +91,7 @@ def _zipf_cdf(V: int, s: float) -> np.ndarray:
 def generate_workload(S: int, frames: int, B_s: int, V: int, seed: int = 7,
                       K: int = 8, dur: tuple = (10, 40), eps: float = 0.3,
                       window: int = 12, zipf_s: float = 1.0,
-                      qhit_target: float = 0.89) -> Workload:
+                      qhit_target: float = 0.87, private: int = 2) -> Workload:
     """Session s draws from its own generator seeded ``seed + s``."""
     assert V >= 2 and B_s >= 1 and S >= 1 and frames >= 0
     cdf = _zipf_cdf(V, zipf_s)
@@ -108,8 +110,11 @@ def generate_workload(S: int, frames: int, B_s: int, V: int, seed: int = 7,
     for s in range(S):
         rng = np.random.default_rng(seed + s)
         transcript = zipf(rng, frames // max(1, dur[0]) + 8)
+        # each path first emits `private` words of its own (hypotheses that
+        # differ in their earlier context), then follows the shared transcript
+        own = zipf(rng, P * private).reshape(P, private) if private else None
         path_ref = np.full(P, -1, dtype=np.int64)
-        path_pos = np.zeros(P, dtype=np.int64)
+        path_pos = np.full(P, -private, dtype=np.int64)
         next_b = rng.integers(0, dur[1], size=P)
         recent = []  # list of (parent_refs, words) of first emissions, last `window` frames
         for t in range(frames):
@@ -122,7 +127,10 @@ def generate_workload(S: int, frames: int, B_s: int, V: int, seed: int = 7,
             nb = len(bpaths)
             if nb:
                 cand = zipf(rng, nb * K).reshape(nb, K)
-                cand[:, 0] = transcript[np.minimum(path_pos[bpaths], len(transcript) - 1)]
+                pos = path_pos[bpaths]
+                cand[:, 0] = np.where(
+                    pos < 0, own[bpaths, np.clip(pos + private, 0, private - 1)] if private else 0,
+                    transcript[np.clip(pos, 0, len(transcript) - 1)])
                 new_par = np.repeat(path_ref[bpaths], K)
                 new_w = cand.reshape(-1)
             else:
