@@ -260,9 +260,12 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   chk(dalloc(h, &P.tile_ticket, 1));
   chk(dalloc(h, &P.counts, 4));
   chk(dalloc(h, &P.g_z, B * H));
-  chk(dalloc(h, &P.g_wxb, B * H));
-  if (c.math == RNNLM_MATH_FP32) chk(dalloc(h, &P.g_rh, B * H));
-  else chk(dalloc(h, &P.g_rh16, B * H));
+  if (c.math == RNNLM_MATH_FP32) {
+    chk(dalloc(h, &P.g_wxb, B * H));
+    chk(dalloc(h, &P.g_rh, B * H));
+  } else {
+    chk(dalloc(h, &P.g_rh16, B * H));
+  }
   if (st == RNNLM_OK && c.math == RNNLM_MATH_BF16 && rnnlm_host::gru_tc_bind(h->tc, P.g_rh16, (uint32_t)B) != 0)
     st = RNNLM_E_CUDA;
   if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.sticky, 0, sizeof(int))));

@@ -6,25 +6,27 @@
 //
 //   gather   A1[r] = [x | h] (x = E[word] bf16, h = bf16 shadow of the parent
 //            state), one warp per row, 16-byte vector copies (k_gather_a1).
-//   phase 1  A = A1 via TMA, B = gate-interleaved weights W1 [H/64 x 192
-//            rows][E+H] bf16 via TMA (per 64-unit block: 64 rows z, 64 rows r,
-//            64 rows h; the h rows are zero on the recurrent half, so those K
-//            chunks issue N = 128 MMAs and load only the z/r rows).  Tile
-//            128 x 192, fp32 accumulators in TMEM (two buffers of 256 columns:
-//            the epilogue of tile i overlaps the MMAs of tile i+1).  Epilogue:
-//            z = s(.+bz), r = s(.+br) -> r.h (bf16, phase-2 A), Wh x + bh (fp32).
-//   phase 2  A = r.h rows via TMA, B = Uh [H][H] bf16 via TMA, tile 128 x 256;
-//            epilogue: c = tanh(Wh x + bh + Uh(r.h)), h' = (1-z) h + z c, the
-//            new fp32 state, its bf16 shadow, and (a1) its compression code +
-//            code-hash contribution (hash terms add, so the four N-tiles of a
-//            row combine with one 64-bit atomicAdd each, order-independent).
+//   phase 1  z, r: A = A1 (TMA), B = W1 [(H/128) x 256 rows][E+H] bf16 (TMA;
+//            per 128-unit block 128 rows [Wz|Uz] then 128 rows [Wr|Ur]),
+//            tile 128 x 256, K = E+H.  Epilogue: z = s(.+bz) (fp32) and
+//            r.h = s(.+br) * h (bf16, phase-2 A operand).
+//   phase 2  candidate: A = [x | r.h] (x chunks from A1, recurrent chunks from
+//            the r.h rows, both TMA), B = W2 [H rows][E+H] = [Wh | Uh] (TMA),
+//            tile 128 x 256, K = E+H: the accumulator is Wh x + Uh (r.h)
+//            directly (no fp32 round trip of Wh x).  Epilogue:
+//            c = tanh(. + bh), h' = (1-z) h + z c, the new fp32 state, its bf16
+//            shadow, and (a1) its compression code + code-hash contribution
+//            (hash terms add, so the N-tiles of a row combine with one 64-bit
+//            atomicAdd each, order-independent).
 //
 // Both GEMM kernels are persistent (grid <= #SMs), warp-specialised: one TMA
 // producer thread, one MMA-issuing thread (tcgen05.mma.cta_group::1.kind::f16,
-// M = 128), eight epilogue warps (tcgen05.ld.32x32b: TMEM lane quarter =
-// warp % 4, two warps per quarter split the columns).  Pipelines are mbarrier
-// rings (full / empty per smem stage, full / empty per TMEM accumulator).
-// Rows >= Q read stale A rows and are discarded.
+// M = 128, N = 256), eight epilogue warps (tcgen05.ld.32x32b: TMEM lane
+// quarter = warp % 4, two warps per quarter split the columns).  Pipelines
+// are mbarrier rings (full / empty per smem stage, full / empty per TMEM
+// accumulator; two 256-column accumulators, so the epilogue of tile i
+// overlaps the MMAs of tile i+1).  Rows >= Q read stale A rows and are
+// discarded.
 #include <cuda.h>
 
 #include <cstring>
@@ -37,14 +39,11 @@ using namespace rnnlm_dev;
 
 constexpr int BM = 128;          // UMMA M (rows per tile)
 constexpr int BK = 64;           // K elements per smem stage (= one 128-byte swizzle atom)
-constexpr int N1 = 192;          // phase-1 tile N (z, r, h of 64 units)
-constexpr int N1H = 128;         // phase-1 N on recurrent K chunks (z, r only)
-constexpr int N2 = 256;          // phase-2 tile N (units)
-constexpr int ST1 = 4;           // phase-1 smem stages
-constexpr int ST2 = 4;           // phase-2 smem stages
+constexpr int UB = 128;          // units per phase-1 block
+constexpr int BN = 256;          // UMMA N of both phases (phase 1: z|r of 128 units; phase 2: 256 units)
+constexpr int ST = 4;            // smem pipeline stages
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
-constexpr int B1_BYTES = N1 * BK * 2;         // 24 KB
-constexpr int B2_BYTES = N2 * BK * 2;         // 32 KB
+constexpr int B_BYTES = BN * BK * 2;          // 32 KB
 constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 columns
 
 // ---------------------------------------------------------------- PTX helpers
@@ -150,16 +149,17 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 __device__ __forceinline__ float sigm(float a) { return 1.0f / (1.0f + __expf(-a)); }
 
 struct TcArgs {
-  uint32_t E, H, nub;
+  uint32_t E, H, nub;              // nub = H / 128 phase-1 unit blocks
   const __nv_bfloat16 *emb16;
   const __nv_bfloat16 *state16;
   const float *state;
-  const float *b1;                 // [nub][3][64]
+  const float *bzr;                // [nub][2][128] (bz, br)
+  const float *bh;                 // [H]
   __nv_bfloat16 *state16_out;
   float *state_out;
   const uint32_t *row_src, *row_dst, *row_word, *counts;
-  float *g_z, *g_wxb;
-  __nv_bfloat16 *g_rh16;
+  float *g_z;                      // [B_max][H]
+  __nv_bfloat16 *g_rh16;           // [B_max][H]
   __nv_bfloat16 *a1;               // [B_max][E+H] gathered phase-1 A operand
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
@@ -187,46 +187,92 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
   }
 }
 
-// =============================================================== phase 1
-// warp 0: TMA producer (A rows + gate-interleaved weights)
-// warp 1: TMEM allocation + MMA issue
-// warps 2-9: epilogue; TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
 constexpr int EPI_WARPS = 8;
-constexpr int P1_THREADS = (2 + EPI_WARPS) * 32;
-constexpr int P2_THREADS = (2 + EPI_WARPS) * 32;
+constexpr int THREADS = (2 + EPI_WARPS) * 32;
 
-__global__ void __launch_bounds__(P1_THREADS, 1)
-    k_gru1_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1x,
-              const __grid_constant__ CUtensorMap map_w1h, TcArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sA = smem;                                   // ST1 x 16 KB
-  uint8_t *sB = smem + ST1 * A_BYTES;                   // ST1 x 24 KB
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + ST1 * B1_BYTES);
-  uint64_t *empty = full + ST1;
-  uint64_t *tfull = empty + ST1;
-  uint64_t *tempty = tfull + 2;
-  uint32_t *tmem_base_sm = reinterpret_cast<uint32_t *>(tempty + 2);
+struct Smem {
+  uint8_t *sA, *sB;
+  uint64_t *full, *empty, *tfull, *tempty;
+  uint32_t *tmem_base;
+};
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t Q = a.counts[1];
-  const uint32_t mt = (Q + BM - 1) / BM;
-  const uint32_t ntiles = mt * a.nub;
-  const uint32_t kx = a.E / BK, kh = a.H / BK, KC = kx + kh;
+__device__ __forceinline__ Smem carve(uint8_t *raw) {
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  Smem m;
+  m.sA = smem;
+  m.sB = smem + ST * A_BYTES;
+  m.full = reinterpret_cast<uint64_t *>(m.sB + ST * B_BYTES);
+  m.empty = m.full + ST;
+  m.tfull = m.empty + ST;
+  m.tempty = m.tfull + 2;
+  m.tmem_base = reinterpret_cast<uint32_t *>(m.tempty + 2);
+  return m;
+}
 
+__device__ __forceinline__ void setup(const Smem &m, int warp) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST1; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS * 32); }
+    for (int s = 0; s < ST; ++s) { mbar_init(&m.full[s], 1); mbar_init(&m.empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&m.tfull[s], 1); mbar_init(&m.tempty[s], EPI_WARPS * 32); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    prefetch_map(&map_a1);
-    prefetch_map(&map_w1x);
-    prefetch_map(&map_w1h);
   }
-  if (warp == 1) tmem_alloc(tmem_base_sm, TMEM_COLS);
+  if (warp == 1) tmem_alloc(m.tmem_base, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_base_sm;
+}
+
+__device__ __forceinline__ void teardown(const Smem &m, int warp, uint32_t tmem_base) {
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// MMA issuer shared by both phases: KC chunks of 4 x (M=128, N=256, K=16).
+__device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t ntiles,
+                                         uint32_t KC, int lane) {
+  uint32_t stage = 0, phase = 0, it = 0;
+  const uint32_t id = idesc_bf16(BM, BN);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const uint32_t acc = it & 1;
+    mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
+    tc_fence_after();
+    const uint32_t tm = tmem_base + acc * BN;
+    for (uint32_t kc = 0; kc < KC; ++kc) {
+      mbar_wait(&m.full[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+        umma_commit(&m.empty[stage]);
+        if (kc == KC - 1) umma_commit(&m.tfull[acc]);
+      }
+      __syncwarp();
+      if (++stage == ST) { stage = 0; phase ^= 1; }
+    }
+  }
+}
+
+// =============================================================== phase 1
+// warp 0: TMA producer; warp 1: TMEM allocation + MMA issue;
+// warps 2-9: epilogue, TMEM lane quarter = warp % 4; warps 2-5 own the z
+// columns, warps 6-9 the r columns of the 128-unit block.
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gru1_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1,
+              TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem m = carve(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t Q = a.counts[1];
+  const uint32_t ntiles = ((Q + BM - 1) / BM) * a.nub;
+  const uint32_t KC = (a.E + a.H) / BK;
+  if (threadIdx.x == 0) { prefetch_map(&map_a1); prefetch_map(&map_w1); }
+  setup(m, warp);
+  const uint32_t tmem_base = *m.tmem_base;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -234,114 +280,72 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
       for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t m0 = (tile / a.nub) * BM, ub = tile % a.nub;
         for (uint32_t kc = 0; kc < KC; ++kc) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t dA = smem_u32(sA + stage * A_BYTES), dB = smem_u32(sB + stage * B1_BYTES);
-          if (kc < kx) {
-            mbar_expect_tx(&full[stage], A_BYTES + N1 * BK * 2);
-            tma_load_2d(dB, &map_w1x, &full[stage], (int)(kc * BK), (int)(ub * N1));
-          } else {
-            mbar_expect_tx(&full[stage], A_BYTES + N1H * BK * 2);
-            tma_load_2d(dB, &map_w1h, &full[stage], (int)(kc * BK), (int)(ub * N1));
-          }
-          tma_load_2d(dA, &map_a1, &full[stage], (int)(kc * BK), (int)m0);
-          if (++stage == ST1) { stage = 0; phase ^= 1; }
+          mbar_wait(&m.empty[stage], phase ^ 1);
+          mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
+          tma_load_2d(smem_u32(m.sA + stage * A_BYTES), &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
+          tma_load_2d(smem_u32(m.sB + stage * B_BYTES), &map_w1, &m.full[stage], (int)(kc * BK), (int)(ub * BN));
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    uint32_t stage = 0, phase = 0, it = 0;
-    const uint32_t id_x = idesc_bf16(BM, N1), id_h = idesc_bf16(BM, N1H);
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t acc = it & 1;
-      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t tm = tmem_base + acc * 256;
-      for (uint32_t kc = 0; kc < KC; ++kc) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B1_BYTES);
-          const uint32_t id = kc < kx ? id_x : id_h;
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
-          umma_commit(&empty[stage]);
-          if (kc == KC - 1) umma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-        if (++stage == ST1) { stage = 0; phase ^= 1; }
-      }
-    }
+    mma_loop(m, tmem_base, ntiles, KC, lane);
   } else {
-    // ------------------------------------------------ epilogue
-    const int q = warp & 3;                             // TMEM lane quarter
-    const int half = (warp - 2) >> 2;                   // 32-unit half of the 64-unit block
+    const int q = warp & 3;
+    const int gate = (warp - 2) >> 2;                   // 0: z columns, 1: r columns
     const int r_in = q * 32 + lane;
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
       const uint32_t m0 = (tile / a.nub) * BM, ub = tile % a.nub;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      mbar_wait(&m.tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t row = m0 + r_in;
       const bool valid = row < Q;
-      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16) + half * 32;
-      const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * 64 + half * 32;
-      const float *bb = a.b1 + (size_t)ub * 192 + half * 32;
-      const size_t o = (size_t)row * a.H + ub * 64 + half * 32;
-      float vz[2][16], vr[2][16], vx[2][16];
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + gate * UB;
+      const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB;
+      const size_t o = (size_t)(valid ? row : 0) * a.H + ub * UB;
+      const __nv_bfloat16 *h16 = a.state16 + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * UB;
+#pragma unroll 1
+      for (int g = 0; g < UB / 16; ++g) {
+        float v[16];
+        tmem_ld16(tbase + g * 16, v);
+        uint4 hb[2];
+        if (gate == 1 && valid) {
+          hb[0] = *reinterpret_cast<const uint4 *>(h16 + g * 16);
+          hb[1] = *reinterpret_cast<const uint4 *>(h16 + g * 16 + 8);
+        }
+        tmem_ld_wait();
+        if (g == UB / 16 - 1) {                         // accumulator drained
+          tc_fence_before();
+          mbar_arrive(&m.tempty[acc]);
+        }
+        if (!valid) continue;
+        float s[16];
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        tmem_ld16(tbase + g * 16, vz[g]);
-        tmem_ld16(tbase + 64 + g * 16, vr[g]);
-        tmem_ld16(tbase + 128 + g * 16, vx[g]);
-      }
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);                        // accumulator drained
-      if (!valid) continue;
+        for (int j = 0; j < 16; ++j) s[j] = sigm(v[j] + __ldg(bias + g * 16 + j));
+        if (gate == 0) {
+          float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        float z[16], rh[16], wx[16];
+          for (int j = 0; j < 4; ++j) gz[j] = make_float4(s[4 * j], s[4 * j + 1], s[4 * j + 2], s[4 * j + 3]);
+        } else {
+          const uint32_t *hw = reinterpret_cast<const uint32_t *>(hb);
+          uint4 pk[2];
+          uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
 #pragma unroll
-        for (int j = 0; j < 16; j += 4) {
-          const float4 hv = *reinterpret_cast<const float4 *>(hp + g * 16 + j);
-          const float hh[4] = {hv.x, hv.y, hv.z, hv.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int u = g * 16 + j + t;
-            z[j + t] = sigm(vz[g][j + t] + __ldg(bb + u));
-            rh[j + t] = sigm(vr[g][j + t] + __ldg(bb + 64 + u)) * hh[t];
-            wx[j + t] = vx[g][j + t] + __ldg(bb + 128 + u);
+          for (int j = 0; j < 8; ++j) {
+            const float h0 = __uint_as_float(hw[j] << 16), h1 = __uint_as_float(hw[j] & 0xFFFF0000u);
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(s[2 * j] * h0, s[2 * j + 1] * h1);
+            pw[j] = *reinterpret_cast<uint32_t *>(&t2);
           }
+          uint4 *gr = reinterpret_cast<uint4 *>(a.g_rh16 + o + g * 16);
+          gr[0] = pk[0];
+          gr[1] = pk[1];
         }
-        float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
-        float4 *gw = reinterpret_cast<float4 *>(a.g_wxb + o + g * 16);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          gz[j] = make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
-          gw[j] = make_float4(wx[4 * j], wx[4 * j + 1], wx[4 * j + 2], wx[4 * j + 3]);
-        }
-        uint4 pk[2];
-        uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          __nv_bfloat162 t2 = __floats2bfloat162_rn(rh[2 * j], rh[2 * j + 1]);
-          pw[j] = *reinterpret_cast<uint32_t *>(&t2);
-        }
-        uint4 *gr = reinterpret_cast<uint4 *>(a.g_rh16 + o + g * 16);
-        gr[0] = pk[0];
-        gr[1] = pk[1];
       }
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
-  }
+  teardown(m, warp, tmem_base);
 }
 
 // Compression code words of 16 consecutive new-state elements starting at
@@ -400,76 +404,39 @@ __device__ __forceinline__ unsigned long long encode16(const TcArgs &a, const fl
 
 // =============================================================== phase 2
 // warp 0: TMA producer; warp 1: TMEM alloc + MMA; warps 2-9: epilogue
-__global__ void __launch_bounds__(P2_THREADS, 1)
-    k_gru2_tc(const __grid_constant__ CUtensorMap map_a2, const __grid_constant__ CUtensorMap map_w2,
-              TcArgs a) {
+// (two warps per TMEM lane quarter, 128 units each).
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gru2_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_rh,
+              const __grid_constant__ CUtensorMap map_w2, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sA = smem;
-  uint8_t *sB = smem + ST2 * A_BYTES;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + ST2 * B2_BYTES);
-  uint64_t *empty = full + ST2;
-  uint64_t *tfull = empty + ST2;
-  uint64_t *tempty = tfull + 2;
-  uint32_t *tmem_base_sm = reinterpret_cast<uint32_t *>(tempty + 2);
-
+  const Smem m = carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Q = a.counts[1];
-  const uint32_t mt = (Q + BM - 1) / BM;
-  const uint32_t nt = a.H / N2;
-  const uint32_t ntiles = mt * nt;
-  const uint32_t KC = a.H / BK;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ST2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS * 32); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    prefetch_map(&map_a2);
-    prefetch_map(&map_w2);
-  }
-  if (warp == 1) tmem_alloc(tmem_base_sm, TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_base_sm;
+  const uint32_t nt = a.H / BN;
+  const uint32_t ntiles = ((Q + BM - 1) / BM) * nt;
+  const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
+  if (threadIdx.x == 0) { prefetch_map(&map_a1); prefetch_map(&map_rh); prefetch_map(&map_w2); }
+  setup(m, warp);
+  const uint32_t tmem_base = *m.tmem_base;
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t m0 = (tile / nt) * BM, n0 = (tile % nt) * N2;
+        const uint32_t m0 = (tile / nt) * BM, n0 = (tile % nt) * BN;
         for (uint32_t kc = 0; kc < KC; ++kc) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], A_BYTES + B2_BYTES);
-          tma_load_2d(smem_u32(sA + stage * A_BYTES), &map_a2, &full[stage], (int)(kc * BK), (int)m0);
-          tma_load_2d(smem_u32(sB + stage * B2_BYTES), &map_w2, &full[stage], (int)(kc * BK), (int)n0);
-          if (++stage == ST2) { stage = 0; phase ^= 1; }
+          mbar_wait(&m.empty[stage], phase ^ 1);
+          mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
+          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES);
+          if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
+          else tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BK), (int)m0);
+          tma_load_2d(smem_u32(m.sB + stage * B_BYTES), &map_w2, &m.full[stage], (int)(kc * BK), (int)n0);
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    uint32_t stage = 0, phase = 0, it = 0;
-    const uint32_t id = idesc_bf16(BM, N2);
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t acc = it & 1;
-      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t tm = tmem_base + acc * 256;
-      for (uint32_t kc = 0; kc < KC; ++kc) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B2_BYTES);
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
-          umma_commit(&empty[stage]);
-          if (kc == KC - 1) umma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-        if (++stage == ST2) { stage = 0; phase ^= 1; }
-      }
-    }
+    mma_loop(m, tmem_base, ntiles, KC, lane);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;                   // 128-unit half of the 256-unit tile
@@ -478,13 +445,13 @@ __global__ void __launch_bounds__(P2_THREADS, 1)
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
       const uint32_t m0 = (tile / nt) * BM;
-      const uint32_t n0 = (tile % nt) * N2 + half * (N2 / 2);
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      const uint32_t n0 = (tile % nt) * BN + half * (BN / 2);
+      mbar_wait(&m.tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t row = m0 + r_in;
       const bool valid = row < Q;
       const uint32_t dst = valid ? a.row_dst[row] : NONE;
-      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16) + half * (N2 / 2);
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
       const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + n0;
       const size_t o = (size_t)(valid ? row : 0) * a.H + n0;
       uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && dst != NONE)
@@ -492,33 +459,31 @@ __global__ void __launch_bounds__(P2_THREADS, 1)
       unsigned long long hs = 0;
       uint32_t signacc = 0;
 #pragma unroll 1
-      for (int g = 0; g < N2 / 32; ++g) {
+      for (int g = 0; g < BN / 32; ++g) {
         float vu[16];
         tmem_ld16(tbase + g * 16, vu);
-        float4 z4[4], w4[4], h4[4];
+        float4 z4[4], h4[4];
         if (dst != NONE) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             z4[j] = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + 4 * j);
-            w4[j] = *reinterpret_cast<const float4 *>(a.g_wxb + o + g * 16 + 4 * j);
             h4[j] = *reinterpret_cast<const float4 *>(hp + g * 16 + 4 * j);
           }
         }
         tmem_ld_wait();
-        if (g == N2 / 32 - 1) {
+        if (g == BN / 32 - 1) {
           tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          mbar_arrive(&m.tempty[acc]);
         }
         if (dst == NONE) continue;
         float hn[16];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float zz[4] = {z4[j].x, z4[j].y, z4[j].z, z4[j].w};
-          const float ww[4] = {w4[j].x, w4[j].y, w4[j].z, w4[j].w};
           const float hh[4] = {h4[j].x, h4[j].y, h4[j].z, h4[j].w};
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const float c = tanhf(ww[t] + vu[4 * j + t]);
+            const float c = tanhf(vu[4 * j + t] + __ldg(a.bh + n0 + g * 16 + 4 * j + t));
             hn[4 * j + t] = (1.0f - zz[t]) * hh[t] + zz[t] * c;
           }
         }
@@ -540,16 +505,10 @@ __global__ void __launch_bounds__(P2_THREADS, 1)
       if (a.cache && dst != NONE) atomicAdd(&a.codehash[dst], hs);
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
-  }
+  teardown(m, warp, tmem_base);
 }
 
-constexpr size_t SMEM1 = 1024 + ST1 * (A_BYTES + B1_BYTES) + 256;
-constexpr size_t SMEM2 = 1024 + ST2 * (A_BYTES + B2_BYTES) + 256;
+constexpr size_t SMEM = 1024 + ST * (A_BYTES + B_BYTES) + 256;
 
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -560,8 +519,8 @@ typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, 
 struct TcState {
   uint32_t E = 0, H = 0, nub = 0, bmax = 0;
   __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr, *a1 = nullptr;
-  float *b1 = nullptr;
-  CUtensorMap map_w1x, map_w1h, map_w2, map_a2, map_a1;
+  float *bzr = nullptr, *bh = nullptr;
+  CUtensorMap map_w1, map_w2, map_a1, map_rh;
   bool bound = false;
 };
 
@@ -577,6 +536,7 @@ static EncodeTiled get_encode() {
   return fn;
 }
 
+// 2D bf16 tensor [outer][inner], box {64, box_outer}, 128-byte swizzle.
 static bool make_map(CUtensorMap *m, void *base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
   EncodeTiled enc = get_encode();
   if (!enc) return false;
@@ -595,40 +555,44 @@ namespace rnnlm_host {
 using namespace rnnlm_tc;
 
 int gru_tc_supported(uint32_t E, uint32_t H) {
-  return E % 64 == 0 && H % N2 == 0 && E >= 64 && H >= N2;
+  return E % BK == 0 && H % BN == 0 && E >= BK && H >= BN;
 }
 
 int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_out) {
   *state_out = nullptr;
   TcState *t = new TcState;
-  t->E = E; t->H = H; t->nub = H / 64;
-  const size_t K1 = E + H, R1 = (size_t)t->nub * N1;
-  std::vector<__nv_bfloat16> w1(R1 * K1, __float2bfloat16_rn(0.0f)), w2((size_t)H * H);
-  std::vector<float> b1((size_t)t->nub * 192);
-  const float *Wg[3] = {w->Wz, w->Wr, w->Wh};
+  t->E = E; t->H = H; t->nub = H / UB;
+  const size_t K1 = E + H;
+  std::vector<__nv_bfloat16> w1((size_t)2 * H * K1), w2((size_t)H * K1);
+  std::vector<float> bzr((size_t)2 * H), bh(H);
+  const float *Wg[2] = {w->Wz, w->Wr};
   const float *Ug[2] = {w->Uz, w->Ur};
-  const float *bg[3] = {w->bz, w->br, w->bh};
+  const float *bg[2] = {w->bz, w->br};
   for (size_t u = 0; u < H; ++u) {
-    const size_t ub = u / 64, uu = u % 64;
-    for (int g = 0; g < 3; ++g) {
-      __nv_bfloat16 *row = w1.data() + (ub * N1 + g * 64 + uu) * K1;
+    const size_t ub = u / UB, uu = u % UB;
+    for (int g = 0; g < 2; ++g) {
+      __nv_bfloat16 *row = w1.data() + (ub * BN + g * UB + uu) * K1;
       for (size_t k = 0; k < E; ++k) row[k] = __float2bfloat16_rn(Wg[g][u * E + k]);
-      if (g < 2)
-        for (size_t k = 0; k < H; ++k) row[E + k] = __float2bfloat16_rn(Ug[g][u * H + k]);
-      b1[ub * 192 + g * 64 + uu] = bg[g][u];
+      for (size_t k = 0; k < H; ++k) row[E + k] = __float2bfloat16_rn(Ug[g][u * H + k]);
+      bzr[ub * BN + g * UB + uu] = bg[g][u];
     }
-    for (size_t k = 0; k < H; ++k) w2[u * H + k] = __float2bfloat16_rn(w->Uh[u * H + k]);
+    __nv_bfloat16 *row2 = w2.data() + u * K1;
+    for (size_t k = 0; k < E; ++k) row2[k] = __float2bfloat16_rn(w->Wh[u * E + k]);
+    for (size_t k = 0; k < H; ++k) row2[E + k] = __float2bfloat16_rn(w->Uh[u * H + k]);
+    bh[u] = w->bh[u];
   }
   bool ok = cudaMalloc(&t->w1, w1.size() * 2) == cudaSuccess &&
             cudaMalloc(&t->w2, w2.size() * 2) == cudaSuccess &&
-            cudaMalloc(&t->b1, b1.size() * 4) == cudaSuccess;
+            cudaMalloc(&t->bzr, bzr.size() * 4) == cudaSuccess &&
+            cudaMalloc(&t->bh, bh.size() * 4) == cudaSuccess;
   ok = ok && cudaMemcpy(t->w1, w1.data(), w1.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(t->w2, w2.data(), w2.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess;
-  ok = ok && cudaMemcpy(t->b1, b1.data(), b1.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
-  ok = ok && make_map(&t->map_w1x, t->w1, K1, R1, N1) && make_map(&t->map_w1h, t->w1, K1, R1, N1H) &&
-       make_map(&t->map_w2, t->w2, H, H, N2);
-  ok = ok && cudaFuncSetAttribute(k_gru1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM1) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2) == cudaSuccess;
+  ok = ok && cudaMemcpy(t->bzr, bzr.data(), bzr.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && cudaMemcpy(t->bh, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && make_map(&t->map_w1, t->w1, K1, 2 * (uint64_t)H, BN) &&
+       make_map(&t->map_w2, t->w2, K1, H, BN);
+  ok = ok && cudaFuncSetAttribute(k_gru1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   *state_out = t;
   if (!ok) {
     (void)cudaGetLastError();
@@ -637,7 +601,7 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_
   return 0;
 }
 
-// The phase-2 A operand map needs the r.h scratch; bound once per engine.
+// The activation maps need the engine's scratch; bound once per engine.
 int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax) {
   TcState *t = static_cast<TcState *>(state);
   t->rh16 = rh16;
@@ -646,7 +610,7 @@ int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax) {
     (void)cudaGetLastError();
     return -1;
   }
-  t->bound = make_map(&t->map_a2, rh16, t->H, bmax, BM) &&
+  t->bound = make_map(&t->map_rh, rh16, t->H, bmax, BM) &&
              make_map(&t->map_a1, t->a1, t->E + t->H, bmax, BM);
   return t->bound ? 0 : -1;
 }
@@ -657,7 +621,8 @@ void gru_tc_release(void *state) {
   cudaFree(t->w1);
   cudaFree(t->w2);
   cudaFree(t->a1);
-  cudaFree(t->b1);
+  cudaFree(t->bzr);
+  cudaFree(t->bh);
   delete t;
 }
 
@@ -666,21 +631,21 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   if (!max_rows || !t || !t->bound) return 0;
   TcArgs a;
   a.E = P.E; a.H = P.H; a.nub = t->nub;
-  a.emb16 = P.emb16; a.state16 = P.state16; a.state = P.state; a.b1 = t->b1;
+  a.emb16 = P.emb16; a.state16 = P.state16; a.state = P.state; a.bzr = t->bzr; a.bh = t->bh;
   a.state16_out = P.state16; a.state_out = P.state;
   a.row_src = P.row_src; a.row_dst = P.row_dst; a.row_word = P.row_word; a.counts = P.counts;
-  a.g_z = P.g_z; a.g_wxb = P.g_wxb; a.g_rh16 = P.g_rh16; a.a1 = t->a1;
+  a.g_z = P.g_z; a.g_rh16 = P.g_rh16; a.a1 = t->a1;
   a.cache = P.cache; a.key_mode = P.key_mode; a.round_digits = P.round_digits;
   a.cstride = P.cstride; a.round_scale = P.round_scale; a.codes = P.codes; a.codehash = P.codehash;
   const uint32_t mt = (max_rows + BM - 1) / BM;
-  uint32_t g1 = mt * t->nub, g2 = mt * (P.H / N2);
+  uint32_t g1 = mt * t->nub, g2 = mt * (P.H / BN);
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
   if (g2 > (uint32_t)num_sms) g2 = num_sms;
   uint32_t gg = (max_rows + 7) / 8;
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
   k_gather_a1<<<gg, 256, 0, s>>>(a);
-  k_gru1_tc<<<g1, P1_THREADS, SMEM1, s>>>(t->map_a1, t->map_w1x, t->map_w1h, a);
-  k_gru2_tc<<<g2, P2_THREADS, SMEM2, s>>>(t->map_a2, t->map_w2, a);
+  k_gru1_tc<<<g1, THREADS, SMEM, s>>>(t->map_a1, t->map_w1, a);
+  k_gru2_tc<<<g2, THREADS, SMEM, s>>>(t->map_a1, t->map_rh, t->map_w2, a);
   return 3;
 }
 }  // namespace rnnlm_host
