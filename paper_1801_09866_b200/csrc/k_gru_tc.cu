@@ -146,7 +146,19 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ float sigm(float a) { return 1.0f / (1.0f + __expf(-a)); }
+__device__ __forceinline__ float sigm(float a) { return __fdividef(1.0f, 1.0f + __expf(-a)); }
+// tanh via exp (relative error ~1e-6; the bf16 path's bar is 1e-3)
+__device__ __forceinline__ float tanh_fast(float a) {
+  const float e = __expf(2.0f * fminf(fmaxf(a, -15.0f), 15.0f));
+  return __fdividef(e - 1.0f, e + 1.0f);
+}
+__device__ __forceinline__ void ld_bias16(const float *p, float *b) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(p) + j);
+    b[4 * j] = v.x; b[4 * j + 1] = v.y; b[4 * j + 2] = v.z; b[4 * j + 3] = v.w;
+  }
+}
 
 struct TcArgs {
   uint32_t E, H, nub;              // nub = H / 128 phase-1 unit blocks
@@ -306,28 +318,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB;
       const size_t o = (size_t)(valid ? row : 0) * a.H + ub * UB;
       const __nv_bfloat16 *h16 = a.state16 + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * UB;
-#pragma unroll 1
-      for (int g = 0; g < UB / 16; ++g) {
-        float v[16];
-        tmem_ld16(tbase + g * 16, v);
-        uint4 hb[2];
+      // TMEM loads are double-buffered: group g+1 is in flight while g is processed
+      auto process = [&](int g, const float *v) {
+        float bias16[16];
+        ld_bias16(bias + g * 16, bias16);
+        uint4 hb[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
         if (gate == 1 && valid) {
           hb[0] = *reinterpret_cast<const uint4 *>(h16 + g * 16);
           hb[1] = *reinterpret_cast<const uint4 *>(h16 + g * 16 + 8);
         }
-        tmem_ld_wait();
-        if (g == UB / 16 - 1) {                         // accumulator drained
-          tc_fence_before();
-          mbar_arrive(&m.tempty[acc]);
-        }
-        if (!valid) continue;
-        float s[16];
+        float sg[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) s[j] = sigm(v[j] + __ldg(bias + g * 16 + j));
+        for (int j = 0; j < 16; ++j) sg[j] = sigm(v[j] + bias16[j]);
+        if (!valid) return;
         if (gate == 0) {
           float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) gz[j] = make_float4(s[4 * j], s[4 * j + 1], s[4 * j + 2], s[4 * j + 3]);
+          for (int j = 0; j < 4; ++j) gz[j] = make_float4(sg[4 * j], sg[4 * j + 1], sg[4 * j + 2], sg[4 * j + 3]);
         } else {
           const uint32_t *hw = reinterpret_cast<const uint32_t *>(hb);
           uint4 pk[2];
@@ -335,14 +342,28 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const float h0 = __uint_as_float(hw[j] << 16), h1 = __uint_as_float(hw[j] & 0xFFFF0000u);
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(s[2 * j] * h0, s[2 * j + 1] * h1);
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(sg[2 * j] * h0, sg[2 * j + 1] * h1);
             pw[j] = *reinterpret_cast<uint32_t *>(&t2);
           }
           uint4 *gr = reinterpret_cast<uint4 *>(a.g_rh16 + o + g * 16);
           gr[0] = pk[0];
           gr[1] = pk[1];
         }
+      };
+      float va[16], vb[16];
+      tmem_ld16(tbase, va);
+      tmem_ld_wait();
+#pragma unroll 1
+      for (int g = 0; g < UB / 16; g += 2) {
+        tmem_ld16(tbase + (g + 1) * 16, vb);
+        process(g, va);
+        tmem_ld_wait();
+        if (g + 2 < UB / 16) tmem_ld16(tbase + (g + 2) * 16, va);
+        process(g + 1, vb);
+        tmem_ld_wait();
       }
+      tc_fence_before();
+      mbar_arrive(&m.tempty[acc]);                      // accumulator drained
     }
   }
   teardown(m, warp, tmem_base);
@@ -458,24 +479,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                           ? a.codes + (size_t)dst * a.cstride : nullptr;
       unsigned long long hs = 0;
       uint32_t signacc = 0;
-#pragma unroll 1
-      for (int g = 0; g < BN / 32; ++g) {
-        float vu[16];
-        tmem_ld16(tbase + g * 16, vu);
+      auto process = [&](int g, const float *vu) {
+        if (dst == NONE) return;
+        float bias16[16];
+        ld_bias16(a.bh + n0 + g * 16, bias16);
         float4 z4[4], h4[4];
-        if (dst != NONE) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            z4[j] = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + 4 * j);
-            h4[j] = *reinterpret_cast<const float4 *>(hp + g * 16 + 4 * j);
-          }
+        for (int j = 0; j < 4; ++j) {
+          z4[j] = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + 4 * j);
+          h4[j] = *reinterpret_cast<const float4 *>(hp + g * 16 + 4 * j);
         }
-        tmem_ld_wait();
-        if (g == BN / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&m.tempty[acc]);
-        }
-        if (dst == NONE) continue;
         float hn[16];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -483,7 +496,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const float hh[4] = {h4[j].x, h4[j].y, h4[j].z, h4[j].w};
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const float c = tanhf(vu[4 * j + t] + __ldg(a.bh + n0 + g * 16 + 4 * j + t));
+            const float c = tanh_fast(vu[4 * j + t] + bias16[4 * j + t]);
             hn[4 * j + t] = (1.0f - zz[t]) * hh[t] + zz[t] * c;
           }
         }
@@ -501,7 +514,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         s16[0] = pk[0];
         s16[1] = pk[1];
         if (a.cache) hs += encode16(a, hn, n0 + g * 16, code, signacc);
+      };
+      float va[16], vb[16];
+      tmem_ld16(tbase, va);
+      tmem_ld_wait();
+#pragma unroll 1
+      for (int g = 0; g < BN / 32; g += 2) {
+        tmem_ld16(tbase + (g + 1) * 16, vb);
+        process(g, va);
+        tmem_ld_wait();
+        if (g + 2 < BN / 32) tmem_ld16(tbase + (g + 2) * 16, va);
+        process(g + 1, vb);
+        tmem_ld_wait();
       }
+      tc_fence_before();
+      mbar_arrive(&m.tempty[acc]);
       if (a.cache && dst != NONE) atomicAdd(&a.codehash[dst], hs);
     }
   }
