@@ -70,6 +70,7 @@ __device__ __forceinline__ bool hkey_match(const Params &P, unsigned long long t
 
 // ---- (a2) probe -------------------------------------------------------------
 __global__ void k_qprobe(Params P, CallArgs A, uint32_t ntiles) {
+  pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < ntiles) P.tile_status[q] = 0ull;
   if (q == 0) *P.tile_ticket = 0u;
@@ -109,6 +110,7 @@ __global__ void k_qprobe(Params P, CallArgs A, uint32_t ntiles) {
 
 // ---- (a2) claim -------------------------------------------------------------
 __global__ void k_qclaim(Params P, CallArgs A) {
+  pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= A.n || P.st[q] != ST_QNEED || P.counts[2] == A.epoch) return;
   const uint32_t s = A.session[q];
@@ -133,6 +135,7 @@ __global__ void k_qclaim(Params P, CallArgs A) {
 
 // ---- (a3) probe ------------------------------------------------------------
 __global__ void k_hprobe(Params P, CallArgs A) {
+  pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= A.n || P.st[q] != ST_QNEED || P.counts[2] == A.epoch) return;
   const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
@@ -161,6 +164,7 @@ __global__ void k_hprobe(Params P, CallArgs A) {
 
 // ---- (a3) claim ------------------------------------------------------------
 __global__ void k_hclaim(Params P, CallArgs A) {
+  pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= A.n || P.st[q] != ST_HNEED || P.counts[2] == A.epoch) return;
   const uint32_t s = A.session[q], w = A.word[q];
@@ -201,6 +205,7 @@ __device__ __forceinline__ unsigned long long from_status(unsigned long long x) 
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
+  pdl_entry();
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_warp[SCAN_THREADS / 32];
   __shared__ unsigned long long s_prefix;
@@ -292,6 +297,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
 
 // ---- (a4) commit: handles, slots, records, cache values, work lists -------
 __global__ void k_commit(Params P, CallArgs A) {
+  pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= A.n) return;
   const uint32_t st = P.st[q];
@@ -352,6 +358,7 @@ __global__ void k_commit(Params P, CallArgs A) {
 
 // ---- (a7) final: QHIT results, outcomes, counters, cursors -----------------
 __global__ void k_final(Params P, CallArgs A) {
+  pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = q < A.n;
   uint32_t st = active ? P.st[q] : ST_INVALID;
@@ -431,6 +438,7 @@ __global__ void k_read_slots(Params P, uint32_t sess, uint32_t n, const uint32_t
 
 __global__ void k_resolve_parents(uint32_t n, const int64_t *__restrict__ ref,
                                   const uint32_t *__restrict__ log, uint32_t *__restrict__ out) {
+  pdl_entry();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t r = ref[i];
@@ -447,23 +455,23 @@ static inline uint32_t nblk(uint32_t n, uint32_t t) { return (n + t - 1) / t; }
 int launch_cache_front(const Params &P, const CallArgs &A, cudaStream_t s) {
   const uint32_t ntiles = nblk(A.n, SCAN_TILE);
   int k = 0;
-  k_qprobe<<<nblk(A.n, 256), 256, 0, s>>>(P, A, ntiles); ++k;
+  launch_pdl(k_qprobe, nblk(A.n, 256), 256, 0, s, P, A, ntiles); ++k;
   if (P.cache) {
-    k_qclaim<<<nblk(A.n, 256), 256, 0, s>>>(P, A); ++k;
-    k_hprobe<<<nblk(A.n, 256), 256, 0, s>>>(P, A); ++k;
-    k_hclaim<<<nblk(A.n, 256), 256, 0, s>>>(P, A); ++k;
+    launch_pdl(k_qclaim, nblk(A.n, 256), 256, 0, s, P, A); ++k;
+    launch_pdl(k_hprobe, nblk(A.n, 256), 256, 0, s, P, A); ++k;
+    launch_pdl(k_hclaim, nblk(A.n, 256), 256, 0, s, P, A); ++k;
   }
-  k_scan<<<ntiles, SCAN_THREADS, 0, s>>>(P, A); ++k;
+  launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, P, A); ++k;
   return k;
 }
 
 int launch_commit(const Params &P, const CallArgs &A, cudaStream_t s) {
-  k_commit<<<nblk(A.n, 256), 256, 0, s>>>(P, A);
+  launch_pdl(k_commit, nblk(A.n, 256), 256, 0, s, P, A);
   return 1;
 }
 
 int launch_final(const Params &P, const CallArgs &A, cudaStream_t s) {
-  k_final<<<nblk(A.n, 256), 256, 0, s>>>(P, A);
+  launch_pdl(k_final, nblk(A.n, 256), 256, 0, s, P, A);
   return 1;
 }
 
@@ -484,7 +492,7 @@ int launch_read_slots(const Params &P, uint32_t sess, uint32_t n, const uint32_t
 int launch_resolve_parents(uint32_t n, const int64_t *ref, const uint32_t *log, uint32_t *out,
                            cudaStream_t s) {
   if (!n) return 0;
-  k_resolve_parents<<<nblk(n, 256), 256, 0, s>>>(n, ref, log, out);
+  launch_pdl(k_resolve_parents, nblk(n, 256), 256, 0, s, n, ref, log, out);
   return 1;
 }
 }  // namespace rnnlm_host

@@ -78,6 +78,7 @@ __device__ unsigned long long encode_row_warp(const Params &P, const float *__re
 
 // New states of this call: rows r < counts[1] (GRU rows), code + hash per row.
 __global__ void k_encode_rows(Params P) {
+  pdl_entry();
   const uint32_t rows = P.counts[1];
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
@@ -160,7 +161,7 @@ int launch_encode_rows(const Params &P, uint32_t max_rows, int num_sms, cudaStre
   uint32_t blocks = (max_rows + 7) / 8;
   const uint32_t cap = (uint32_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
-  k_encode_rows<<<blocks, 256, 0, s>>>(P);
+  launch_pdl(k_encode_rows, blocks, 256, 0, s, P);
   return 1;
 }
 

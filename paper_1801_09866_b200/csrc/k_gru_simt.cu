@@ -26,6 +26,7 @@ constexpr int BM = 64, BU = 64, BK = 16, NT = 256, AST = BM + 4;
 __device__ __forceinline__ float sigmoidf_(float a) { return 1.0f / (1.0f + expf(-a)); }
 
 __global__ void __launch_bounds__(NT) k_gru1_f32(Params P) {
+  pdl_entry();
   __shared__ __align__(16) float As[BK][AST];
   __shared__ __align__(16) float Bs[BK][3 * BU];
   const uint32_t Q = P.counts[1];
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(NT) k_gru1_f32(Params P) {
 }
 
 __global__ void __launch_bounds__(NT) k_gru2_f32(Params P) {
+  pdl_entry();
   __shared__ __align__(16) float As[BK][AST];
   __shared__ __align__(16) float Bs[BK][BU];
   const uint32_t Q = P.counts[1];
@@ -207,8 +209,8 @@ int launch_gru_simt(const Params &P, uint32_t max_rows, int num_sms, cudaStream_
   uint32_t gy = ((uint32_t)num_sms * 2 + nub - 1) / nub;
   if (gy > tiles) gy = tiles;
   if (gy < 1) gy = 1;
-  k_gru1_f32<<<dim3(nub, gy), NT, 0, s>>>(P);
-  k_gru2_f32<<<dim3(nub, gy), NT, 0, s>>>(P);
+  launch_pdl(k_gru1_f32, dim3(nub, gy), NT, 0, s, P);
+  launch_pdl(k_gru2_f32, dim3(nub, gy), NT, 0, s, P);
   return 2;
 }
 }  // namespace rnnlm_host

@@ -185,6 +185,7 @@ struct TcArgs {
 // one warp per row, 16-byte loads/stores (the paper's per-frame (h || x)
 // block, built in HBM instead of host memory).
 __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
+  pdl_entry();
   const uint32_t Q = a.counts[1];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -279,11 +280,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Smem m = carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t Q = a.counts[1];
-  const uint32_t ntiles = ((Q + BM - 1) / BM) * a.nub;
   const uint32_t KC = (a.E + a.H) / BK;
   if (threadIdx.x == 0) { prefetch_map(&map_a1); prefetch_map(&map_w1); }
   setup(m, warp);
+  pdl_entry();
+  const uint32_t Q = a.counts[1];
+  const uint32_t ntiles = ((Q + BM - 1) / BM) * a.nub;
   const uint32_t tmem_base = *m.tmem_base;
 
   if (warp == 0) {
@@ -432,12 +434,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Smem m = carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t Q = a.counts[1];
   const uint32_t nt = a.H / BN;
-  const uint32_t ntiles = ((Q + BM - 1) / BM) * nt;
   const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
   if (threadIdx.x == 0) { prefetch_map(&map_a1); prefetch_map(&map_rh); prefetch_map(&map_w2); }
   setup(m, warp);
+  pdl_entry();
+  const uint32_t Q = a.counts[1];
+  const uint32_t ntiles = ((Q + BM - 1) / BM) * nt;
   const uint32_t tmem_base = *m.tmem_base;
 
   if (warp == 0) {
@@ -670,9 +673,9 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   if (g2 > (uint32_t)num_sms) g2 = num_sms;
   uint32_t gg = (max_rows + 7) / 8;
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
-  k_gather_a1<<<gg, 256, 0, s>>>(a);
-  k_gru1_tc<<<g1, THREADS, SMEM, s>>>(t->map_a1, t->map_w1, a);
-  k_gru2_tc<<<g2, THREADS, SMEM, s>>>(t->map_a1, t->map_rh, t->map_w2, a);
+  launch_pdl(k_gather_a1, gg, 256, 0, s, a);
+  launch_pdl(k_gru1_tc, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, a);
+  launch_pdl(k_gru2_tc, g2, THREADS, SMEM, s, t->map_a1, t->map_rh, t->map_w2, a);
   return 3;
 }
 }  // namespace rnnlm_host

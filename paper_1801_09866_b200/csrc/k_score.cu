@@ -38,6 +38,7 @@ __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v <
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 
 __global__ void __launch_bounds__(256) k_score(Params P, CallArgs A) {
+  pdl_entry();
   const uint32_t total = P.counts[0];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -108,7 +109,7 @@ int launch_score(const Params &P, const CallArgs &A, int num_sms, cudaStream_t s
   uint32_t blocks = (A.n + 7) / 8;                    // <= one warp per query
   const uint32_t cap = (uint32_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
-  k_score<<<blocks, 256, 0, s>>>(P, A);
+  launch_pdl(k_score, blocks, 256, 0, s, P, A);
   return 1;
 }
 

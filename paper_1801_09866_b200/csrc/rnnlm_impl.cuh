@@ -122,10 +122,34 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 
 __device__ __forceinline__ void latch(int *sticky, int err) { atomicCAS(sticky, 0, err); }
 
+// Programmatic dependent launch (PDL): every kernel of the step is launched
+// with programmatic stream serialisation, so its launch and CTA rasterisation
+// overlap the tail of the previous kernel; griddepcontrol.wait then blocks
+// until the previous grid has completed and its memory is visible.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace rnnlm_dev
 
 // ---- host launchers (one per kernel family) --------------------------------
 namespace rnnlm_host {
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 using rnnlm_dev::CallArgs;
 using rnnlm_dev::Params;
 constexpr int SCAN_TILE = 1024;   // queries per look-back tile
