@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--prefill", type=int, default=40,
                     help="untimed frames run before warm-up so timed frames are mid-utterance")
     ap.add_argument("--uniform-words", action="store_true", help="(ncu evidence) no Zipf reuse")
+    ap.add_argument("--timing-level", type=int, default=1, help="1: kernel groups, 2: + GRU kernels")
     return ap.parse_args()
 
 
@@ -261,7 +262,7 @@ def run_ours(args):
         step(t)
     torch.cuda.synchronize()
     st0 = eng.cache_stats()
-    eng.set_timing(True)
+    eng.set_timing(args.timing_level)
     eng.get_timing(reset=True)
     l0 = eng.launch_count()
     clocks = ClockSampler(local)
@@ -348,7 +349,8 @@ def run_ours(args):
                      "gru_ms_per_step": timing["ms_gru"] / args.steps,
                      "share_of_step": (timing["ms_gru"] / total_ms) if total_ms else None},
         "kernel_ms_per_step": {kk: timing[kk] / args.steps for kk in
-                               ("ms_cache", "ms_score", "ms_gru", "ms_encode", "ms_final")},
+                               ("ms_cache", "ms_score", "ms_gru", "ms_encode", "ms_final",
+                                "ms_gru_gather", "ms_gru_phase1", "ms_gru_phase2")},
         "hit_rates": {"query_cache": d_stats["query_hits"] / max(1, d_stats["total_queries"]),
                       "hidden_cache": d_stats["hidden_hits"] / max(1, d_stats["hidden_lookups"]),
                       "gru_rows_per_step": rows / args.steps},

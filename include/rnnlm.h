@@ -124,6 +124,8 @@ typedef struct {
   double ms_final;      /* result write + counters (a7) */
   uint64_t calls;       /* timed query_batch calls */
   uint64_t launches;    /* kernels launched by those calls */
+  /* timing level 2, BF16 path only: split of ms_gru */
+  double ms_gru_gather, ms_gru_phase1, ms_gru_phase2;
 } rnnlm_timing;
 
 /* Create an engine on cfg->device: validates dims and weights, copies the
@@ -180,7 +182,9 @@ uint32_t rnnlm_code_bytes(const rnnlm_t *h);
 rnnlm_status rnnlm_resolve_parents(uint32_t n, const int64_t *d_ref, const uint32_t *d_log,
                                    uint32_t *d_parent, rnnlm_stream_t stream);
 
-rnnlm_status rnnlm_set_timing(rnnlm_t *h, int enable);
+/* level 0: off; 1: per kernel group; 2: also per GRU kernel (adds events inside
+ * the GRU group, which serialise those launches). */
+rnnlm_status rnnlm_set_timing(rnnlm_t *h, int level);
 rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset);
 /* Kernels launched by this handle since create (host-side count). */
 uint64_t rnnlm_launch_count(const rnnlm_t *h);

@@ -42,7 +42,8 @@ class Timing(ctypes.Structure):
     _fields_ = [("ms_cache", ctypes.c_double), ("ms_score", ctypes.c_double),
                 ("ms_gru", ctypes.c_double), ("ms_encode", ctypes.c_double),
                 ("ms_final", ctypes.c_double), ("calls", ctypes.c_uint64),
-                ("launches", ctypes.c_uint64)]
+                ("launches", ctypes.c_uint64), ("ms_gru_gather", ctypes.c_double),
+                ("ms_gru_phase1", ctypes.c_double), ("ms_gru_phase2", ctypes.c_double)]
 
 
 # name -> (restype, argtypes); every symbol include/rnnlm.h declares

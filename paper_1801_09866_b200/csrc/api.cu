@@ -18,7 +18,8 @@ int gru_tc_supported(uint32_t E, uint32_t H);
 int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_out);
 void gru_tc_release(void *state);
 int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax);
-int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s);
+int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s,
+                  cudaEvent_t ev_gathered, cudaEvent_t ev_phase1);
 }  // namespace rnnlm_host
 
 struct rnnlm {
@@ -30,9 +31,9 @@ struct rnnlm {
   uint32_t epoch = 0;
   uint64_t launches = 0;
   // timing
-  bool timing = false;
+  int timing = 0;
   std::vector<cudaEvent_t> ev_pool;
-  std::vector<std::vector<cudaEvent_t>> ev_pending;   // 6 events per timed call
+  std::vector<std::vector<cudaEvent_t>> ev_pending;   // NEV (+2 at level 2) events per timed call
   rnnlm_timing acc{};
 };
 
@@ -345,7 +346,16 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
   if (h->timing) cudaEventRecord(ev[1], s);
   k += rnnlm_host::launch_score(P, A, h->num_sms, s);
   if (h->timing) cudaEventRecord(ev[2], s);
-  if (P.math == RNNLM_MATH_BF16) k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s);
+  if (P.math == RNNLM_MATH_BF16) {
+    cudaEvent_t e1 = nullptr, e2 = nullptr;
+    if (h->timing >= 2) {
+      e1 = take_event(h);
+      e2 = take_event(h);
+      ev.push_back(e1);
+      ev.push_back(e2);
+    }
+    k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s, e1, e2);
+  }
   else k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
   if (h->timing) cudaEventRecord(ev[3], s);
   if (P.math != RNNLM_MATH_BF16)                      // the tcgen05 epilogue encodes in place
@@ -439,9 +449,9 @@ rnnlm_status rnnlm_resolve_parents(uint32_t n, const int64_t *d_ref, const uint3
   return cuda_status(cudaGetLastError());
 }
 
-rnnlm_status rnnlm_set_timing(rnnlm_t *h, int enable) {
+rnnlm_status rnnlm_set_timing(rnnlm_t *h, int level) {
   if (!h) return RNNLM_E_INVALID_ARG;
-  h->timing = enable != 0;
+  h->timing = level < 0 ? 0 : level;
   return RNNLM_OK;
 }
 
@@ -457,6 +467,15 @@ rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset) {
     h->acc.ms_gru += ms[2];
     h->acc.ms_encode += ms[3];
     h->acc.ms_final += ms[4];
+    if (ev.size() >= NEV + 2) {          // level 2: [2]=before GRU, [6]=gathered, [7]=phase 1, [3]=after GRU
+      float a, b, c;
+      cudaEventElapsedTime(&a, ev[2], ev[NEV]);
+      cudaEventElapsedTime(&b, ev[NEV], ev[NEV + 1]);
+      cudaEventElapsedTime(&c, ev[NEV + 1], ev[3]);
+      h->acc.ms_gru_gather += a;
+      h->acc.ms_gru_phase1 += b;
+      h->acc.ms_gru_phase2 += c;
+    }
     for (cudaEvent_t e2 : ev) h->ev_pool.push_back(e2);
   }
   h->ev_pending.clear();

@@ -482,16 +482,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                           ? a.codes + (size_t)dst * a.cstride : nullptr;
       unsigned long long hs = 0;
       uint32_t signacc = 0;
-      auto process = [&](int g, const float *vu) {
+      // global operands of group g+1 (z, h, bias) are loaded while group g is
+      // processed; TMEM loads are double-buffered the same way
+      auto fetch = [&](int g, float4 *z4, float4 *h4, float *bias16) {
         if (dst == NONE) return;
-        float bias16[16];
         ld_bias16(a.bh + n0 + g * 16, bias16);
-        float4 z4[4], h4[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           z4[j] = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + 4 * j);
           h4[j] = *reinterpret_cast<const float4 *>(hp + g * 16 + 4 * j);
         }
+      };
+      auto process = [&](int g, const float *vu, const float4 *z4, const float4 *h4,
+                         const float *bias16) {
+        if (dst == NONE) return;
         float hn[16];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -518,16 +522,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         s16[1] = pk[1];
         if (a.cache) hs += encode16(a, hn, n0 + g * 16, code, signacc);
       };
-      float va[16], vb[16];
+      float va[16], vb[16], ba[16], bb2[16];
+      float4 za[4], ha[4], zb[4], hb[4];
+      fetch(0, za, ha, ba);
       tmem_ld16(tbase, va);
       tmem_ld_wait();
 #pragma unroll 1
       for (int g = 0; g < BN / 32; g += 2) {
         tmem_ld16(tbase + (g + 1) * 16, vb);
-        process(g, va);
+        fetch(g + 1, zb, hb, bb2);
+        process(g, va, za, ha, ba);
         tmem_ld_wait();
-        if (g + 2 < BN / 32) tmem_ld16(tbase + (g + 2) * 16, va);
-        process(g + 1, vb);
+        if (g + 2 < BN / 32) {
+          tmem_ld16(tbase + (g + 2) * 16, va);
+          fetch(g + 2, za, ha, ba);
+        }
+        process(g + 1, vb, zb, hb, bb2);
         tmem_ld_wait();
       }
       tc_fence_before();
@@ -656,7 +666,8 @@ void gru_tc_release(void *state) {
   delete t;
 }
 
-int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, cudaStream_t s) {
+int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, cudaStream_t s,
+                  cudaEvent_t ev_gathered, cudaEvent_t ev_phase1) {
   TcState *t = static_cast<TcState *>(state);
   if (!max_rows || !t || !t->bound) return 0;
   TcArgs a;
@@ -674,7 +685,9 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   uint32_t gg = (max_rows + 7) / 8;
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
   launch_pdl(k_gather_a1, gg, 256, 0, s, a);
+  if (ev_gathered) cudaEventRecord(ev_gathered, s);
   launch_pdl(k_gru1_tc, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, a);
+  if (ev_phase1) cudaEventRecord(ev_phase1, s);
   launch_pdl(k_gru2_tc, g2, THREADS, SMEM, s, t->map_a1, t->map_rh, t->map_w2, a);
   return 3;
 }

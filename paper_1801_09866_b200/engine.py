@@ -137,8 +137,8 @@ class RNNLM:
         return out
 
     # ---- timing ----------------------------------------------------------------
-    def set_timing(self, enable: bool):
-        check(_lib.load().rnnlm_set_timing(self._h, 1 if enable else 0))
+    def set_timing(self, level):
+        check(_lib.load().rnnlm_set_timing(self._h, int(level)))
 
     def get_timing(self, reset: bool = True) -> dict:
         t = Timing()
