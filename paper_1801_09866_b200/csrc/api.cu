@@ -240,7 +240,6 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   // ---- pools
   chk(dalloc(h, &P.rec, S * cap));
   chk(dalloc(h, &P.state, S * cap * H));
-  if (c.math == RNNLM_MATH_BF16) chk(dalloc(h, &P.state16, S * cap * H));
   if (P.cache) {
     if (c.key_mode != RNNLM_KEY_OFF) chk(dalloc(h, &P.codes, S * cap * P.cstride));
     chk(dalloc(h, &P.codehash, S * cap));

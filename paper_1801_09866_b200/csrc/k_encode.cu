@@ -96,7 +96,6 @@ __global__ void k_reset_root(Params P, uint32_t lo) {
   const size_t row = (size_t)s * P.cap;
   for (uint32_t i = threadIdx.x; i < P.H; i += blockDim.x) {
     P.state[row * P.H + i] = 0.0f;
-    if (P.state16) P.state16[row * P.H + i] = __float2bfloat16_rn(0.0f);
   }
   if (threadIdx.x == 0) {
     Rec r;

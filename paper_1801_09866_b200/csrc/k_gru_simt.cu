@@ -191,7 +191,6 @@ __global__ void __launch_bounds__(NT) k_gru2_f32(Params P) {
         const float c = tanhf(P.g_wxb[o] + acc[i][j]);
         const float hn = (1.0f - z) * hp[u] + z * c;
         P.state[(size_t)dst * H + u] = hn;
-        if (P.state16) P.state16[(size_t)dst * H + u] = __float2bfloat16_rn(hn);
       }
     }
   }

@@ -4,7 +4,7 @@
 // frame's (h || x) rows form one block) is a real dense contraction:
 // [Q, E+H] x [E+H, 3H] for Q misses (Chung form, reading 1), executed as
 //
-//   gather   A1[r] = [x | h] (x = E[word] bf16, h = bf16 shadow of the parent
+//   gather   A1[r] = [x | bf16(h)] (x = E[word] bf16, h = the fp32 parent
 //            state), one warp per row, 16-byte vector copies (k_gather_a1).
 //   phase 1  z, r: A = A1 (TMA), B = W1 [(H/128) x 256 rows][E+H] bf16 (TMA;
 //            per 128-unit block 128 rows [Wz|Uz] then 128 rows [Wr|Ur]),
@@ -14,8 +14,8 @@
 //            the r.h rows, both TMA), B = W2 [H rows][E+H] = [Wh | Uh] (TMA),
 //            tile 128 x 256, K = E+H: the accumulator is Wh x + Uh (r.h)
 //            directly (no fp32 round trip of Wh x).  Epilogue:
-//            c = tanh(. + bh), h' = (1-z) h + z c, the new fp32 state, its bf16
-//            shadow, and (a1) its compression code + code-hash contribution
+//            c = tanh(. + bh), h' = (1-z) h + z c, the new fp32 state and
+//            (a1) its compression code + code-hash contribution
 //            (hash terms add, so the N-tiles of a row combine with one 64-bit
 //            atomicAdd each, order-independent).
 //
@@ -163,11 +163,9 @@ __device__ __forceinline__ void ld_bias16(const float *p, float *b) {
 struct TcArgs {
   uint32_t E, H, nub;              // nub = H / 128 phase-1 unit blocks
   const __nv_bfloat16 *emb16;
-  const __nv_bfloat16 *state16;
   const float *state;
   const float *bzr;                // [nub][2][128] (bz, br)
   const float *bh;                 // [H]
-  __nv_bfloat16 *state16_out;
   float *state_out;
   const uint32_t *row_src, *row_dst, *row_word, *counts;
   float *g_z;                      // [B_max][H]
@@ -181,9 +179,10 @@ struct TcArgs {
 };
 
 // ---------------------------------------------------------------- A gather
-// Phase-1 A operand: row r = [E[word_r] | h16[src_r]] (bf16, K-major, dense),
-// one warp per row, 16-byte loads/stores (the paper's per-frame (h || x)
-// block, built in HBM instead of host memory).
+// Phase-1 A operand: row r = [E[word_r] | bf16(state[src_r])] (bf16, K-major,
+// dense), one warp per row, 16-byte loads/stores (the paper's per-frame
+// (h || x) block, built in HBM instead of host memory).  States are
+// stored only in fp32; the bf16 operand copy is made here.
 __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
   pdl_entry();
   const uint32_t Q = a.counts[1];
@@ -192,11 +191,17 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
   const uint32_t K1 = a.E + a.H;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Q; r += nw) {
     const uint4 *x = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)a.row_word[r] * a.E);
-    const uint4 *h = reinterpret_cast<const uint4 *>(a.state16 + (size_t)a.row_src[r] * a.H);
+    const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
     uint4 *dst = reinterpret_cast<uint4 *>(a.a1 + (size_t)r * K1);
     const uint32_t nx = a.E / 8, nh = a.H / 8;
     for (uint32_t i = lane; i < nx; i += 32) dst[i] = __ldg(x + i);
-    for (uint32_t i = lane; i < nh; i += 32) dst[nx + i] = h[i];
+    for (uint32_t i = lane; i < nh; i += 32) {
+      const float4 u = h[2 * i], v = h[2 * i + 1];
+      __nv_bfloat162 b0 = __floats2bfloat162_rn(u.x, u.y), b1 = __floats2bfloat162_rn(u.z, u.w);
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(v.x, v.y), b3 = __floats2bfloat162_rn(v.z, v.w);
+      dst[nx + i] = make_uint4(*reinterpret_cast<uint32_t *>(&b0), *reinterpret_cast<uint32_t *>(&b1),
+                               *reinterpret_cast<uint32_t *>(&b2), *reinterpret_cast<uint32_t *>(&b3));
+    }
   }
 }
 
@@ -319,7 +324,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + gate * UB;
       const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB;
       const size_t o = (size_t)(valid ? row : 0) * a.H + ub * UB;
-      const __nv_bfloat16 *h16 = a.state16 + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * UB;
+      // bf16 parent state = the recurrent half of the row's gathered A1 row
+      const __nv_bfloat16 *h16 = a.a1 + (size_t)(valid ? row : 0) * (a.E + a.H) + a.E + ub * UB;
       // TMEM loads are double-buffered: group g+1 is in flight while g is processed
       auto process = [&](int g, const float *v) {
         float bias16[16];
@@ -478,6 +484,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
       const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + n0;
       const size_t o = (size_t)(valid ? row : 0) * a.H + n0;
+      {  // warm L2 with the next tile's z and parent-state rows of this thread
+        const uint32_t nxt = tile + gridDim.x;
+        if (nxt < ntiles) {
+          const uint32_t nrow = (nxt / nt) * BM + r_in;
+          const uint32_t nn0 = (nxt % nt) * BN + half * (BN / 2);
+          if (nrow < Q) {
+            const float *zp = a.g_z + (size_t)nrow * a.H + nn0;
+            const float *sp = a.state + (size_t)a.row_src[nrow] * a.H + nn0;
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(zp + 32 * l));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(sp + 32 * l));
+            }
+          }
+        }
+      }
       uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && dst != NONE)
                           ? a.codes + (size_t)dst * a.cstride : nullptr;
       unsigned long long hs = 0;
@@ -510,16 +532,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         float4 *so = reinterpret_cast<float4 *>(a.state_out + (size_t)dst * a.H + n0 + g * 16);
 #pragma unroll
         for (int j = 0; j < 4; ++j) so[j] = make_float4(hn[4 * j], hn[4 * j + 1], hn[4 * j + 2], hn[4 * j + 3]);
-        uint4 pk[2];
-        uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          __nv_bfloat162 t2 = __floats2bfloat162_rn(hn[2 * j], hn[2 * j + 1]);
-          pw[j] = *reinterpret_cast<uint32_t *>(&t2);
-        }
-        uint4 *s16 = reinterpret_cast<uint4 *>(a.state16_out + (size_t)dst * a.H + n0 + g * 16);
-        s16[0] = pk[0];
-        s16[1] = pk[1];
         if (a.cache) hs += encode16(a, hn, n0 + g * 16, code, signacc);
       };
       float va[16], vb[16], ba[16], bb2[16];
@@ -672,8 +684,8 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   if (!max_rows || !t || !t->bound) return 0;
   TcArgs a;
   a.E = P.E; a.H = P.H; a.nub = t->nub;
-  a.emb16 = P.emb16; a.state16 = P.state16; a.state = P.state; a.bzr = t->bzr; a.bh = t->bh;
-  a.state16_out = P.state16; a.state_out = P.state;
+  a.emb16 = P.emb16; a.state = P.state; a.bzr = t->bzr; a.bh = t->bh;
+  a.state_out = P.state;
   a.row_src = P.row_src; a.row_dst = P.row_dst; a.row_word = P.row_word; a.counts = P.counts;
   a.g_z = P.g_z; a.g_rh16 = P.g_rh16; a.a1 = t->a1;
   a.cache = P.cache; a.key_mode = P.key_mode; a.round_digits = P.round_digits;

@@ -80,7 +80,6 @@ struct Params {
   // pools
   Rec *rec;                       // S*cap
   float *state;                   // S*cap x H fp32
-  __nv_bfloat16 *state16;         // S*cap x H bf16 shadow (MATH_BF16)
   uint8_t *codes;                 // S*cap x cstride (key modes sign/round)
   unsigned long long *codehash;   // S*cap
   QEntry *qtab;                   // S*(qmask+1)
