@@ -19,10 +19,15 @@
 //            (hash terms add, so the N-tiles of a row combine with one 64-bit
 //            atomicAdd each, order-independent).
 //
-// Both GEMM kernels are persistent (grid <= #SMs), warp-specialised: one TMA
-// producer thread, one MMA-issuing thread (tcgen05.mma.cta_group::1.kind::f16,
-// M = 128, N = 256), eight epilogue warps (tcgen05.ld.32x32b: TMEM lane
-// quarter = warp % 4, two warps per quarter split the columns).  Pipelines
+// Both phases run in ONE persistent kernel (grid <= #SMs) over a merged tile
+// list in which the phase-2 tiles of an M-tile trail its phase-1 tiles; a
+// per-M-tile counter (release by the phase-1 epilogues, acquire by the TMA
+// producer of the phase-2 tile) carries the r.h / z dependency, so phase 2 of
+// early rows overlaps phase 1 of later rows and neither phase has a wave
+// tail.  Warp-specialised: one TMA producer thread, one MMA-issuing thread
+// (tcgen05.mma.cta_group::1.kind::f16, M = 128, N = 256), eight epilogue
+// warps (tcgen05.ld.32x32b: TMEM lane quarter = warp % 4, two warps per
+// quarter split the columns).  Pipelines
 // are mbarrier rings (full / empty per smem stage, full / empty per TMEM
 // accumulator; two 256-column accumulators, so the epilogue of tile i
 // overlaps the MMAs of tile i+1).  Rows >= Q read stale A rows and are
@@ -171,6 +176,8 @@ struct TcArgs {
   float *g_z;                      // [B_max][H]
   __nv_bfloat16 *g_rh16;           // [B_max][H]
   __nv_bfloat16 *a1;               // [B_max][E+H] gathered phase-1 A operand
+  uint32_t *done1;                 // per M-tile phase-1 epilogue arrivals (zeroed by the gather)
+  uint32_t lag;                    // phase-2 tiles trail phase-1 tiles by this many M-tiles
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
   float round_scale;
@@ -189,6 +196,8 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t K1 = a.E + a.H;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (Q + BM - 1) / BM; i += gridDim.x * blockDim.x)
+    a.done1[i] = 0u;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Q; r += nw) {
     const uint4 *x = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)a.row_word[r] * a.E);
     const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
@@ -248,7 +257,45 @@ __device__ __forceinline__ void teardown(const Smem &m, int warp, uint32_t tmem_
   }
 }
 
-// MMA issuer shared by both phases: KC chunks of 4 x (M=128, N=256, K=16).
+// ---------------------------------------------------------------- tile schedule
+// One persistent kernel runs both phases.  Per M-tile m (128 rows) there are
+// nub phase-1 tiles P1(m, j) (z|r of units [128j, 128j+128)) and nt phase-2
+// tiles P2(m, j) (candidate of units [256j, 256j+256)).  Global order: step s
+// holds P1(s, *) then P2(s - L, *), so a phase-2 tile comes ~L M-tiles after
+// the phase-1 tiles it depends on (r.h of ALL units of its rows).  Every CTA
+// walks its tiles in increasing global index and a tile only waits on tiles
+// with smaller indices, so the persistent grid (all CTAs resident) cannot
+// deadlock.
+struct Tile {
+  uint32_t kind, m, j;             // kind 0: phase 1, 1: phase 2
+};
+
+__device__ __forceinline__ Tile tile_of(uint32_t t, uint32_t mt, uint32_t n1, uint32_t n2, uint32_t L) {
+  Tile x;
+  const uint32_t a = L * n1, b = (mt - L) * (n1 + n2);
+  if (t < a) {
+    x.kind = 0; x.m = t / n1; x.j = t % n1;
+  } else if (t < a + b) {
+    const uint32_t u = t - a, s = L + u / (n1 + n2), j = u % (n1 + n2);
+    if (j < n1) { x.kind = 0; x.m = s; x.j = j; }
+    else { x.kind = 1; x.m = s - L; x.j = j - n1; }
+  } else {
+    const uint32_t u = t - a - b;
+    x.kind = 1; x.m = mt - L + u / n2; x.j = u % n2;
+  }
+  return x;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_phase1(const uint32_t *cnt, uint32_t target) {
+  while (ld_acquire(cnt) < target) __nanosleep(128);
+}
+
+// MMA issuer: KC chunks of 4 x (M=128, N=256, K=16) per tile, both phases.
 __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t ntiles,
                                          uint32_t KC, int lane) {
   uint32_t stage = 0, phase = 0, it = 0;
@@ -273,108 +320,6 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
       if (++stage == ST) { stage = 0; phase ^= 1; }
     }
   }
-}
-
-// =============================================================== phase 1
-// warp 0: TMA producer; warp 1: TMEM allocation + MMA issue;
-// warps 2-9: epilogue, TMEM lane quarter = warp % 4; warps 2-5 own the z
-// columns, warps 6-9 the r columns of the 128-unit block.
-__global__ void __launch_bounds__(THREADS, 1)
-    k_gru1_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1,
-              TcArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const Smem m = carve(smem_raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t KC = (a.E + a.H) / BK;
-  if (threadIdx.x == 0) { prefetch_map(&map_a1); prefetch_map(&map_w1); }
-  setup(m, warp);
-  pdl_entry();
-  const uint32_t Q = a.counts[1];
-  const uint32_t ntiles = ((Q + BM - 1) / BM) * a.nub;
-  const uint32_t tmem_base = *m.tmem_base;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t m0 = (tile / a.nub) * BM, ub = tile % a.nub;
-        for (uint32_t kc = 0; kc < KC; ++kc) {
-          mbar_wait(&m.empty[stage], phase ^ 1);
-          mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
-          tma_load_2d(smem_u32(m.sA + stage * A_BYTES), &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
-          tma_load_2d(smem_u32(m.sB + stage * B_BYTES), &map_w1, &m.full[stage], (int)(kc * BK), (int)(ub * BN));
-          if (++stage == ST) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    mma_loop(m, tmem_base, ntiles, KC, lane);
-  } else {
-    const int q = warp & 3;
-    const int gate = (warp - 2) >> 2;                   // 0: z columns, 1: r columns
-    const int r_in = q * 32 + lane;
-    uint32_t it = 0;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t acc = it & 1;
-      const uint32_t m0 = (tile / a.nub) * BM, ub = tile % a.nub;
-      mbar_wait(&m.tfull[acc], (it >> 1) & 1);
-      tc_fence_after();
-      const uint32_t row = m0 + r_in;
-      const bool valid = row < Q;
-      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + gate * UB;
-      const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB;
-      const size_t o = (size_t)(valid ? row : 0) * a.H + ub * UB;
-      // bf16 parent state = the recurrent half of the row's gathered A1 row
-      const __nv_bfloat16 *h16 = a.a1 + (size_t)(valid ? row : 0) * (a.E + a.H) + a.E + ub * UB;
-      // TMEM loads are double-buffered: group g+1 is in flight while g is processed
-      auto process = [&](int g, const float *v) {
-        float bias16[16];
-        ld_bias16(bias + g * 16, bias16);
-        uint4 hb[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-        if (gate == 1 && valid) {
-          hb[0] = *reinterpret_cast<const uint4 *>(h16 + g * 16);
-          hb[1] = *reinterpret_cast<const uint4 *>(h16 + g * 16 + 8);
-        }
-        float sg[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) sg[j] = sigm(v[j] + bias16[j]);
-        if (!valid) return;
-        if (gate == 0) {
-          float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) gz[j] = make_float4(sg[4 * j], sg[4 * j + 1], sg[4 * j + 2], sg[4 * j + 3]);
-        } else {
-          const uint32_t *hw = reinterpret_cast<const uint32_t *>(hb);
-          uint4 pk[2];
-          uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float h0 = __uint_as_float(hw[j] << 16), h1 = __uint_as_float(hw[j] & 0xFFFF0000u);
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(sg[2 * j] * h0, sg[2 * j + 1] * h1);
-            pw[j] = *reinterpret_cast<uint32_t *>(&t2);
-          }
-          uint4 *gr = reinterpret_cast<uint4 *>(a.g_rh16 + o + g * 16);
-          gr[0] = pk[0];
-          gr[1] = pk[1];
-        }
-      };
-      float va[16], vb[16];
-      tmem_ld16(tbase, va);
-      tmem_ld_wait();
-#pragma unroll 1
-      for (int g = 0; g < UB / 16; g += 2) {
-        tmem_ld16(tbase + (g + 1) * 16, vb);
-        process(g, va);
-        tmem_ld_wait();
-        if (g + 2 < UB / 16) tmem_ld16(tbase + (g + 2) * 16, va);
-        process(g + 1, vb);
-        tmem_ld_wait();
-      }
-      tc_fence_before();
-      mbar_arrive(&m.tempty[acc]);                      // accumulator drained
-    }
-  }
-  teardown(m, warp, tmem_base);
 }
 
 // Compression code words of 16 consecutive new-state elements starting at
@@ -431,36 +376,167 @@ __device__ __forceinline__ unsigned long long encode16(const TcArgs &a, const fl
   return hs;
 }
 
-// =============================================================== phase 2
-// warp 0: TMA producer; warp 1: TMEM alloc + MMA; warps 2-9: epilogue
-// (two warps per TMEM lane quarter, 128 units each).
+
+// Phase-1 epilogue of one thread: row r_in of the tile, the 128 z columns
+// (gate 0) or r columns (gate 1) of unit block ub.
+__device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid,
+                                           int gate, uint32_t ub) {
+  const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB;
+  const size_t o = (size_t)(valid ? row : 0) * a.H + ub * UB;
+  // bf16 parent state = the recurrent half of the row's gathered A1 row
+  const __nv_bfloat16 *h16 = a.a1 + (size_t)(valid ? row : 0) * (a.E + a.H) + a.E + ub * UB;
+  auto process = [&](int g, const float *v) {
+    float bias16[16];
+    ld_bias16(bias + g * 16, bias16);
+    uint4 hb[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    if (gate == 1 && valid) {
+      hb[0] = *reinterpret_cast<const uint4 *>(h16 + g * 16);
+      hb[1] = *reinterpret_cast<const uint4 *>(h16 + g * 16 + 8);
+    }
+    float sg[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sg[j] = sigm(v[j] + bias16[j]);
+    if (!valid) return;
+    if (gate == 0) {
+      float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) gz[j] = make_float4(sg[4 * j], sg[4 * j + 1], sg[4 * j + 2], sg[4 * j + 3]);
+    } else {
+      const uint32_t *hw = reinterpret_cast<const uint32_t *>(hb);
+      uint4 pk[2];
+      uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float h0 = __uint_as_float(hw[j] << 16), h1 = __uint_as_float(hw[j] & 0xFFFF0000u);
+        __nv_bfloat162 t2 = __floats2bfloat162_rn(sg[2 * j] * h0, sg[2 * j + 1] * h1);
+        pw[j] = *reinterpret_cast<uint32_t *>(&t2);
+      }
+      uint4 *gr = reinterpret_cast<uint4 *>(a.g_rh16 + o + g * 16);
+      gr[0] = pk[0];
+      gr[1] = pk[1];
+    }
+  };
+  float va[16], vb[16];
+  tmem_ld16(tbase, va);
+  tmem_ld_wait();
+#pragma unroll 1
+  for (int g = 0; g < UB / 16; g += 2) {
+    tmem_ld16(tbase + (g + 1) * 16, vb);
+    process(g, va);
+    tmem_ld_wait();
+    if (g + 2 < UB / 16) tmem_ld16(tbase + (g + 2) * 16, va);
+    process(g + 1, vb);
+    tmem_ld_wait();
+  }
+}
+
+// Phase-2 epilogue of one thread: row r_in, 128 units starting at n0.
+__device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid,
+                                           uint32_t n0) {
+  const uint32_t dst = valid ? a.row_dst[row] : NONE;
+  const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + n0;
+  const size_t o = (size_t)(valid ? row : 0) * a.H + n0;
+  uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && dst != NONE)
+                      ? a.codes + (size_t)dst * a.cstride : nullptr;
+  unsigned long long hs = 0;
+  uint32_t signacc = 0;
+  // global operands of group g+1 (z, h, bias) are loaded while group g is
+  // processed; TMEM loads are double-buffered the same way
+  auto fetch = [&](int g, float4 *z4, float4 *h4, float *bias16) {
+    if (dst == NONE) return;
+    ld_bias16(a.bh + n0 + g * 16, bias16);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      z4[j] = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + 4 * j);
+      h4[j] = *reinterpret_cast<const float4 *>(hp + g * 16 + 4 * j);
+    }
+  };
+  auto process = [&](int g, const float *vu, const float4 *z4, const float4 *h4, const float *bias16) {
+    if (dst == NONE) return;
+    float hn[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float zz[4] = {z4[j].x, z4[j].y, z4[j].z, z4[j].w};
+      const float hh[4] = {h4[j].x, h4[j].y, h4[j].z, h4[j].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float c = tanh_fast(vu[4 * j + t] + bias16[4 * j + t]);
+        hn[4 * j + t] = (1.0f - zz[t]) * hh[t] + zz[t] * c;
+      }
+    }
+    float4 *so = reinterpret_cast<float4 *>(a.state_out + (size_t)dst * a.H + n0 + g * 16);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) so[j] = make_float4(hn[4 * j], hn[4 * j + 1], hn[4 * j + 2], hn[4 * j + 3]);
+    if (a.cache) hs += encode16(a, hn, n0 + g * 16, code, signacc);
+  };
+  float va[16], vb[16], ba[16], bb2[16];
+  float4 za[4], ha[4], zb[4], hb[4];
+  fetch(0, za, ha, ba);
+  tmem_ld16(tbase, va);
+  tmem_ld_wait();
+#pragma unroll 1
+  for (int g = 0; g < BN / 32; g += 2) {
+    tmem_ld16(tbase + (g + 1) * 16, vb);
+    fetch(g + 1, zb, hb, bb2);
+    process(g, va, za, ha, ba);
+    tmem_ld_wait();
+    if (g + 2 < BN / 32) {
+      tmem_ld16(tbase + (g + 2) * 16, va);
+      fetch(g + 2, za, ha, ba);
+    }
+    process(g + 1, vb, zb, hb, bb2);
+    tmem_ld_wait();
+  }
+  if (a.cache && dst != NONE) atomicAdd(&a.codehash[dst], hs);
+}
+
+// =============================================================== fused GRU kernel
+// warp 0: TMA producer (waits on the phase-1 counter before a phase-2 tile);
+// warp 1: TMEM allocation + MMA issue; warps 2-9: epilogue, TMEM lane quarter
+// = warp % 4, column half = (warp - 2) / 4.
 __global__ void __launch_bounds__(THREADS, 1)
-    k_gru2_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_rh,
-              const __grid_constant__ CUtensorMap map_w2, TcArgs a) {
+    k_gru_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1,
+             const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2,
+             TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Smem m = carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t nt = a.H / BN;
+  const uint32_t n1 = a.nub, n2 = a.H / BN;
   const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
-  if (threadIdx.x == 0) { prefetch_map(&map_a1); prefetch_map(&map_rh); prefetch_map(&map_w2); }
+  const uint32_t target = n1 * EPI_WARPS;               // phase-1 arrivals per M-tile
+  if (threadIdx.x == 0) {
+    prefetch_map(&map_a1); prefetch_map(&map_w1); prefetch_map(&map_rh); prefetch_map(&map_w2);
+  }
   setup(m, warp);
   pdl_entry();
   const uint32_t Q = a.counts[1];
-  const uint32_t ntiles = ((Q + BM - 1) / BM) * nt;
+  const uint32_t mt = (Q + BM - 1) / BM;
+  const uint32_t L = mt < a.lag ? mt : a.lag;
+  const uint32_t ntiles = mt * (n1 + n2);
   const uint32_t tmem_base = *m.tmem_base;
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t m0 = (tile / nt) * BM, n0 = (tile % nt) * BN;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile x = tile_of(t, mt, n1, n2, L);
+        const uint32_t m0 = x.m * BM;
+        if (x.kind == 1) {
+          wait_phase1(a.done1 + x.m, target);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (uint32_t kc = 0; kc < KC; ++kc) {
           mbar_wait(&m.empty[stage], phase ^ 1);
           mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
-          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES);
-          if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
-          else tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BK), (int)m0);
-          tma_load_2d(smem_u32(m.sB + stage * B_BYTES), &map_w2, &m.full[stage], (int)(kc * BK), (int)n0);
+          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * B_BYTES);
+          if (x.kind == 0) {
+            tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
+            tma_load_2d(dB, &map_w1, &m.full[stage], (int)(kc * BK), (int)(x.j * BN));
+          } else {
+            if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
+            else tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BK), (int)m0);
+            tma_load_2d(dB, &map_w2, &m.full[stage], (int)(kc * BK), (int)(x.j * BN));
+          }
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
       }
@@ -469,92 +545,34 @@ __global__ void __launch_bounds__(THREADS, 1)
     mma_loop(m, tmem_base, ntiles, KC, lane);
   } else {
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;                   // 128-unit half of the 256-unit tile
+    const int half = (warp - 2) >> 2;
     const int r_in = q * 32 + lane;
     uint32_t it = 0;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const Tile x = tile_of(t, mt, n1, n2, L);
       const uint32_t acc = it & 1;
-      const uint32_t m0 = (tile / nt) * BM;
-      const uint32_t n0 = (tile % nt) * BN + half * (BN / 2);
       mbar_wait(&m.tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const uint32_t row = m0 + r_in;
+      const uint32_t row = x.m * BM + r_in;
       const bool valid = row < Q;
-      const uint32_t dst = valid ? a.row_dst[row] : NONE;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
-      const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + n0;
-      const size_t o = (size_t)(valid ? row : 0) * a.H + n0;
-      {  // warm L2 with the next tile's z and parent-state rows of this thread
-        const uint32_t nxt = tile + gridDim.x;
-        if (nxt < ntiles) {
-          const uint32_t nrow = (nxt / nt) * BM + r_in;
-          const uint32_t nn0 = (nxt % nt) * BN + half * (BN / 2);
-          if (nrow < Q) {
-            const float *zp = a.g_z + (size_t)nrow * a.H + nn0;
-            const float *sp = a.state + (size_t)a.row_src[nrow] * a.H + nn0;
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(zp + 32 * l));
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(sp + 32 * l));
-            }
-          }
+      if (x.kind == 0) {
+        epi_phase1(a, tbase, row, valid, half, x.j);
+        tc_fence_before();
+        mbar_arrive(&m.tempty[acc]);
+        // publish this warp's z / r.h columns to the phase-2 tiles of the M-tile
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(a.done1 + x.m, 1u);
         }
+      } else {
+        wait_phase1(a.done1 + x.m, target);               // acquire z of this M-tile
+        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2));
+        tc_fence_before();
+        mbar_arrive(&m.tempty[acc]);
       }
-      uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && dst != NONE)
-                          ? a.codes + (size_t)dst * a.cstride : nullptr;
-      unsigned long long hs = 0;
-      uint32_t signacc = 0;
-      // global operands of group g+1 (z, h, bias) are loaded while group g is
-      // processed; TMEM loads are double-buffered the same way
-      auto fetch = [&](int g, float4 *z4, float4 *h4, float *bias16) {
-        if (dst == NONE) return;
-        ld_bias16(a.bh + n0 + g * 16, bias16);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          z4[j] = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + 4 * j);
-          h4[j] = *reinterpret_cast<const float4 *>(hp + g * 16 + 4 * j);
-        }
-      };
-      auto process = [&](int g, const float *vu, const float4 *z4, const float4 *h4,
-                         const float *bias16) {
-        if (dst == NONE) return;
-        float hn[16];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float zz[4] = {z4[j].x, z4[j].y, z4[j].z, z4[j].w};
-          const float hh[4] = {h4[j].x, h4[j].y, h4[j].z, h4[j].w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float c = tanh_fast(vu[4 * j + t] + bias16[4 * j + t]);
-            hn[4 * j + t] = (1.0f - zz[t]) * hh[t] + zz[t] * c;
-          }
-        }
-        float4 *so = reinterpret_cast<float4 *>(a.state_out + (size_t)dst * a.H + n0 + g * 16);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) so[j] = make_float4(hn[4 * j], hn[4 * j + 1], hn[4 * j + 2], hn[4 * j + 3]);
-        if (a.cache) hs += encode16(a, hn, n0 + g * 16, code, signacc);
-      };
-      float va[16], vb[16], ba[16], bb2[16];
-      float4 za[4], ha[4], zb[4], hb[4];
-      fetch(0, za, ha, ba);
-      tmem_ld16(tbase, va);
-      tmem_ld_wait();
-#pragma unroll 1
-      for (int g = 0; g < BN / 32; g += 2) {
-        tmem_ld16(tbase + (g + 1) * 16, vb);
-        fetch(g + 1, zb, hb, bb2);
-        process(g, va, za, ha, ba);
-        tmem_ld_wait();
-        if (g + 2 < BN / 32) {
-          tmem_ld16(tbase + (g + 2) * 16, va);
-          fetch(g + 2, za, ha, ba);
-        }
-        process(g + 1, vb, zb, hb, bb2);
-        tmem_ld_wait();
-      }
-      tc_fence_before();
-      mbar_arrive(&m.tempty[acc]);
-      if (a.cache && dst != NONE) atomicAdd(&a.codehash[dst], hs);
     }
   }
   teardown(m, warp, tmem_base);
@@ -571,6 +589,7 @@ typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, 
 struct TcState {
   uint32_t E = 0, H = 0, nub = 0, bmax = 0;
   __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr, *a1 = nullptr;
+  uint32_t *done1 = nullptr;
   float *bzr = nullptr, *bh = nullptr;
   CUtensorMap map_w1, map_w2, map_a1, map_rh;
   bool bound = false;
@@ -643,8 +662,7 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_
   ok = ok && cudaMemcpy(t->bh, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && make_map(&t->map_w1, t->w1, K1, 2 * (uint64_t)H, BN) &&
        make_map(&t->map_w2, t->w2, K1, H, BN);
-  ok = ok && cudaFuncSetAttribute(k_gru1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   *state_out = t;
   if (!ok) {
     (void)cudaGetLastError();
@@ -658,7 +676,8 @@ int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax) {
   TcState *t = static_cast<TcState *>(state);
   t->rh16 = rh16;
   t->bmax = bmax;
-  if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * 2) != cudaSuccess) {
+  if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * 2) != cudaSuccess ||
+      cudaMalloc(&t->done1, ((size_t)bmax / BM + 2) * sizeof(uint32_t)) != cudaSuccess) {
     (void)cudaGetLastError();
     return -1;
   }
@@ -673,6 +692,7 @@ void gru_tc_release(void *state) {
   cudaFree(t->w1);
   cudaFree(t->w2);
   cudaFree(t->a1);
+  cudaFree(t->done1);
   cudaFree(t->bzr);
   cudaFree(t->bh);
   delete t;
@@ -690,17 +710,17 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.g_z = P.g_z; a.g_rh16 = P.g_rh16; a.a1 = t->a1;
   a.cache = P.cache; a.key_mode = P.key_mode; a.round_digits = P.round_digits;
   a.cstride = P.cstride; a.round_scale = P.round_scale; a.codes = P.codes; a.codehash = P.codehash;
+  a.done1 = t->done1;
+  a.lag = 16;
   const uint32_t mt = (max_rows + BM - 1) / BM;
-  uint32_t g1 = mt * t->nub, g2 = mt * (P.H / BN);
+  uint32_t g1 = mt * (t->nub + P.H / BN);
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
-  if (g2 > (uint32_t)num_sms) g2 = num_sms;
   uint32_t gg = (max_rows + 7) / 8;
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
   launch_pdl(k_gather_a1, gg, 256, 0, s, a);
   if (ev_gathered) cudaEventRecord(ev_gathered, s);
-  launch_pdl(k_gru1_tc, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, a);
+  launch_pdl(k_gru_tc, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
   if (ev_phase1) cudaEventRecord(ev_phase1, s);
-  launch_pdl(k_gru2_tc, g2, THREADS, SMEM, s, t->map_a1, t->map_rh, t->map_w2, a);
-  return 3;
+  return 2;
 }
 }  // namespace rnnlm_host
