@@ -711,7 +711,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.cache = P.cache; a.key_mode = P.key_mode; a.round_digits = P.round_digits;
   a.cstride = P.cstride; a.round_scale = P.round_scale; a.codes = P.codes; a.codehash = P.codehash;
   a.done1 = t->done1;
-  a.lag = 16;
+  a.lag = 48;
   const uint32_t mt = (max_rows + BM - 1) / BM;
   uint32_t g1 = mt * (t->nub + P.H / BN);
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
