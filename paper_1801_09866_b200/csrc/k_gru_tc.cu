@@ -177,6 +177,7 @@ struct TcArgs {
   __nv_bfloat16 *g_rh16;           // [B_max][H]
   __nv_bfloat16 *a1;               // [B_max][E+H] gathered phase-1 A operand
   uint32_t *done1;                 // per M-tile phase-1 epilogue arrivals (zeroed by the gather)
+  uint32_t *tile_ctr;              // dynamic tile scheduler (zeroed by the gather)
   uint32_t lag;                    // phase-2 tiles trail phase-1 tiles by this many M-tiles
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
   const uint32_t K1 = a.E + a.H;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (Q + BM - 1) / BM; i += gridDim.x * blockDim.x)
     a.done1[i] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.tile_ctr = 0u;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Q; r += nw) {
     const uint4 *x = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)a.row_word[r] * a.E);
     const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
@@ -217,10 +219,14 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 
+constexpr int TQ = 4;            // depth of the tile-id ring (producer -> MMA / epilogue)
+constexpr uint32_t NO_TILE = 0xFFFFFFFFu;
+
 struct Smem {
   uint8_t *sA, *sB;
-  uint64_t *full, *empty, *tfull, *tempty;
+  uint64_t *full, *empty, *tfull, *tempty, *qfull, *qempty;
   uint32_t *tmem_base;
+  uint32_t *tile_q;
 };
 
 __device__ __forceinline__ Smem carve(uint8_t *raw) {
@@ -232,7 +238,10 @@ __device__ __forceinline__ Smem carve(uint8_t *raw) {
   m.empty = m.full + ST;
   m.tfull = m.empty + ST;
   m.tempty = m.tfull + 2;
-  m.tmem_base = reinterpret_cast<uint32_t *>(m.tempty + 2);
+  m.qfull = m.tempty + 2;
+  m.qempty = m.qfull + TQ;
+  m.tmem_base = reinterpret_cast<uint32_t *>(m.qempty + TQ);
+  m.tile_q = m.tmem_base + 4;
   return m;
 }
 
@@ -240,6 +249,8 @@ __device__ __forceinline__ void setup(const Smem &m, int warp) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) { mbar_init(&m.full[s], 1); mbar_init(&m.empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&m.tfull[s], 1); mbar_init(&m.tempty[s], EPI_WARPS * 32); }
+    // tile ids: the producer publishes, the MMA lane and one lane per epilogue warp release
+    for (int s = 0; s < TQ; ++s) { mbar_init(&m.qfull[s], 1); mbar_init(&m.qempty[s], 1 + EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc(m.tmem_base, TMEM_COLS);
@@ -262,10 +273,11 @@ __device__ __forceinline__ void teardown(const Smem &m, int warp, uint32_t tmem_
 // nub phase-1 tiles P1(m, j) (z|r of units [128j, 128j+128)) and nt phase-2
 // tiles P2(m, j) (candidate of units [256j, 256j+256)).  Global order: step s
 // holds P1(s, *) then P2(s - L, *), so a phase-2 tile comes ~L M-tiles after
-// the phase-1 tiles it depends on (r.h of ALL units of its rows).  Every CTA
-// walks its tiles in increasing global index and a tile only waits on tiles
-// with smaller indices, so the persistent grid (all CTAs resident) cannot
-// deadlock.
+// the phase-1 tiles it depends on (r.h of ALL units of its rows).  CTAs claim
+// tiles from a global atomic counter, so tiles are started in increasing
+// index order by CTAs that are running; a tile only waits on tiles with
+// smaller indices, which were claimed earlier by running CTAs, so the kernel
+// makes progress whatever the number of co-resident CTAs.
 struct Tile {
   uint32_t kind, m, j;             // kind 0: phase 1, 1: phase 2
 };
@@ -295,12 +307,22 @@ __device__ __forceinline__ void wait_phase1(const uint32_t *cnt, uint32_t target
   while (ld_acquire(cnt) < target) __nanosleep(128);
 }
 
+// Next tile id from the producer's ring (MMA lane / epilogue warps).
+__device__ __forceinline__ uint32_t next_tile(const Smem &m, uint32_t it, bool release_lane) {
+  const uint32_t slot = it % TQ;
+  mbar_wait(&m.qfull[slot], (it / TQ) & 1);
+  const uint32_t t = *reinterpret_cast<volatile uint32_t *>(&m.tile_q[slot]);
+  __syncwarp();
+  if (release_lane) mbar_arrive(&m.qempty[slot]);
+  return t;
+}
+
 // MMA issuer: KC chunks of 4 x (M=128, N=256, K=16) per tile, both phases.
-__device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t ntiles,
-                                         uint32_t KC, int lane) {
-  uint32_t stage = 0, phase = 0, it = 0;
+__device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, int lane) {
+  uint32_t stage = 0, phase = 0;
   const uint32_t id = idesc_bf16(BM, BN);
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  for (uint32_t it = 0;; ++it) {
+    if (next_tile(m, it, lane == 0) == NO_TILE) break;
     const uint32_t acc = it & 1;
     mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
     tc_fence_after();
@@ -518,7 +540,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t slot = it % TQ;
+        mbar_wait(&m.qempty[slot], ((it / TQ) & 1) ^ 1);
+        uint32_t t = atomicAdd(a.tile_ctr, 1u);
+        if (t >= ntiles) t = NO_TILE;
+        m.tile_q[slot] = t;
+        mbar_arrive(&m.qfull[slot]);
+        if (t == NO_TILE) break;
         const Tile x = tile_of(t, mt, n1, n2, L);
         const uint32_t m0 = x.m * BM;
         if (x.kind == 1) {
@@ -542,13 +571,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    mma_loop(m, tmem_base, ntiles, KC, lane);
+    mma_loop(m, tmem_base, KC, lane);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r_in = q * 32 + lane;
-    uint32_t it = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t t = next_tile(m, it, lane == 0);
+      if (t == NO_TILE) break;
       const Tile x = tile_of(t, mt, n1, n2, L);
       const uint32_t acc = it & 1;
       mbar_wait(&m.tfull[acc], (it >> 1) & 1);
@@ -677,7 +707,7 @@ int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax) {
   t->rh16 = rh16;
   t->bmax = bmax;
   if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * 2) != cudaSuccess ||
-      cudaMalloc(&t->done1, ((size_t)bmax / BM + 2) * sizeof(uint32_t)) != cudaSuccess) {
+      cudaMalloc(&t->done1, ((size_t)bmax / BM + 4) * sizeof(uint32_t)) != cudaSuccess) {
     (void)cudaGetLastError();
     return -1;
   }
@@ -711,6 +741,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.cache = P.cache; a.key_mode = P.key_mode; a.round_digits = P.round_digits;
   a.cstride = P.cstride; a.round_scale = P.round_scale; a.codes = P.codes; a.codehash = P.codehash;
   a.done1 = t->done1;
+  a.tile_ctr = t->done1 + (t->bmax / BM + 2);
   a.lag = 48;
   const uint32_t mt = (max_rows + BM - 1) / BM;
   uint32_t g1 = mt * (t->nub + P.H / BN);
