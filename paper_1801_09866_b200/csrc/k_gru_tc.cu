@@ -34,6 +34,7 @@
 // discarded.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -608,6 +609,270 @@ __global__ void __launch_bounds__(THREADS, 1)
   teardown(m, warp, tmem_base);
 }
 
+// =============================================================== CTA-pair variant
+// Same tile stream and epilogues, but each tile is 256 rows computed by a CTA
+// pair (cluster of 2) with tcgen05.mma.cta_group::2 (M = 256, N = 256): each
+// CTA TMA-loads its own 128 A rows and HALF of the B tile (128 of 256 rows);
+// the pair's tensor cores read the peer's B half directly, so every SM pulls
+// 32 KB per K-chunk from L2 instead of 48 KB (the one-CTA kernel is
+// L2->SM-bandwidth bound).  The leader CTA claims tiles, issues the MMAs and
+// owns the pipeline barriers that both CTAs' TMA and epilogues signal.
+constexpr int STP = 6;                         // pair-kernel smem stages
+constexpr int BP_BYTES = (BN / 2) * BK * 2;    // 16 KB: this CTA's half of a B chunk
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// wait with cluster-scope acquire (the phase may have been completed by the peer CTA)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+__device__ __forceinline__ void st_cl_u32(uint32_t cl_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cl_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, uint32_t mbar_cl,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cl), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this smem offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)), "h"((uint16_t)3)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t *dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+
+struct SmemP {
+  uint8_t *sA, *sB;
+  uint64_t *full, *empty, *tfull, *tempty, *qfull, *qempty;
+  uint32_t *tmem_base, *tile_q;
+};
+
+__device__ __forceinline__ SmemP carve_pair(uint8_t *raw) {
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  SmemP m;
+  m.sA = smem;
+  m.sB = smem + STP * A_BYTES;
+  m.full = reinterpret_cast<uint64_t *>(m.sB + STP * BP_BYTES);
+  m.empty = m.full + STP;
+  m.tfull = m.empty + STP;
+  m.tempty = m.tfull + 2;
+  m.qfull = m.tempty + 2;
+  m.qempty = m.qfull + TQ;
+  m.tmem_base = reinterpret_cast<uint32_t *>(m.qempty + TQ);
+  m.tile_q = m.tmem_base + 4;
+  return m;
+}
+
+// warp 0: TMA producer (both CTAs; the leader also claims tiles);
+// warp 1: TMEM allocation (both) + MMA issue (leader only);
+// warps 2-9: epilogue of this CTA's 128 rows.
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gru_tc2(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1h,
+              const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2h,
+              TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const SmemP m = carve_pair(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t n1 = a.nub, n2 = a.H / BN;
+  const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
+  const uint32_t target = n1 * 2 * EPI_WARPS;           // phase-1 arrivals per 256-row tile
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STP; ++s) { mbar_init(&m.full[s], leader ? 2 : 1); mbar_init(&m.empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&m.tfull[s], 1); mbar_init(&m.tempty[s], 2 * EPI_WARPS); }
+    for (int s = 0; s < TQ; ++s) { mbar_init(&m.qfull[s], 1); mbar_init(&m.qempty[s], 2 * (2 + EPI_WARPS)); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&map_a1); prefetch_map(&map_w1h); prefetch_map(&map_rh); prefetch_map(&map_w2h);
+  }
+  if (warp == 1) tmem_alloc_pair(m.tmem_base, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();                                      // the peer's barriers exist
+  pdl_entry();
+  const uint32_t Q = a.counts[1];
+  const uint32_t mt = (Q + 2 * BM - 1) / (2 * BM);
+  const uint32_t L = mt < a.lag / 2 ? mt : a.lag / 2;
+  const uint32_t ntiles = mt * (n1 + n2);
+  const uint32_t tmem_base = *m.tmem_base;
+  const uint32_t full0 = mapa(smem_u32(&m.full[0]), 0);       // leader's barriers
+  const uint32_t tempty0 = mapa(smem_u32(&m.tempty[0]), 0);
+  const uint32_t qempty0 = mapa(smem_u32(&m.qempty[0]), 0);
+
+  // tile id of ring slot `it` for a consumer warp; one lane releases the slot
+  // on the leader's qempty (ring consumers: both CTAs' producer + epilogue warps)
+  auto take = [&](uint32_t it, bool release) -> uint32_t {
+    const uint32_t slot = it % TQ;
+    mbar_wait_cl(&m.qfull[slot], (it / TQ) & 1);
+    const uint32_t t = *reinterpret_cast<volatile uint32_t *>(&m.tile_q[slot]);
+    __syncwarp();
+    if (release) mbar_arrive_cl(qempty0 + slot * 8);
+    return t;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t it = 0;; ++it) {
+        uint32_t t;
+        if (leader) {
+          const uint32_t slot = it % TQ;
+          mbar_wait_cl(&m.qempty[slot], ((it / TQ) & 1) ^ 1);
+          t = atomicAdd(a.tile_ctr, 1u);
+          if (t >= ntiles) t = NO_TILE;
+          m.tile_q[slot] = t;
+          st_cl_u32(mapa(smem_u32(&m.tile_q[slot]), 1), t);
+          mbar_arrive(&m.qfull[slot]);
+          mbar_arrive_cl(mapa(smem_u32(&m.qfull[slot]), 1));
+          mbar_arrive_cl(qempty0 + slot * 8);          // the leader's producer is a ring consumer too
+        } else {
+          t = take(it, true);
+        }
+        if (t == NO_TILE) break;
+        const Tile x = tile_of(t, mt, n1, n2, L);
+        const uint32_t m0 = x.m * 2 * BM + rank * BM;
+        const uint32_t b0row = x.j * BN + rank * (BN / 2);
+        if (x.kind == 1) {
+          wait_phase1(a.done1 + x.m, target);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        for (uint32_t kc = 0; kc < KC; ++kc) {
+          mbar_wait(&m.empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&m.full[stage], 2 * (A_BYTES + BP_BYTES));
+          else mbar_arrive_cl(full0 + stage * 8);
+          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
+          const uint32_t fb = full0 + stage * 8;
+          if (x.kind == 0) {
+            tma_load_2d_pair(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
+            tma_load_2d_pair(dB, &map_w1h, fb, (int)(kc * BK), (int)b0row);
+          } else {
+            if (kc < kx) tma_load_2d_pair(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
+            else tma_load_2d_pair(dA, &map_rh, fb, (int)((kc - kx) * BK), (int)m0);
+            tma_load_2d_pair(dB, &map_w2h, fb, (int)(kc * BK), (int)b0row);
+          }
+          if (++stage == STP) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      uint32_t stage = 0, phase = 0;
+      const uint32_t id = idesc_bf16(2 * BM, BN);
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t slot = it % TQ;                  // the leader MMA lane reads its own ring
+        mbar_wait(&m.qfull[slot], (it / TQ) & 1);
+        const uint32_t t = *reinterpret_cast<volatile uint32_t *>(&m.tile_q[slot]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cl(qempty0 + slot * 8);
+        if (t == NO_TILE) break;
+        const uint32_t acc = it & 1;
+        mbar_wait_cl(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tm = tmem_base + acc * BN;
+        for (uint32_t kc = 0; kc < KC; ++kc) {
+          mbar_wait_cl(&m.full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_pair(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+            umma_commit_pair(&m.empty[stage]);
+            if (kc == KC - 1) umma_commit_pair(&m.tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == STP) { stage = 0; phase ^= 1; }
+        }
+      }
+    } else {
+      // the peer's MMA warp only consumes ring slots (keeps the qempty count uniform)
+      for (uint32_t it = 0;; ++it)
+        if (take(it, lane == 0) == NO_TILE) break;
+    }
+  } else {
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r_in = q * 32 + lane;
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t t = take(it, lane == 0);
+      if (t == NO_TILE) break;
+      const Tile x = tile_of(t, mt, n1, n2, L);
+      const uint32_t acc = it & 1;
+      mbar_wait(&m.tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t row = x.m * 2 * BM + rank * BM + r_in;
+      const bool valid = row < Q;
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
+      if (x.kind == 0) {
+        epi_phase1(a, tbase, row, valid, half, x.j);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(a.done1 + x.m, 1u);
+        }
+      } else {
+        wait_phase1(a.done1 + x.m, target);
+        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, TMEM_COLS);
+  }
+}
+
+constexpr size_t SMEM_PAIR = 1024 + STP * (A_BYTES + BP_BYTES) + 256;
+
 constexpr size_t SMEM = 1024 + ST * (A_BYTES + B_BYTES) + 256;
 
 // ---------------------------------------------------------------- host side
@@ -620,8 +885,9 @@ struct TcState {
   uint32_t E = 0, H = 0, nub = 0, bmax = 0;
   __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr, *a1 = nullptr;
   uint32_t *done1 = nullptr;
+  bool pair = true;                // CTA-pair (cta_group::2) kernel; RNNLM_TC_PAIR=0 selects one-CTA
   float *bzr = nullptr, *bh = nullptr;
-  CUtensorMap map_w1, map_w2, map_a1, map_rh;
+  CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h;
   bool bound = false;
 };
 
@@ -663,6 +929,7 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_
   *state_out = nullptr;
   TcState *t = new TcState;
   t->E = E; t->H = H; t->nub = H / UB;
+  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = atoi(e) != 0;
   const size_t K1 = E + H;
   std::vector<__nv_bfloat16> w1((size_t)2 * H * K1), w2((size_t)H * K1);
   std::vector<float> bzr((size_t)2 * H), bh(H);
@@ -691,8 +958,11 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_
   ok = ok && cudaMemcpy(t->bzr, bzr.data(), bzr.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bh, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && make_map(&t->map_w1, t->w1, K1, 2 * (uint64_t)H, BN) &&
-       make_map(&t->map_w2, t->w2, K1, H, BN);
+       make_map(&t->map_w2, t->w2, K1, H, BN) &&
+       make_map(&t->map_w1h, t->w1, K1, 2 * (uint64_t)H, BN / 2) &&
+       make_map(&t->map_w2h, t->w2, K1, H, BN / 2);
   ok = ok && cudaFuncSetAttribute(k_gru_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PAIR) == cudaSuccess;
   *state_out = t;
   if (!ok) {
     (void)cudaGetLastError();
@@ -750,7 +1020,15 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
   launch_pdl(k_gather_a1, gg, 256, 0, s, a);
   if (ev_gathered) cudaEventRecord(ev_gathered, s);
-  launch_pdl(k_gru_tc, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+  if (t->pair) {
+    uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / BN) * 2;
+    const uint32_t cap = (uint32_t)num_sms & ~1u;
+    if (gp > cap) gp = cap;
+    launch_pdl_cluster(k_gru_tc2, gp, THREADS, SMEM_PAIR, s, 2, t->map_a1, t->map_w1h, t->map_rh,
+                       t->map_w2h, a);
+  } else {
+    launch_pdl(k_gru_tc, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+  }
   if (ev_phase1) cudaEventRecord(ev_phase1, s);
   return 2;
 }
