@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t slot = it % TQ;
     mbar_wait_cl(&m.qfull[slot], (it / TQ) & 1);
     const uint32_t t = *reinterpret_cast<volatile uint32_t *>(&m.tile_q[slot]);
-    __syncwarp();
+    __syncwarp(__activemask());                      // the producer calls this from one lane
     if (release) mbar_arrive_cl(qempty0 + slot * 8);
     return t;
   };
