@@ -805,11 +805,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) mbar_arrive_cl(qempty0 + slot * 8);
         if (t == NO_TILE) break;
         const uint32_t acc = it & 1;
-        mbar_wait_cl(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tm = tmem_base + acc * BN;
         for (uint32_t kc = 0; kc < KC; ++kc) {
-          mbar_wait_cl(&m.full[stage], phase);
+          mbar_wait(&m.full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
@@ -885,7 +885,7 @@ struct TcState {
   uint32_t E = 0, H = 0, nub = 0, bmax = 0;
   __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr, *a1 = nullptr;
   uint32_t *done1 = nullptr;
-  bool pair = true;                // CTA-pair (cta_group::2) kernel; RNNLM_TC_PAIR=0 selects one-CTA
+  bool pair = false;               // CTA-pair (cta_group::2) kernel (experimental): RNNLM_TC_PAIR=1
   float *bzr = nullptr, *bh = nullptr;
   CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h;
   bool bound = false;
