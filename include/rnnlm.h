@@ -24,6 +24,8 @@
  *   - One rnnlm_t per CUDA device; one host thread per handle at a time.
  *   - Every call that takes a cudaStream_t is stream-ordered and asynchronous
  *     and allocates nothing (so a caller may capture it in a CUDA graph).
+ *     rnnlm_query_batch forks part of its work onto an internal stream and
+ *     joins it back into the caller's stream before returning.
  *     rnnlm_cache_stats, rnnlm_get_timing and rnnlm_create/destroy synchronise.
  *   - Pointers named d_* are DEVICE pointers owned by the caller; they must
  *     stay valid until the work on the given stream completes.  Pointers
@@ -114,17 +116,18 @@ typedef struct {
   int32_t pad_;
 } rnnlm_stats;
 
-/* Per-kernel-group device time accumulated while timing is enabled
- * (CUDA events on the caller's stream around each group). */
+/* Per-kernel-group device time accumulated while timing is enabled (CUDA
+ * events around each group, on the stream the group runs on; scoring and the
+ * result write run on an internal side stream concurrently with the GRU). */
 typedef struct {
   double ms_cache;      /* key/probe/claim/scan/commit kernels (a1-a4) */
-  double ms_score;      /* NCE + MaxEnt scoring (a6) */
+  double ms_score;      /* NCE + MaxEnt scoring (a6), side stream */
   double ms_gru;        /* gather + gate contraction + gates, both phases (a5) */
-  double ms_encode;     /* code + code hash of new states (a1, at state creation) */
-  double ms_final;      /* result write + counters (a7) */
+  double ms_encode;     /* code + code hash of new states (a1; FP32 path only) */
+  double ms_final;      /* result write + counters (a7), side stream */
   uint64_t calls;       /* timed query_batch calls */
   uint64_t launches;    /* kernels launched by those calls */
-  /* timing level 2, BF16 path only: split of ms_gru */
+  /* timing level 2, BF16 path only: split of ms_gru (gather, fused GEMM) */
   double ms_gru_gather, ms_gru_phase1, ms_gru_phase2;
 } rnnlm_timing;
 

@@ -30,6 +30,9 @@ struct rnnlm {
   void *tc = nullptr;                 // tensor-core GRU state (descriptors, weights)
   uint32_t epoch = 0;
   uint64_t launches = 0;
+  // scoring + result write run on a side stream, concurrently with the GRU
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // timing
   int timing = 0;
   std::vector<cudaEvent_t> ev_pool;
@@ -39,7 +42,9 @@ struct rnnlm {
 
 namespace {
 
-constexpr int NEV = 6;
+// per timed call: [0] start, [1] fork (after commit), [2] score end, [3] final end (side
+// stream), [4] gathered (level 2), [5] GRU end, [6] encode end (main stream)
+constexpr int NEV = 7;
 
 rnnlm_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return RNNLM_OK;
@@ -111,6 +116,11 @@ void free_all(rnnlm *h) {
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   h->ev_pending.clear();
   h->ev_pool.clear();
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->side) cudaStreamDestroy(h->side);
+  h->ev_fork = h->ev_join = nullptr;
+  h->side = nullptr;
 }
 
 cudaEvent_t take_event(rnnlm *h) {
@@ -268,6 +278,9 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   }
   if (st == RNNLM_OK && c.math == RNNLM_MATH_BF16 && rnnlm_host::gru_tc_bind(h->tc, P.g_rh16, (uint32_t)B) != 0)
     st = RNNLM_E_CUDA;
+  if (st == RNNLM_OK) chk(cuda_status(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking)));
+  if (st == RNNLM_OK) chk(cuda_status(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)));
+  if (st == RNNLM_OK) chk(cuda_status(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming)));
   if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.sticky, 0, sizeof(int))));
   if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.counts, 0, 4 * sizeof(uint32_t))));
   if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.row_dst, 0xFF, B * sizeof(uint32_t))));
@@ -339,30 +352,34 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
     for (int i = 0; i < NEV; ++i) ev.push_back(take_event(h));
     cudaEventRecord(ev[0], s);
   }
+  // (a1)-(a4) on the caller's stream
   int k = 0;
   k += rnnlm_host::launch_cache_front(P, A, s);
   k += rnnlm_host::launch_commit(P, A, s);
-  if (h->timing) cudaEventRecord(ev[1], s);
-  k += rnnlm_host::launch_score(P, A, h->num_sms, s);
-  if (h->timing) cudaEventRecord(ev[2], s);
+  // fork: (a6) scoring and (a7) result write depend only on the commit; the
+  // GRU (a5) too.  Scoring + result write go to the side stream and overlap
+  // the tensor-core GRU; the caller's stream joins them before returning.
+  cudaEvent_t fork = h->timing ? ev[1] : h->ev_fork;
+  cudaEventRecord(fork, s);
+  cudaStreamWaitEvent(h->side, fork, 0);
+  k += rnnlm_host::launch_score(P, A, h->num_sms, h->side);
+  if (h->timing) cudaEventRecord(ev[2], h->side);
+  k += rnnlm_host::launch_final(P, A, h->side);
+  if (h->timing) cudaEventRecord(ev[3], h->side);
+  cudaEventRecord(h->ev_join, h->side);
   if (P.math == RNNLM_MATH_BF16) {
-    cudaEvent_t e1 = nullptr, e2 = nullptr;
-    if (h->timing >= 2) {
-      e1 = take_event(h);
-      e2 = take_event(h);
-      ev.push_back(e1);
-      ev.push_back(e2);
-    }
-    k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s, e1, e2);
+    k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s, h->timing >= 2 ? ev[4] : nullptr,
+                                   nullptr);
+  } else {
+    k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
   }
-  else k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
-  if (h->timing) cudaEventRecord(ev[3], s);
+  if (h->timing) cudaEventRecord(ev[5], s);
   if (P.math != RNNLM_MATH_BF16)                      // the tcgen05 epilogue encodes in place
     k += rnnlm_host::launch_encode_rows(P, n, h->num_sms, s);
-  if (h->timing) cudaEventRecord(ev[4], s);
-  k += rnnlm_host::launch_final(P, A, s);
+  if (h->timing) cudaEventRecord(ev[6], s);
+  cudaStreamWaitEvent(s, h->ev_join, 0);
   if (h->timing) {
-    cudaEventRecord(ev[5], s);
+    if (h->timing < 2) { h->ev_pool.push_back(ev[4]); ev[4] = nullptr; }
     h->ev_pending.push_back(ev);
     h->acc.calls += 1;
     h->acc.launches += (uint64_t)k;
@@ -457,25 +474,25 @@ rnnlm_status rnnlm_set_timing(rnnlm_t *h, int level) {
 rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset) {
   if (!h || !out) return RNNLM_E_INVALID_ARG;
   for (auto &ev : h->ev_pending) {
-    cudaError_t e = cudaEventSynchronize(ev[NEV - 1]);
+    cudaError_t e = cudaEventSynchronize(ev[6]);
+    if (!e) e = cudaEventSynchronize(ev[3]);
     if (e) return cuda_status(e);
-    float ms[NEV - 1];
-    for (int i = 0; i + 1 < NEV; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
-    h->acc.ms_cache += ms[0];
-    h->acc.ms_score += ms[1];
-    h->acc.ms_gru += ms[2];
-    h->acc.ms_encode += ms[3];
-    h->acc.ms_final += ms[4];
-    if (ev.size() >= NEV + 2) {          // level 2: [2]=before GRU, [6]=gathered, [7]=phase 1, [3]=after GRU
-      float a, b, c;
-      cudaEventElapsedTime(&a, ev[2], ev[NEV]);
-      cudaEventElapsedTime(&b, ev[NEV], ev[NEV + 1]);
-      cudaEventElapsedTime(&c, ev[NEV + 1], ev[3]);
-      h->acc.ms_gru_gather += a;
-      h->acc.ms_gru_phase1 += b;
-      h->acc.ms_gru_phase2 += c;
+    auto el = [](cudaEvent_t x, cudaEvent_t y) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, x, y);
+      return (double)ms;
+    };
+    h->acc.ms_cache += el(ev[0], ev[1]);
+    h->acc.ms_score += el(ev[1], ev[2]);
+    h->acc.ms_final += el(ev[2], ev[3]);
+    h->acc.ms_gru += el(ev[1], ev[5]);
+    h->acc.ms_encode += el(ev[5], ev[6]);
+    if (ev[4]) {
+      h->acc.ms_gru_gather += el(ev[1], ev[4]);
+      h->acc.ms_gru_phase1 += el(ev[4], ev[5]);
     }
-    for (cudaEvent_t e2 : ev) h->ev_pool.push_back(e2);
+    for (cudaEvent_t e2 : ev)
+      if (e2) h->ev_pool.push_back(e2);
   }
   h->ev_pending.clear();
   *out = h->acc;

@@ -471,7 +471,7 @@ int launch_commit(const Params &P, const CallArgs &A, cudaStream_t s) {
 }
 
 int launch_final(const Params &P, const CallArgs &A, cudaStream_t s) {
-  launch_pdl(k_final, nblk(A.n, 256), 256, 0, s, P, A);
+  launch_pdl(k_final, nblk(A.n, 128), 128, 0, s, P, A);
   return 1;
 }
 

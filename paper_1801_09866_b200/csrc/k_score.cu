@@ -37,7 +37,7 @@ __device__ __forceinline__ unsigned long long maxent_index(const Rec &r, uint32_
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 
-__global__ void __launch_bounds__(256) k_score(Params P, CallArgs A) {
+__global__ void __launch_bounds__(128) k_score(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t total = P.counts[0];
   const uint32_t lane = threadIdx.x & 31;
@@ -106,10 +106,11 @@ using namespace rnnlm_dev;
 
 int launch_score(const Params &P, const CallArgs &A, int num_sms, cudaStream_t s) {
   if (!A.n) return 0;
-  uint32_t blocks = (A.n + 7) / 8;                    // <= one warp per query
+  // 128-thread blocks (four warps) so that they fit beside a GRU CTA on the same SM
+  uint32_t blocks = (A.n + 3) / 4;                    // <= one warp per query
   const uint32_t cap = (uint32_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
-  launch_pdl(k_score, blocks, 256, 0, s, P, A);
+  launch_pdl(k_score, blocks, 128, 0, s, P, A);
   return 1;
 }
 
