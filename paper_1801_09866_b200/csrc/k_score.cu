@@ -8,12 +8,12 @@
 // (reading 13).  The score conditions on the PARENT history (reading 2), so
 // this kernel does not depend on this call's GRU work.
 //
-// One warp per non-QHIT query (compacted list from k_commit): lanes stream the
-// word's output row (fp32, or bf16 when every entry is bf16-exact) and the
-// parent state with 16-byte loads, then a fixed xor-butterfly reduction
-// (identical result in every lane, independent of the batch).  Lane k < K
-// evaluates the order-(k+1) MaxEnt index and gathers one table entry; the K
-// values are added in order 1..K.
+// Eight lanes per non-QHIT query (compacted list from k_commit), four queries
+// per warp: lanes stream the word's output row (fp32, or bf16 when every entry
+// is bf16-exact) and the parent state with 16-byte loads, then a fixed
+// xor-butterfly reduction over the eight lanes (deterministic, independent of
+// the batch).  Lane k < K of the group evaluates the order-(k+1) MaxEnt index
+// and gathers one table entry; the K values are added in order 1..K.
 //   idx_1 = w mod M;  idx_k = (idx_{k-1} * 237967 + ctx_{k-1} + 1) mod M
 // (reading 11; ctx_{k-1} = (k-1)-th most recent word, u64).
 #include "rnnlm_impl.cuh"
@@ -37,47 +37,66 @@ __device__ __forceinline__ unsigned long long maxent_index(const Rec &r, uint32_
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 
+// Four queries per warp, eight lanes per query: each lane streams H/8 output
+// weights and state elements with 16-byte loads (many independent loads in
+// flight), then a fixed xor-tree over the eight lanes.
 __global__ void __launch_bounds__(128) k_score(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t total = P.counts[0];
-  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31, gid = lane >> 3, gl = lane & 7;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nw) {
-    const uint32_t q = P.nonq_list[i];
-    if (P.st[q] == ST_INVALID) continue;                 // warp-uniform
-    const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
-    const size_t cb = (size_t)s * P.cap;
-    const Rec pr = P.rec[cb + p];
-    const float *h = P.state + (cb + pr.slot) * P.H;
+  const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (uint32_t base = wg * 4; base < total; base += nw * 4) {
+    const uint32_t i = base + gid;
+    uint32_t q = i < total ? P.nonq_list[i] : 0u;
+    const bool act = i < total && P.st[q] != ST_INVALID;
+    uint32_t s = 0, w = 0;
+    Rec pr;
+    pr.slot = 0;
+    for (int j = 0; j < MAX_CTX; ++j) pr.ctx[j] = NONE;
+    if (act) {
+      s = A.session[q];
+      w = A.word[q];
+      pr = P.rec[(size_t)s * P.cap + A.parent[q]];
+    }
+    const float *h = P.state + ((size_t)s * P.cap + pr.slot) * P.H;
     float acc = 0.0f;
-    if (P.nce_w16) {
-      const uint4 *row = reinterpret_cast<const uint4 *>(P.nce_w16 + (size_t)w * P.H);
-      for (uint32_t j = lane; j < P.H / 8; j += 32) {
-        const uint4 t = __ldg(row + j);
-        const float4 h0 = reinterpret_cast<const float4 *>(h)[2 * j];
-        const float4 h1 = reinterpret_cast<const float4 *>(h)[2 * j + 1];
-        acc = fmaf(bf16lo(t.x), h0.x, acc); acc = fmaf(bf16hi(t.x), h0.y, acc);
-        acc = fmaf(bf16lo(t.y), h0.z, acc); acc = fmaf(bf16hi(t.y), h0.w, acc);
-        acc = fmaf(bf16lo(t.z), h1.x, acc); acc = fmaf(bf16hi(t.z), h1.y, acc);
-        acc = fmaf(bf16lo(t.w), h1.z, acc); acc = fmaf(bf16hi(t.w), h1.w, acc);
-      }
-    } else {
-      const float4 *row = reinterpret_cast<const float4 *>(P.nce_w + (size_t)w * P.H);
-      for (uint32_t j = lane; j < P.H / 4; j += 32) {
-        const float4 t = __ldg(row + j);
-        const float4 hv = reinterpret_cast<const float4 *>(h)[j];
-        acc = fmaf(t.x, hv.x, acc); acc = fmaf(t.y, hv.y, acc);
-        acc = fmaf(t.z, hv.z, acc); acc = fmaf(t.w, hv.w, acc);
+    if (act) {
+      if (P.nce_w16) {
+        const uint4 *row = reinterpret_cast<const uint4 *>(P.nce_w16 + (size_t)w * P.H);
+#pragma unroll 4
+        for (uint32_t j = gl; j < P.H / 8; j += 8) {
+          const uint4 t = __ldg(row + j);
+          const float4 h0 = reinterpret_cast<const float4 *>(h)[2 * j];
+          const float4 h1 = reinterpret_cast<const float4 *>(h)[2 * j + 1];
+          acc = fmaf(bf16lo(t.x), h0.x, acc); acc = fmaf(bf16hi(t.x), h0.y, acc);
+          acc = fmaf(bf16lo(t.y), h0.z, acc); acc = fmaf(bf16hi(t.y), h0.w, acc);
+          acc = fmaf(bf16lo(t.z), h1.x, acc); acc = fmaf(bf16hi(t.z), h1.y, acc);
+          acc = fmaf(bf16lo(t.w), h1.z, acc); acc = fmaf(bf16hi(t.w), h1.w, acc);
+        }
+      } else {
+        const float4 *row = reinterpret_cast<const float4 *>(P.nce_w + (size_t)w * P.H);
+#pragma unroll 4
+        for (uint32_t j = gl; j < P.H / 4; j += 8) {
+          const float4 t = __ldg(row + j);
+          const float4 hv = reinterpret_cast<const float4 *>(h)[j];
+          acc = fmaf(t.x, hv.x, acc); acc = fmaf(t.y, hv.y, acc);
+          acc = fmaf(t.z, hv.z, acc); acc = fmaf(t.w, hv.w, acc);
+        }
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    const uint32_t K = min(P.N, ctx_len(pr, P.N) + 1);
+    for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const uint32_t K = act ? min(P.N, ctx_len(pr, P.N) + 1) : 0u;
     float me = 0.0f;
-    if (lane < K) me = __ldg(P.maxent + maxent_index(pr, w, lane + 1, P.M_mask));
-    float sc = acc + __ldg(P.nce_b + w);
-    for (uint32_t k = 0; k < K; ++k) sc += __shfl_sync(0xffffffffu, me, k);
-    if (lane == 0) {
+    if (gl < K) me = __ldg(P.maxent + maxent_index(pr, w, gl + 1, P.M_mask));
+    float sc = acc + (act ? __ldg(P.nce_b + w) : 0.0f);
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      const float v = __shfl_sync(0xffffffffu, me, (lane & ~7u) + k);
+      if (k < K) sc += v;
+    }
+    if (act && gl == 0) {
       A.score[q] = sc;
       if (P.cache) P.qtab[(size_t)s * (P.qmask + 1) + P.qent[q]].score = sc;
     }
@@ -107,7 +126,7 @@ using namespace rnnlm_dev;
 int launch_score(const Params &P, const CallArgs &A, int num_sms, cudaStream_t s) {
   if (!A.n) return 0;
   // 128-thread blocks (four warps) so that they fit beside a GRU CTA on the same SM
-  uint32_t blocks = (A.n + 3) / 4;                    // <= one warp per query
+  uint32_t blocks = (A.n + 15) / 16;                  // <= one 8-lane group per query
   const uint32_t cap = (uint32_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
   launch_pdl(k_score, blocks, 128, 0, s, P, A);
