@@ -42,7 +42,7 @@ struct rnnlm {
 
 namespace {
 
-// per timed call: [0] start, [1] fork (after commit), [2] score end, [3] final end (side
+// per timed call: [0] start, [1] fork (after commit), [2] final end, [3] score end (side
 // stream), [4] gathered (level 2), [5] GRU end, [6] encode end (main stream)
 constexpr int NEV = 7;
 
@@ -262,7 +262,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   chk(dalloc(h, &P.sticky, 1));
   // ---- scratch
   uint32_t **u32s[] = {&P.st, &P.qent, &P.aux, &P.hent, &P.pslot, &P.cslot, &P.excl_nonq,
-                       &P.excl_miss, &P.nonq_list, &P.row_src, &P.row_dst, &P.row_word};
+                       &P.excl_miss, &P.nonq_list, &P.dup_list, &P.row_src, &P.row_dst, &P.row_word};
   for (uint32_t **p : u32s) chk(dalloc(h, p, B));
   uint32_t **segs[] = {&P.seg_excl_nonq, &P.seg_excl_miss, &P.seg_cnt_nonq, &P.seg_cnt_miss};
   for (uint32_t **p : segs) chk(dalloc(h, p, S));
@@ -278,7 +278,12 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   }
   if (st == RNNLM_OK && c.math == RNNLM_MATH_BF16 && rnnlm_host::gru_tc_bind(h->tc, P.g_rh16, (uint32_t)B) != 0)
     st = RNNLM_E_CUDA;
-  if (st == RNNLM_OK) chk(cuda_status(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking)));
+  if (st == RNNLM_OK) {
+    // scoring + result write are short; give them priority over the GRU's CTAs
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    chk(cuda_status(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi)));
+  }
   if (st == RNNLM_OK) chk(cuda_status(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)));
   if (st == RNNLM_OK) chk(cuda_status(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming)));
   if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.sticky, 0, sizeof(int))));
@@ -362,9 +367,10 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
   cudaEvent_t fork = h->timing ? ev[1] : h->ev_fork;
   cudaEventRecord(fork, s);
   cudaStreamWaitEvent(h->side, fork, 0);
-  k += rnnlm_host::launch_score(P, A, h->num_sms, h->side);
-  if (h->timing) cudaEventRecord(ev[2], h->side);
   k += rnnlm_host::launch_final(P, A, h->side);
+  if (h->timing) cudaEventRecord(ev[2], h->side);
+  k += rnnlm_host::launch_score(P, A, h->num_sms, h->side);
+  k += rnnlm_host::launch_dup_scores(P, A, h->num_sms, h->side);
   if (h->timing) cudaEventRecord(ev[3], h->side);
   cudaEventRecord(h->ev_join, h->side);
   if (P.math == RNNLM_MATH_BF16) {
@@ -483,8 +489,8 @@ rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset) {
       return (double)ms;
     };
     h->acc.ms_cache += el(ev[0], ev[1]);
-    h->acc.ms_score += el(ev[1], ev[2]);
-    h->acc.ms_final += el(ev[2], ev[3]);
+    h->acc.ms_final += el(ev[1], ev[2]);
+    h->acc.ms_score += el(ev[2], ev[3]);
     h->acc.ms_gru += el(ev[1], ev[5]);
     h->acc.ms_encode += el(ev[5], ev[6]);
     if (ev[4]) {

@@ -21,7 +21,8 @@
 //   k_scan    owner == q -> MISS else SHIT; one decoupled look-back scan
 //             over (non-QHIT, MISS) flags -> dense handles and slots
 //   k_commit  records, cache values, GRU row list, scoring list
-//   k_final   QHIT results, outcomes, counters, allocation cursors
+//   k_final   QHIT results (handles), outcomes, counters, allocation cursors
+//   k_dup_scores  same-call duplicates copy their owner's score (after k_score)
 //
 // Kernel boundaries separate "claim" from "read owner", which is what makes
 // the outcome independent of thread scheduling.
@@ -73,7 +74,7 @@ __global__ void k_qprobe(Params P, CallArgs A, uint32_t ntiles) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < ntiles) P.tile_status[q] = 0ull;
-  if (q == 0) *P.tile_ticket = 0u;
+  if (q == 0) { *P.tile_ticket = 0u; P.counts[3] = 0u; }
   if (q >= A.n) return;
   const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
   int err = 0;
@@ -371,11 +372,17 @@ __global__ void k_final(Params P, CallArgs A) {
       A.child[q] = e.child;
       if (e.child == NONE) st = ST_INVALID; else oc = RNNLM_QHIT;   // entry of a failed query
     } else if (st == ST_QHIT_NEW) {
+      // the owner's handle is final after k_commit; its score is copied by
+      // k_dup_scores once k_score has run
       const uint32_t o = P.aux[q];
       const uint32_t c = A.child[o];
-      A.score[q] = A.score[o];
       A.child[q] = c;
-      if (c == NONE) st = ST_INVALID; else oc = RNNLM_QHIT;
+      if (c == NONE) {
+        st = ST_INVALID;
+      } else {
+        oc = RNNLM_QHIT;
+        P.dup_list[atomicAdd(&P.counts[3], 1u)] = q;
+      }
     } else if (st == ST_SHIT_OLD || st == ST_SHIT_NEW) {
       oc = RNNLM_SHIT;
     } else if (st == ST_MISS || st == ST_MISS_NC) {
@@ -412,6 +419,16 @@ __global__ void k_final(Params P, CallArgs A) {
     const uint32_t ns = c->next_slot + P.seg_cnt_miss[s];
     c->next_handle = nh < P.cap ? nh : P.cap;
     c->next_slot = ns < P.cap ? ns : P.cap;
+  }
+}
+
+// Duplicates of this call's new queries (QHIT_NEW) take their owner's score.
+__global__ void k_dup_scores(Params P, CallArgs A) {
+  pdl_entry();
+  const uint32_t nd = P.counts[3];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
+    const uint32_t q = P.dup_list[i];
+    A.score[q] = A.score[P.aux[q]];
   }
 }
 
@@ -467,6 +484,13 @@ int launch_cache_front(const Params &P, const CallArgs &A, cudaStream_t s) {
 
 int launch_commit(const Params &P, const CallArgs &A, cudaStream_t s) {
   launch_pdl(k_commit, nblk(A.n, 256), 256, 0, s, P, A);
+  return 1;
+}
+
+int launch_dup_scores(const Params &P, const CallArgs &A, int num_sms, cudaStream_t s) {
+  uint32_t blocks = nblk(A.n, 128);
+  if (blocks > (uint32_t)num_sms) blocks = num_sms;
+  launch_pdl(k_dup_scores, blocks, 128, 0, s, P, A);
   return 1;
 }
 

@@ -91,11 +91,12 @@ struct Params {
   // per-call scratch (B_max)
   uint32_t *st, *qent, *aux, *hent, *pslot, *cslot, *excl_nonq, *excl_miss;
   uint32_t *nonq_list;
+  uint32_t *dup_list;             // QHIT_NEW queries of this call (count in counts[3])
   uint32_t *row_src, *row_dst, *row_word;   // GRU rows: global state rows + word
   uint32_t *seg_excl_nonq, *seg_excl_miss, *seg_cnt_nonq, *seg_cnt_miss;  // per session
   unsigned long long *tile_status;
   uint32_t *tile_ticket;
-  uint32_t *counts;               // [0] non-QHIT total, [1] GRU rows, [2] bad-batch epoch
+  uint32_t *counts;               // [0] non-QHIT total, [1] GRU rows, [2] bad-batch epoch, [3] duplicates
   // GRU intermediates (rows x H)
   float *g_z, *g_rh, *g_wxb;
   __nv_bfloat16 *g_rh16;
@@ -175,6 +176,7 @@ int launch_cache_front(const Params &P, const CallArgs &A, cudaStream_t s);   //
 int launch_commit(const Params &P, const CallArgs &A, cudaStream_t s);
 int launch_score(const Params &P, const CallArgs &A, int num_sms, cudaStream_t s);
 int launch_final(const Params &P, const CallArgs &A, cudaStream_t s);
+int launch_dup_scores(const Params &P, const CallArgs &A, int num_sms, cudaStream_t s);
 int launch_gru_simt(const Params &P, uint32_t max_rows, int num_sms, cudaStream_t s);
 int launch_encode_rows(const Params &P, uint32_t max_rows, int num_sms, cudaStream_t s);
 int launch_reset_root(const Params &P, uint32_t s_lo, uint32_t s_hi, cudaStream_t s);
