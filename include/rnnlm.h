@@ -88,7 +88,7 @@ typedef enum {
 typedef enum { RNNLM_QHIT = 0, RNNLM_SHIT = 1, RNNLM_MISS = 2, RNNLM_INVALID = 255 } rnnlm_outcome;
 
 typedef struct {
-  uint32_t vocab, embed, hidden;        /* V >= 2 (word 0 = <s>), E, H; E and H multiples of 8 */
+  uint32_t vocab, embed, hidden;        /* 2 <= V < 2^31 (word 0 = <s>), E, H; E and H multiples of 8 */
   uint32_t maxent_log2, maxent_order;   /* MaxEnt table M = 2^maxent_log2 floats (<= 2^31); order N in 1..8 */
   uint32_t key_mode, round_digits;      /* rnnlm_key_mode; round_digits in 1..4 when ROUND */
   uint32_t math;                        /* rnnlm_math */

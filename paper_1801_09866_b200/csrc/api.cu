@@ -166,7 +166,8 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   if (c.vocab < 2 || c.embed == 0 || c.hidden == 0 || c.embed % 8 || c.hidden % 8 ||
       c.maxent_order < 1 || c.maxent_order > 8 || c.maxent_log2 > 31 || c.num_sessions == 0 ||
       c.max_queries_per_call == 0 || c.max_histories_per_session < 2 ||
-      c.max_histories_per_session > 0x7FFFFFFFu || c.max_queries_per_call > 0x7FFFFFFFu)
+      c.max_histories_per_session > 0x7FFFFFFFu || c.max_queries_per_call > 0x7FFFFFFFu ||
+      c.vocab > 0x7FFFFFFFu)
     return RNNLM_E_DIMENSION;
   if (c.key_mode > RNNLM_KEY_SIGN) return RNNLM_E_INVALID_ARG;
   if (c.key_mode == RNNLM_KEY_ROUND && (c.round_digits < 1 || c.round_digits > 4))
@@ -264,6 +265,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   uint32_t **u32s[] = {&P.st, &P.qent, &P.aux, &P.hent, &P.pslot, &P.cslot, &P.excl_nonq,
                        &P.excl_miss, &P.nonq_list, &P.dup_list, &P.row_src, &P.row_dst, &P.row_word};
   for (uint32_t **p : u32s) chk(dalloc(h, p, B));
+  chk(dalloc(h, &P.claimed, B));
   uint32_t **segs[] = {&P.seg_excl_nonq, &P.seg_excl_miss, &P.seg_cnt_nonq, &P.seg_cnt_miss};
   for (uint32_t **p : segs) chk(dalloc(h, p, S));
   chk(dalloc(h, &P.tile_status, (B + rnnlm_host::SCAN_TILE - 1) / rnnlm_host::SCAN_TILE));

@@ -11,16 +11,14 @@
 // (SURVEY 8(c)); the GPU reproduces it bit-exactly with a deterministic
 // "first occupant = lowest query index" rule:
 //
-//   k_qprobe  read-only probe of the LM-query cache (entries from earlier
-//             calls only: nothing is inserted yet) + validation
-//   k_qclaim  not-found keys: CAS-insert (or find the concurrent insert),
-//             atomicMin(owner, q)
-//   k_hprobe  owner == q -> first occurrence (non-QHIT); else duplicate.
-//             First occurrences probe the hidden cache read-only
-//   k_hclaim  not-found hidden keys: CAS-insert / find + atomicMin(owner, q)
+//   k_qcache  validation; LM-query cache probe: a key left by an earlier call
+//             is a hit, otherwise CAS-insert (or join the concurrent insert)
+//             of the key tagged NEW and atomicMin(owner, q)
+//   k_hcache  owner == q -> first occurrence (non-QHIT); else duplicate.
+//             First occurrences probe + claim the hidden cache the same way
 //   k_scan    owner == q -> MISS else SHIT; one decoupled look-back scan
 //             over (non-QHIT, MISS) flags -> dense handles and slots
-//   k_commit  records, cache values, GRU row list, scoring list
+//   k_commit  records, cache values (NEW tags cleared), GRU row list, scoring list
 //   k_final   QHIT results (handles), outcomes, counters, allocation cursors
 //   k_dup_scores  same-call duplicates copy their owner's score (after k_score)
 //
@@ -69,13 +67,21 @@ __device__ __forceinline__ bool hkey_match(const Params &P, unsigned long long t
   return code_equal(P, base + ref, base + ps);
 }
 
-// ---- (a2) probe -------------------------------------------------------------
-__global__ void k_qprobe(Params P, CallArgs A, uint32_t ntiles) {
+// Entries inserted during the current call carry NEW_BIT in their word field;
+// entries of earlier calls never do (k_commit clears the bit).  A probe that
+// meets its key without the bit is a hit on an earlier call; with the bit, a
+// key claimed concurrently in this call.  Chains are never shortened, so an
+// earlier-call entry of a key always precedes every slot filled in this call.
+constexpr unsigned long long NEW_BIT = 1ull << 31;
+
+// ---- (a2) LM-query cache: probe + claim ---------------------------------------
+__global__ void k_qcache(Params P, CallArgs A, uint32_t ntiles) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < ntiles) P.tile_status[q] = 0ull;
   if (q == 0) { *P.tile_ticket = 0u; P.counts[3] = 0u; }
   if (q >= A.n) return;
+  P.claimed[q] = 0;
   const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
   int err = 0;
   if (s >= P.S) err = RNNLM_E_INVALID_ARG;
@@ -94,48 +100,29 @@ __global__ void k_qprobe(Params P, CallArgs A, uint32_t ntiles) {
     P.pslot[q] = P.rec[(size_t)s * P.cap + p].slot;
     return;
   }
-  const unsigned long long key = ((unsigned long long)p << 32) | w;
+  const unsigned long long key = ((unsigned long long)p << 32) | w, nkey = key | NEW_BIT;
   const size_t base = (size_t)s * (P.qmask + 1);
   uint32_t idx = (uint32_t)(mix64(key) & P.qmask);
   for (uint32_t probes = 0; probes <= P.qmask; ++probes) {
-    const unsigned long long t = P.qtab[base + idx].tag;
+    unsigned long long t = vload64(&P.qtab[base + idx].tag);
     if (t == key) { P.st[q] = ST_QHIT_OLD; P.qent[q] = idx; return; }
-    if (t == TAG_EMPTY) { P.st[q] = ST_QNEED; P.qent[q] = idx; return; }
+    if (t == TAG_EMPTY) t = atomicCAS(&P.qtab[base + idx].tag, TAG_EMPTY, nkey);
+    if (t == TAG_EMPTY || t == nkey) {                  // claimed (or joined) in this call
+      atomicMin(&P.qowner[base + idx], q);
+      P.st[q] = ST_QNEED;
+      P.qent[q] = idx;
+      P.claimed[q] = 1;
+      return;
+    }
     idx = (idx + 1) & P.qmask;
   }
-  // table full: only possible once the session's handles are exhausted (tables
-  // hold >= 2 x capacity entries), so this is a capacity failure
+  // table full: tables hold >= cap + B_max keys, so this needs exhausted handles
   P.st[q] = ST_INVALID;
   latch(P.sticky, RNNLM_E_CAPACITY);
 }
 
-// ---- (a2) claim -------------------------------------------------------------
-__global__ void k_qclaim(Params P, CallArgs A) {
-  pdl_entry();
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= A.n || P.st[q] != ST_QNEED || P.counts[2] == A.epoch) return;
-  const uint32_t s = A.session[q];
-  const unsigned long long key = ((unsigned long long)A.parent[q] << 32) | A.word[q];
-  const size_t base = (size_t)s * (P.qmask + 1);
-  uint32_t idx = P.qent[q];                 // slots before the hint hold other keys
-  uint32_t probes = 0;
-  for (;; ++probes) {
-    if (probes > P.qmask) {                 // table full -> capacity failure
-      P.st[q] = ST_INVALID;
-      latch(P.sticky, RNNLM_E_CAPACITY);
-      return;
-    }
-    unsigned long long t = vload64(&P.qtab[base + idx].tag);
-    if (t == TAG_EMPTY) t = atomicCAS(&P.qtab[base + idx].tag, TAG_EMPTY, key);
-    if (t == TAG_EMPTY || t == key) break;
-    idx = (idx + 1) & P.qmask;
-  }
-  atomicMin(&P.qowner[base + idx], q);
-  P.qent[q] = idx;
-}
-
-// ---- (a3) probe ------------------------------------------------------------
-__global__ void k_hprobe(Params P, CallArgs A) {
+// ---- (a3) hidden-state cache: owner resolution + probe + claim -----------------
+__global__ void k_hcache(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= A.n || P.st[q] != ST_QNEED || P.counts[2] == A.epoch) return;
@@ -146,50 +133,32 @@ __global__ void k_hprobe(Params P, CallArgs A) {
   const uint32_t ps = P.rec[cb + p].slot;
   P.pslot[q] = ps;
   const unsigned long long hh = P.codehash[cb + ps];
+  const unsigned long long mine = (((unsigned long long)ps << 32) | w) | NEW_BIT;
   const size_t base = (size_t)s * (P.hmask + 1);
   uint32_t idx = hhome(hh, w, P.hmask);
   for (uint32_t probes = 0; probes <= P.hmask; ++probes) {
-    const unsigned long long t = P.htab[base + idx].tag;
-    if (t == TAG_EMPTY) { P.st[q] = ST_HNEED; P.hent[q] = idx; return; }
-    if (hkey_match(P, t, s, w, ps, hh)) {
-      P.st[q] = ST_SHIT_OLD;
-      P.hent[q] = idx;
-      P.cslot[q] = P.htab[base + idx].slot;
-      return;
-    }
-    idx = (idx + 1) & P.hmask;
-  }
-  P.st[q] = ST_INVALID;                     // table full -> capacity failure
-  latch(P.sticky, RNNLM_E_CAPACITY);
-}
-
-// ---- (a3) claim ------------------------------------------------------------
-__global__ void k_hclaim(Params P, CallArgs A) {
-  pdl_entry();
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= A.n || P.st[q] != ST_HNEED || P.counts[2] == A.epoch) return;
-  const uint32_t s = A.session[q], w = A.word[q];
-  const uint32_t ps = P.pslot[q];
-  const unsigned long long hh = P.codehash[(size_t)s * P.cap + ps];
-  const unsigned long long mine = ((unsigned long long)ps << 32) | w;
-  const size_t base = (size_t)s * (P.hmask + 1);
-  uint32_t idx = P.hent[q];
-  for (uint32_t probes = 0;; ++probes) {
-    if (probes > P.hmask) {                 // table full -> capacity failure
-      P.st[q] = ST_INVALID;
-      latch(P.sticky, RNNLM_E_CAPACITY);
-      return;
-    }
     unsigned long long t = vload64(&P.htab[base + idx].tag);
     if (t == TAG_EMPTY) {
       t = atomicCAS(&P.htab[base + idx].tag, TAG_EMPTY, mine);
-      if (t == TAG_EMPTY) break;
+      if (t == TAG_EMPTY) t = mine;                     // inserted: falls into the claim below
     }
-    if (hkey_match(P, t, s, w, ps, hh)) break;
+    if (hkey_match(P, t & ~NEW_BIT, s, w, ps, hh)) {
+      if (!(t & NEW_BIT)) {                             // cached by an earlier call
+        P.st[q] = ST_SHIT_OLD;
+        P.hent[q] = idx;
+        P.cslot[q] = P.htab[base + idx].slot;
+        return;
+      }
+      atomicMin(&P.howner[base + idx], q);
+      P.st[q] = ST_HNEED;
+      P.hent[q] = idx;
+      P.claimed[q] |= 2;
+      return;
+    }
     idx = (idx + 1) & P.hmask;
   }
-  atomicMin(&P.howner[base + idx], q);
-  P.hent[q] = idx;
+  P.st[q] = ST_INVALID;                                 // table full -> capacity failure
+  latch(P.sticky, RNNLM_E_CAPACITY);
 }
 
 // ---- (a4) decoupled look-back scan over (non-QHIT, MISS) ------------------
@@ -248,30 +217,44 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
   }
   if (lane == 31) s_warp[wid] = inc;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long run = 0;
-    for (int i = 0; i < SCAN_THREADS / 32; ++i) {
-      const unsigned long long t = s_warp[i];
-      s_warp[i] = run;
-      run += t;
-    }
-    const unsigned long long agg = run;
+  if (wid == 0) {
+    // block aggregate (every lane of warp 0 computes it)
+    unsigned long long agg = 0;
+    for (int i = 0; i < SCAN_THREADS / 32; ++i) agg += s_warp[i];
     unsigned long long excl = 0;
     if (tile == 0) {
-      atomicExch(&P.tile_status[0], to_status(agg, ST_INC));
+      if (lane == 0) atomicExch(&P.tile_status[0], to_status(agg, ST_INC));
     } else {
-      atomicExch(&P.tile_status[tile], to_status(agg, ST_AGG));
+      if (lane == 0) atomicExch(&P.tile_status[tile], to_status(agg, ST_AGG));
+      // warp-parallel look-back over 32 predecessors at a time: lane l reads
+      // tile (j - l); the nearest inclusive prefix ends the walk
       int j = (int)tile - 1;
       for (;;) {
-        unsigned long long x;
-        do { x = vload64(&P.tile_status[j]); } while ((x >> 62) == 0);
-        excl += from_status(x);
-        if ((x >> 62) == 2) break;
-        --j;
+        const int idx = j - lane;
+        unsigned long long x = idx >= 0 ? vload64(&P.tile_status[idx]) : to_status(0ull, ST_INC);
+        while (__any_sync(0xffffffffu, (x >> 62) == 0)) {
+          if ((x >> 62) == 0) x = vload64(&P.tile_status[idx]);
+        }
+        const uint32_t incm = __ballot_sync(0xffffffffu, (x >> 62) == 2);
+        const int stop = incm ? __ffs(incm) - 1 : 31;
+        unsigned long long part = lane <= stop ? from_status(x) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (incm) break;
+        j -= 32;
       }
-      atomicExch(&P.tile_status[tile], to_status(excl + agg, ST_INC));
+      if (lane == 0) atomicExch(&P.tile_status[tile], to_status(excl + agg, ST_INC));
     }
-    s_prefix = excl;
+    if (lane == 0) {
+      unsigned long long run = 0;
+      for (int i = 0; i < SCAN_THREADS / 32; ++i) {
+        const unsigned long long t = s_warp[i];
+        s_warp[i] = run;
+        run += t;
+      }
+      s_prefix = excl;
+    }
   }
   __syncthreads();
   unsigned long long run = s_prefix + s_warp[wid] + (inc - tsum);
@@ -309,6 +292,23 @@ __global__ void k_commit(Params P, CallArgs A) {
   if (!bad && s < P.S && (q == A.n - 1 || A.session[q + 1] != s)) {   // last of the session
     P.seg_cnt_nonq[s] = P.excl_nonq[q] + (nonq ? 1u : 0u) - P.seg_excl_nonq[s];
     P.seg_cnt_miss[s] = P.excl_miss[q] + (miss ? 1u : 0u) - P.seg_excl_miss[s];
+  }
+  // entries this query claimed AND owns: clear NEW_BIT (good batch) or remove
+  // them again (rejected batch: every entry of this call goes, chains return
+  // to their state before the call)
+  const uint8_t cl = P.claimed[q];
+  if (cl) {
+    const size_t qb0 = (size_t)s * (P.qmask + 1), hb0 = (size_t)s * (P.hmask + 1);
+    if ((cl & 1) && P.qowner[qb0 + P.qent[q]] == q) {
+      QEntry *e = &P.qtab[qb0 + P.qent[q]];
+      if (bad) { e->tag = TAG_EMPTY; P.qowner[qb0 + P.qent[q]] = NONE; }
+      else e->tag &= ~NEW_BIT;
+    }
+    if ((cl & 2) && P.howner[hb0 + P.hent[q]] == q) {
+      HEntry *e = &P.htab[hb0 + P.hent[q]];
+      if (bad) { e->tag = TAG_EMPTY; P.howner[hb0 + P.hent[q]] = NONE; }
+      else e->tag &= ~NEW_BIT;
+    }
   }
   if (!nonq) return;
   const uint32_t w = A.word[q], p = A.parent[q];
@@ -472,12 +472,8 @@ static inline uint32_t nblk(uint32_t n, uint32_t t) { return (n + t - 1) / t; }
 int launch_cache_front(const Params &P, const CallArgs &A, cudaStream_t s) {
   const uint32_t ntiles = nblk(A.n, SCAN_TILE);
   int k = 0;
-  launch_pdl(k_qprobe, nblk(A.n, 256), 256, 0, s, P, A, ntiles); ++k;
-  if (P.cache) {
-    launch_pdl(k_qclaim, nblk(A.n, 256), 256, 0, s, P, A); ++k;
-    launch_pdl(k_hprobe, nblk(A.n, 256), 256, 0, s, P, A); ++k;
-    launch_pdl(k_hclaim, nblk(A.n, 256), 256, 0, s, P, A); ++k;
-  }
+  launch_pdl(k_qcache, nblk(A.n, 256), 256, 0, s, P, A, ntiles); ++k;
+  if (P.cache) { launch_pdl(k_hcache, nblk(A.n, 256), 256, 0, s, P, A); ++k; }
   launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, P, A); ++k;
   return k;
 }

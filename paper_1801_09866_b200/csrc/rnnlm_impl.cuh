@@ -17,6 +17,7 @@ constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr int MAX_CTX = 7;            // maxent_order <= 8
 
 // LM-query cache entry (a2): key (parent handle << 32 | word), value (score, child).
+// Bit 31 of the word field marks an entry inserted by the running call (so V < 2^31).
 struct __align__(16) QEntry {
   unsigned long long tag;
   float score;
@@ -92,6 +93,7 @@ struct Params {
   uint32_t *st, *qent, *aux, *hent, *pslot, *cslot, *excl_nonq, *excl_miss;
   uint32_t *nonq_list;
   uint32_t *dup_list;             // QHIT_NEW queries of this call (count in counts[3])
+  uint8_t *claimed;               // bit 0: claimed a query-cache entry, bit 1: a hidden-cache entry
   uint32_t *row_src, *row_dst, *row_word;   // GRU rows: global state rows + word
   uint32_t *seg_excl_nonq, *seg_excl_miss, *seg_cnt_nonq, *seg_cnt_miss;  // per session
   unsigned long long *tile_status;
