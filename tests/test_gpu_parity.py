@@ -277,3 +277,37 @@ def test_multisession_bf16_sample():
     wl = generate_workload(4, 3, 2048, d.V, seed=7)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16)
     replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+
+
+def test_per_query_calls_equal_per_frame_batches():
+    """Frame-wise batching changes nothing in the results: one call
+    per query returns bitwise the same scores, handles and states."""
+    d, m = forgetful_model()
+    wl = generate_workload(2, 12, 24, d.V, seed=31, dur=(2, 6))
+    outs = []
+    for per_query in (False, True):
+        eng = RNNLM.from_dims(d, m, key_mode=KEY_SIGN, num_sessions=2, max_queries_per_call=64,
+                              max_histories_per_session=wl.max_histories_hint())
+        child = np.zeros(wl.n_total, np.uint32)
+        score = np.zeros(wl.n_total, np.float32)
+        for t in range(wl.frames):
+            sl = wl.frame_slice(t)
+            par = O.resolve_parents(wl.parent_ref[sl], child)
+            if per_query:
+                for i in range(sl.start, sl.stop):
+                    j = i - sl.start
+                    sc, ch, _ = eng.query_batch(_dev(wl.session[i:i + 1]), _dev(par[j:j + 1]),
+                                                _dev(wl.word[i:i + 1]))
+                    child[i] = ch.cpu().numpy().view(np.uint32)[0]
+                    score[i] = sc.cpu().numpy()[0]
+            else:
+                sc, ch, _ = eng.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]))
+                child[sl] = ch.cpu().numpy().view(np.uint32)
+                score[sl] = sc.cpu().numpy()
+        states = [eng.read_states(s, child[wl.session == s]).cpu().numpy() for s in range(2)]
+        outs.append((score, child, states, eng.cache_stats()))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1], outs[1][1])
+    for a, b in zip(outs[0][2], outs[1][2]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert outs[0][3]["gru_computations"] == outs[1][3]["gru_computations"]
