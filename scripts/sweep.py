@@ -70,9 +70,10 @@ def run(dims, model, wl, key, math, warm=5, timed_from=None):
 
 
 def sweep(a):
-    dims = model_dims("large")
+    cfg = a.config
+    dims = model_dims(cfg)
     model = generate_model(dims, seed=1234)
-    wl = generate_workload(a.sessions, a.frames, CONFIGS["large"]["B_s"], dims.V, seed=7)
+    wl = generate_workload(a.sessions, a.frames, CONFIGS[cfg]["B_s"], dims.V, seed=7)
     ref_st, _, ref_sc, ref_ch = run(dims, model, wl, "off", R.MATH_FP32)
     base = None
     for key in ("off", "round:3", "round:2", "round:1", "sign"):
@@ -82,7 +83,7 @@ def sweep(a):
         if base is None:
             base = st["gru_computations"]
         print(json.dumps({
-            "sweep": "compression", "mode": key, "math": "bf16", "sessions": wl.S,
+            "sweep": "compression", "config": cfg, "mode": key, "math": "bf16", "sessions": wl.S,
             "frames": wl.frames, "queries": st["total_queries"],
             "query_cache_hit_rate": st["query_hits"] / st["total_queries"],
             "hidden_cache_hit_rate": st["hidden_hits"] / max(1, st["hidden_lookups"]),
@@ -139,9 +140,11 @@ def main():
     ap.add_argument("--what", default="sweep", choices=["sweep", "ablation"])
     ap.add_argument("--sessions", type=int, default=16)
     ap.add_argument("--frames", type=int, default=120)
-    ap.add_argument("--config", default="moderate")
+    ap.add_argument("--config", default=None, help="sweep: large (default); ablation: moderate")
     ap.add_argument("--math", default="bf16")
     a = ap.parse_args()
+    if a.config is None:
+        a.config = "large" if a.what == "sweep" else "moderate"
     (sweep if a.what == "sweep" else ablation)(a)
 
 
