@@ -871,6 +871,171 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// =============================================================== multicast variant
+// Cluster of 2 CTAs on two M-tiles with the SAME weight tile: each CTA runs its
+// own one-CTA MMAs (M = 128, N = 256) but TMA-loads only half of the B chunk
+// and multicasts it into both CTAs' shared memory, so each SM pulls 32 KB per
+// K-chunk from L2 instead of 48 KB.  A stage is refilled only after both CTAs'
+// MMAs released it (commit multicast to both empty barriers).
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap *map, uint64_t *bar,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)), "h"((uint16_t)3)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gru_tc_mc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1h,
+                const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2h,
+                TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem m = carve(smem_raw);                      // 4 stages x (16 KB A + 32 KB B)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t n1 = a.nub, n2 = a.H / BN;
+  const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
+  const uint32_t target = n1 * 2 * EPI_WARPS;           // phase-1 arrivals per 256-row pair tile
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) { mbar_init(&m.full[s], 1); mbar_init(&m.empty[s], 2); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&m.tfull[s], 1); mbar_init(&m.tempty[s], EPI_WARPS); }
+    for (int s = 0; s < TQ; ++s) { mbar_init(&m.qfull[s], 1); mbar_init(&m.qempty[s], 2 * (2 + EPI_WARPS)); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&map_a1); prefetch_map(&map_w1h); prefetch_map(&map_rh); prefetch_map(&map_w2h);
+  }
+  if (warp == 1) tmem_alloc(m.tmem_base, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();
+  pdl_entry();
+  const uint32_t Q = a.counts[1];
+  const uint32_t mt = (Q + 2 * BM - 1) / (2 * BM);
+  const uint32_t L = mt < a.lag / 2 ? mt : a.lag / 2;
+  const uint32_t ntiles = mt * (n1 + n2);
+  const uint32_t tmem_base = *m.tmem_base;
+  const uint32_t qempty0 = mapa(smem_u32(&m.qempty[0]), 0);
+  auto take = [&](uint32_t it, bool release) -> uint32_t {
+    const uint32_t slot = it % TQ;
+    mbar_wait_cl(&m.qfull[slot], (it / TQ) & 1);
+    const uint32_t t = *reinterpret_cast<volatile uint32_t *>(&m.tile_q[slot]);
+    __syncwarp(__activemask());
+    if (release) mbar_arrive_cl(qempty0 + slot * 8);
+    return t;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t it = 0;; ++it) {
+        uint32_t t;
+        if (leader) {
+          const uint32_t slot = it % TQ;
+          mbar_wait_cl(&m.qempty[slot], ((it / TQ) & 1) ^ 1);
+          t = atomicAdd(a.tile_ctr, 1u);
+          if (t >= ntiles) t = NO_TILE;
+          m.tile_q[slot] = t;
+          st_cl_u32(mapa(smem_u32(&m.tile_q[slot]), 1), t);
+          mbar_arrive(&m.qfull[slot]);
+          mbar_arrive_cl(mapa(smem_u32(&m.qfull[slot]), 1));
+          mbar_arrive_cl(qempty0 + slot * 8);
+        } else {
+          t = take(it, true);
+        }
+        if (t == NO_TILE) break;
+        const Tile x = tile_of(t, mt, n1, n2, L);
+        const uint32_t m0 = x.m * 2 * BM + rank * BM;
+        const uint32_t b0row = x.j * BN + rank * (BN / 2);
+        if (x.kind == 1) {
+          wait_phase1(a.done1 + x.m, target);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        for (uint32_t kc = 0; kc < KC; ++kc) {
+          mbar_wait(&m.empty[stage], phase ^ 1);
+          mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
+          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES);
+          const uint32_t dB = smem_u32(m.sB + stage * B_BYTES) + rank * BP_BYTES;
+          const CUtensorMap *mb = x.kind == 0 ? &map_w1h : &map_w2h;
+          if (x.kind == 1 && kc >= kx) tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BK), (int)m0);
+          else tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
+          tma_load_2d_mc(dB, mb, &m.full[stage], (int)(kc * BK), (int)b0row, (uint16_t)3);
+          if (++stage == ST) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    uint32_t stage = 0, phase = 0;
+    const uint32_t id = idesc_bf16(BM, BN);
+    for (uint32_t it = 0;; ++it) {
+      if (take(it, lane == 0) == NO_TILE) break;
+      const uint32_t acc = it & 1;
+      mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t tm = tmem_base + acc * BN;
+      for (uint32_t kc = 0; kc < KC; ++kc) {
+        mbar_wait(&m.full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+          umma_commit_mc(&m.empty[stage]);
+          if (kc == KC - 1) umma_commit(&m.tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == ST) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r_in = q * 32 + lane;
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t t = take(it, lane == 0);
+      if (t == NO_TILE) break;
+      const Tile x = tile_of(t, mt, n1, n2, L);
+      const uint32_t acc = it & 1;
+      mbar_wait(&m.tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t row = x.m * 2 * BM + rank * BM + r_in;
+      const bool valid = row < Q;
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
+      if (x.kind == 0) {
+        epi_phase1(a, tbase, row, valid, half, x.j);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&m.tempty[acc]);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(a.done1 + x.m, 1u);
+        }
+      } else {
+        wait_phase1(a.done1 + x.m, target);
+        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&m.tempty[acc]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
 constexpr size_t SMEM_PAIR = 1024 + STP * (A_BYTES + BP_BYTES) + 256;
 
 constexpr size_t SMEM = 1024 + ST * (A_BYTES + B_BYTES) + 256;
@@ -885,7 +1050,7 @@ struct TcState {
   uint32_t E = 0, H = 0, nub = 0, bmax = 0;
   __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr, *a1 = nullptr;
   uint32_t *done1 = nullptr;
-  bool pair = false;               // CTA-pair (cta_group::2) kernel (experimental): RNNLM_TC_PAIR=1
+  int pair = 0;                    // 0: one-CTA kernel; 1: cta_group::2 pair; 2: B multicast in a cluster of 2 (RNNLM_TC_PAIR)
   float *bzr = nullptr, *bh = nullptr;
   CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h;
   bool bound = false;
@@ -929,7 +1094,7 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_
   *state_out = nullptr;
   TcState *t = new TcState;
   t->E = E; t->H = H; t->nub = H / UB;
-  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = atoi(e) != 0;
+  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = atoi(e);
   const size_t K1 = E + H;
   std::vector<__nv_bfloat16> w1((size_t)2 * H * K1), w2((size_t)H * K1);
   std::vector<float> bzr((size_t)2 * H), bh(H);
@@ -963,6 +1128,7 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_
        make_map(&t->map_w2h, t->w2, K1, H, BN / 2);
   ok = ok && cudaFuncSetAttribute(k_gru_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PAIR) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   *state_out = t;
   if (!ok) {
     (void)cudaGetLastError();
@@ -1024,8 +1190,12 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / BN) * 2;
     const uint32_t cap = (uint32_t)num_sms & ~1u;
     if (gp > cap) gp = cap;
-    launch_pdl_cluster(k_gru_tc2, gp, THREADS, SMEM_PAIR, s, 2, t->map_a1, t->map_w1h, t->map_rh,
-                       t->map_w2h, a);
+    if (t->pair == 1)
+      launch_pdl_cluster(k_gru_tc2, gp, THREADS, SMEM_PAIR, s, 2, t->map_a1, t->map_w1h, t->map_rh,
+                         t->map_w2h, a);
+    else
+      launch_pdl_cluster(k_gru_tc_mc, gp, THREADS, SMEM, s, 2, t->map_a1, t->map_w1h, t->map_rh,
+                         t->map_w2h, a);
   } else {
     launch_pdl(k_gru_tc, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
   }
