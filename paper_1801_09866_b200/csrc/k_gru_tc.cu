@@ -180,6 +180,7 @@ struct TcArgs {
   uint32_t *done1;                 // per M-tile phase-1 epilogue arrivals (zeroed by the gather)
   uint32_t *tile_ctr;              // dynamic tile scheduler (zeroed by the gather)
   uint32_t lag;                    // phase-2 tiles trail phase-1 tiles by this many M-tiles
+  uint32_t diag;                   // timing diagnostics only (results invalid): 1 no MMA, 2 no TMA
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
   float round_scale;
@@ -319,7 +320,8 @@ __device__ __forceinline__ uint32_t next_tile(const Smem &m, uint32_t it, bool r
 }
 
 // MMA issuer: KC chunks of 4 x (M=128, N=256, K=16) per tile, both phases.
-__device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, int lane) {
+__device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, int lane,
+                                         uint32_t diag) {
   uint32_t stage = 0, phase = 0;
   const uint32_t id = idesc_bf16(BM, BN);
   for (uint32_t it = 0;; ++it) {
@@ -334,8 +336,9 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
       if (lane == 0) {
         const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+        if (diag != 1)
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
         umma_commit(&m.empty[stage]);
         if (kc == KC - 1) umma_commit(&m.tfull[acc]);
       }
@@ -557,6 +560,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (uint32_t kc = 0; kc < KC; ++kc) {
           mbar_wait(&m.empty[stage], phase ^ 1);
+          if (a.diag == 2) {
+            mbar_arrive(&m.full[stage]);
+            if (++stage == ST) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
           const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * B_BYTES);
           if (x.kind == 0) {
@@ -572,7 +580,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    mma_loop(m, tmem_base, KC, lane);
+    mma_loop(m, tmem_base, KC, lane, a.diag);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -777,6 +785,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (uint32_t kc = 0; kc < KC; ++kc) {
           mbar_wait(&m.empty[stage], phase ^ 1);
+          if (a.diag == 2) {
+            if (leader) mbar_arrive(&m.full[stage]);
+            else mbar_arrive_cl(full0 + stage * 8);
+            if (++stage == STP) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (leader) mbar_expect_tx(&m.full[stage], 2 * (A_BYTES + BP_BYTES));
           else mbar_arrive_cl(full0 + stage * 8);
           const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
@@ -815,7 +829,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              umma_bf16_pair(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+              if (a.diag != 1) umma_bf16_pair(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
             umma_commit_pair(&m.empty[stage]);
             if (kc == KC - 1) umma_commit_pair(&m.tfull[acc]);
           }
@@ -1051,6 +1065,7 @@ struct TcState {
   __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr, *a1 = nullptr;
   uint32_t *done1 = nullptr;
   int pair = 0;                    // 0: one-CTA kernel; 1: cta_group::2 pair; 2: B multicast in a cluster of 2 (RNNLM_TC_PAIR)
+  uint32_t diag = 0;               // RNNLM_TC_DIAG: timing diagnostics, results invalid (1 no MMA, 2 no TMA)
   float *bzr = nullptr, *bh = nullptr;
   CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h;
   bool bound = false;
@@ -1095,6 +1110,7 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_
   TcState *t = new TcState;
   t->E = E; t->H = H; t->nub = H / UB;
   if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = atoi(e);
+  if (const char *e = getenv("RNNLM_TC_DIAG")) t->diag = (uint32_t)atoi(e);
   const size_t K1 = E + H;
   std::vector<__nv_bfloat16> w1((size_t)2 * H * K1), w2((size_t)H * K1);
   std::vector<float> bzr((size_t)2 * H), bh(H);
@@ -1179,6 +1195,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.done1 = t->done1;
   a.tile_ctr = t->done1 + (t->bmax / BM + 2);
   a.lag = 48;
+  a.diag = t->diag;
   const uint32_t mt = (max_rows + BM - 1) / BM;
   uint32_t g1 = mt * (t->nub + P.H / BN);
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
