@@ -38,6 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-I" + os.path.join(ROOT, "include"), "-o", SO + ".tmp", *sources()]
+    # experiment knobs (e.g. -DRNNLM_TC_ST=3); the default build passes none
+    cmd[1:1] = os.environ.get("RNNLM_NVCC_FLAGS", "").split()
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

@@ -47,7 +47,10 @@ constexpr int BM = 128;          // UMMA M (rows per tile)
 constexpr int BK = 64;           // K elements per smem stage (= one 128-byte swizzle atom)
 constexpr int UB = 128;          // units per phase-1 block
 constexpr int BN = 256;          // UMMA N of both phases (phase 1: z|r of 128 units; phase 2: 256 units)
-constexpr int ST = 4;            // smem pipeline stages
+#ifndef RNNLM_TC_ST
+#define RNNLM_TC_ST 4
+#endif
+constexpr int ST = RNNLM_TC_ST;  // smem pipeline stages
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES = BN * BK * 2;          // 32 KB
 constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 columns
@@ -786,22 +789,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (uint32_t kc = 0; kc < KC; ++kc) {
           mbar_wait(&m.empty[stage], phase ^ 1);
           if (a.diag == 2) {
-            if (leader) mbar_arrive(&m.full[stage]);
-            else mbar_arrive_cl(full0 + stage * 8);
+            mbar_arrive(&m.full[stage]);
             if (++stage == STP) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (leader) mbar_expect_tx(&m.full[stage], 2 * (A_BYTES + BP_BYTES));
-          else mbar_arrive_cl(full0 + stage * 8);
+          // each CTA's TMA signals its own full barrier; the peer's landing is
+          // forwarded to the leader by the peer's warp 1
+          uint64_t *fb = &m.full[stage];
+          mbar_expect_tx(fb, A_BYTES + BP_BYTES);
           const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
-          const uint32_t fb = full0 + stage * 8;
           if (x.kind == 0) {
-            tma_load_2d_pair(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
-            tma_load_2d_pair(dB, &map_w1h, fb, (int)(kc * BK), (int)b0row);
+            tma_load_2d(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
+            tma_load_2d(dB, &map_w1h, fb, (int)(kc * BK), (int)b0row);
           } else {
-            if (kc < kx) tma_load_2d_pair(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
-            else tma_load_2d_pair(dA, &map_rh, fb, (int)((kc - kx) * BK), (int)m0);
-            tma_load_2d_pair(dB, &map_w2h, fb, (int)(kc * BK), (int)b0row);
+            if (kc < kx) tma_load_2d(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
+            else tma_load_2d(dA, &map_rh, fb, (int)((kc - kx) * BK), (int)m0);
+            tma_load_2d(dB, &map_w2h, fb, (int)(kc * BK), (int)b0row);
           }
           if (++stage == STP) { stage = 0; phase ^= 1; }
         }
@@ -823,7 +826,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         const uint32_t tm = tmem_base + acc * BN;
         for (uint32_t kc = 0; kc < KC; ++kc) {
-          mbar_wait(&m.full[stage], phase);
+          mbar_wait_cl(&m.full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
@@ -838,9 +841,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     } else {
-      // the peer's MMA warp only consumes ring slots (keeps the qempty count uniform)
-      for (uint32_t it = 0;; ++it)
+      // the peer's warp 1 forwards "this CTA's half of the stage has landed"
+      // to the leader's full barrier (second arrival), tile by tile
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t it = 0;; ++it) {
         if (take(it, lane == 0) == NO_TILE) break;
+        for (uint32_t kc = 0; kc < KC; ++kc) {
+          mbar_wait(&m.full[stage], phase);
+          if (lane == 0) mbar_arrive_cl(full0 + stage * 8);
+          __syncwarp();
+          if (++stage == STP) { stage = 0; phase ^= 1; }
+        }
+      }
     }
   } else {
     const int q = warp & 3;
