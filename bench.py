@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--workload", default="multi", choices=list(CONFIGS))
     ap.add_argument("--sessions", type=int, default=None, help="sessions per rank (default: config)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--math", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--math", default="bf16", choices=["bf16", "tf32", "fp32"])
     ap.add_argument("--key", default="sign", help="off | sign | round:K")
     ap.add_argument("--no-cache", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -223,7 +223,7 @@ def run_ours(args):
     wl = generate_workload(S, frames, B_s, V_draw, seed=7 + rank * S,
                            zipf_s=0.0 if args.uniform_words else 1.0)
     mode, k = key_mode(args.key)
-    math = R.MATH_BF16 if args.math == "bf16" else R.MATH_FP32
+    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32}[args.math]
     n = wl.n_per_frame
     cap = wl.max_histories_hint()
     eng = R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math,
@@ -318,6 +318,10 @@ def run_ours(args):
     if math == R.MATH_BF16:
         peak = peaks.get("bf16_tflops_sustained", 1400.0)
         bound, peak_src = "tensor", ("measured bf16_tflops_sustained" if peaks else "fallback")
+    elif math == R.MATH_TF32:
+        # no measured TF32 peak: the measured bf16 peak x the nominal dense ratio (1.125 / 2.25 PF)
+        peak = 0.5 * peaks.get("bf16_tflops_sustained", 1400.0)
+        bound, peak_src = "tensor", "measured bf16_tflops_sustained x 0.5 (nominal tf32/bf16 dense ratio)"
     else:
         sm_max = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # FP32 FFMA lanes x 2 flop x clock
@@ -333,7 +337,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None,
-        "dtype": "bf16" if math == R.MATH_BF16 else "f32", "data": "synthetic",
+        "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32": "f32"}[args.math], "data": "synthetic",
         "config": {"workload": args.workload, "sessions_per_gpu": S, "queries_per_session_frame": B_s,
                    "queries_per_step": total_queries // args.steps, "V": dims.V, "E": dims.E,
                    "H": dims.H, "maxent": f"2^{dims.maxent_log2} {dims.N}-gram", "key": args.key,

@@ -81,8 +81,12 @@ typedef enum {
 /* Arithmetic of the GRU gate contraction (a5).  States are always fp32. */
 typedef enum {
   RNNLM_MATH_FP32 = 0,      /* FP32 FFMA (SIMT) */
-  RNNLM_MATH_TF32 = 1,      /* reserved (rnnlm_create returns RNNLM_E_INVALID_ARG in ABI v1) */
+  RNNLM_MATH_TF32 = 1,      /* fp32 operands read as TF32, fp32 accumulation on tcgen05 tensor cores */
   RNNLM_MATH_BF16 = 2       /* bf16 operands, fp32 accumulation on tcgen05 tensor cores */
+  /* The two tensor-core modes need E % 64 == 0 and H % 256 == 0 (else
+   * rnnlm_create returns RNNLM_E_DIMENSION).  BF16 stores bf16 copies of E
+   * and the gate weights (and of nce_w when every entry is bf16-exact); TF32
+   * keeps every parameter fp32. */
 } rnnlm_math;
 
 typedef enum { RNNLM_QHIT = 0, RNNLM_SHIT = 1, RNNLM_MISS = 2, RNNLM_INVALID = 255 } rnnlm_outcome;
@@ -123,11 +127,11 @@ typedef struct {
   double ms_cache;      /* key/probe/claim/scan/commit kernels (a1-a4) */
   double ms_score;      /* NCE + MaxEnt scoring (a6), side stream */
   double ms_gru;        /* gather + gate contraction + gates, both phases (a5) */
-  double ms_encode;     /* code + code hash of new states (a1; FP32 path only) */
+  double ms_encode;     /* code + code hash of new states (a1; FP32 SIMT path only) */
   double ms_final;      /* result write + counters (a7), side stream */
   uint64_t calls;       /* timed query_batch calls */
   uint64_t launches;    /* kernels launched by those calls */
-  /* timing level 2, BF16 path only: split of ms_gru (gather, fused GEMM) */
+  /* timing level 2, tensor-core paths only: split of ms_gru (gather, fused GEMM) */
   double ms_gru_gather, ms_gru_phase1, ms_gru_phase2;
 } rnnlm_timing;
 

@@ -15,9 +15,9 @@ namespace rnnlm_host {
 // Tensor-core path (k_gru_tc.cu).  Returns kernels launched, or -1 if the
 // configuration is not supported by it.
 int gru_tc_supported(uint32_t E, uint32_t H);
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_out);
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, void **state_out);
 void gru_tc_release(void *state);
-int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax);
+int gru_tc_bind(void *state, void *rh, uint32_t bmax);
 int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s,
                   cudaEvent_t ev_gathered, cudaEvent_t ev_phase1);
 }  // namespace rnnlm_host
@@ -172,8 +172,9 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   if (c.key_mode > RNNLM_KEY_SIGN) return RNNLM_E_INVALID_ARG;
   if (c.key_mode == RNNLM_KEY_ROUND && (c.round_digits < 1 || c.round_digits > 4))
     return RNNLM_E_INVALID_ARG;
-  if (c.math != RNNLM_MATH_FP32 && c.math != RNNLM_MATH_BF16) return RNNLM_E_INVALID_ARG;
-  if (c.math == RNNLM_MATH_BF16 && !rnnlm_host::gru_tc_supported(c.embed, c.hidden))
+  if (c.math > RNNLM_MATH_BF16) return RNNLM_E_INVALID_ARG;
+  const bool tc = c.math != RNNLM_MATH_FP32;           // tcgen05 path (BF16 or TF32 operands)
+  if (tc && !rnnlm_host::gru_tc_supported(c.embed, c.hidden))
     return RNNLM_E_DIMENSION;
   const size_t V = c.vocab, E = c.embed, H = c.hidden, M = (size_t)1 << c.maxent_log2;
   const float *arrs[] = {w->emb, w->Wz, w->Uz, w->bz, w->Wr, w->Ur, w->br,
@@ -244,8 +245,10 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
     chk(upload(h, const_cast<float **>(&P.b1), b1.data(), b1.size()));
     chk(upload(h, const_cast<float **>(&P.w2), w2.data(), w2.size()));
   } else {
-    chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.emb16), w->emb, V * E));
-    if (st == RNNLM_OK && rnnlm_host::gru_tc_prepare(w, c.embed, c.hidden, &h->tc) != 0)
+    if (c.math == RNNLM_MATH_BF16)
+      chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.emb16), w->emb, V * E));
+    if (st == RNNLM_OK &&
+        rnnlm_host::gru_tc_prepare(w, c.embed, c.hidden, c.math == RNNLM_MATH_TF32, &h->tc) != 0)
       st = RNNLM_E_OOM;
   }
   // ---- pools
@@ -272,13 +275,12 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   chk(dalloc(h, &P.tile_ticket, 1));
   chk(dalloc(h, &P.counts, 4));
   chk(dalloc(h, &P.g_z, B * H));
-  if (c.math == RNNLM_MATH_FP32) {
-    chk(dalloc(h, &P.g_wxb, B * H));
-    chk(dalloc(h, &P.g_rh, B * H));
-  } else {
-    chk(dalloc(h, &P.g_rh16, B * H));
-  }
-  if (st == RNNLM_OK && c.math == RNNLM_MATH_BF16 && rnnlm_host::gru_tc_bind(h->tc, P.g_rh16, (uint32_t)B) != 0)
+  if (c.math == RNNLM_MATH_FP32) chk(dalloc(h, &P.g_wxb, B * H));
+  if (c.math == RNNLM_MATH_BF16) chk(dalloc(h, &P.g_rh16, B * H));
+  else chk(dalloc(h, &P.g_rh, B * H));
+  if (st == RNNLM_OK && tc &&
+      rnnlm_host::gru_tc_bind(h->tc, c.math == RNNLM_MATH_BF16 ? (void *)P.g_rh16 : (void *)P.g_rh,
+                              (uint32_t)B) != 0)
     st = RNNLM_E_CUDA;
   if (st == RNNLM_OK) {
     // scoring + result write are short; give them priority over the GRU's CTAs
@@ -375,14 +377,14 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
   k += rnnlm_host::launch_dup_scores(P, A, h->num_sms, h->side);
   if (h->timing) cudaEventRecord(ev[3], h->side);
   cudaEventRecord(h->ev_join, h->side);
-  if (P.math == RNNLM_MATH_BF16) {
+  if (P.math != RNNLM_MATH_FP32) {
     k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s, h->timing >= 2 ? ev[4] : nullptr,
                                    nullptr);
   } else {
     k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
   }
   if (h->timing) cudaEventRecord(ev[5], s);
-  if (P.math != RNNLM_MATH_BF16)                      // the tcgen05 epilogue encodes in place
+  if (P.math == RNNLM_MATH_FP32)                      // the tcgen05 epilogue encodes in place
     k += rnnlm_host::launch_encode_rows(P, n, h->num_sms, s);
   if (h->timing) cudaEventRecord(ev[6], s);
   cudaStreamWaitEvent(s, h->ev_join, 0);

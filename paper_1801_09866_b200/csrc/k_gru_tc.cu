@@ -121,6 +121,15 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// Same with fp32 operands read as TF32 (kind::tf32, K = 8 per instruction).
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -150,9 +159,42 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-// Instruction descriptor: kind::f16, A = B = BF16, D = F32, K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor: D = F32, A/B format fmt (kind::f16: BF16 = 1;
+// kind::tf32: TF32 = 2), both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_of(uint32_t fmt, int M, int N) {
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) { return idesc_of(1, M, N); }
+
+// Operand element type of the fused kernel: bf16 (kind::f16) or fp32 read as
+// TF32 (kind::tf32).  A smem stage is one 128-byte swizzle atom of K either
+// way (64 bf16 / 32 fp32 elements), four 32-byte MMA K-steps per stage.
+template <typename T> struct Op;
+template <> struct Op<__nv_bfloat16> {
+  static constexpr int BKE = 64;
+  static constexpr uint32_t FMT = 1;
+  static __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    umma_bf16(d, a, b, id, acc);
+  }
+};
+template <> struct Op<float> {
+  static constexpr int BKE = 32;
+  static constexpr uint32_t FMT = 2;
+  static __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    umma_tf32(d, a, b, id, acc);
+  }
+};
+
+// fp32 -> TF32 (10 explicit mantissa bits), round to nearest, ties away; the
+// result is an fp32 bit pattern with the low 13 bits zero, which the MMA
+// reads exactly (no truncation of the operand inside the tensor core).
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ float4 to_tf32(float4 v) {
+  return make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
 }
 
 __device__ __forceinline__ float sigm(float a) { return __fdividef(1.0f, 1.0f + __expf(-a)); }
@@ -179,7 +221,10 @@ struct TcArgs {
   const uint32_t *row_src, *row_dst, *row_word, *counts;
   float *g_z;                      // [B_max][H]
   __nv_bfloat16 *g_rh16;           // [B_max][H]
-  __nv_bfloat16 *a1;               // [B_max][E+H] gathered phase-1 A operand
+  __nv_bfloat16 *a1;               // [B_max][E+H] gathered phase-1 A operand (bf16 path)
+  const float *emb;                // [V][E] fp32 (TF32 path)
+  float *a1f;                      // [B_max][E+H] gathered phase-1 A operand (TF32 path)
+  float *g_rhf;                    // [B_max][H] r.h, phase-2 A operand (TF32 path)
   uint32_t *done1;                 // per M-tile phase-1 epilogue arrivals (zeroed by the gather)
   uint32_t *tile_ctr;              // dynamic tile scheduler (zeroed by the gather)
   uint32_t lag;                    // phase-2 tiles trail phase-1 tiles by this many M-tiles
@@ -196,6 +241,7 @@ struct TcArgs {
 // dense), one warp per row, 16-byte loads/stores (the paper's per-frame
 // (h || x) block, built in HBM instead of host memory).  States are
 // stored only in fp32; the bf16 operand copy is made here.
+template <typename T>
 __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
   pdl_entry();
   const uint32_t Q = a.counts[1];
@@ -206,17 +252,27 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
     a.done1[i] = 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.tile_ctr = 0u;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Q; r += nw) {
-    const uint4 *x = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)a.row_word[r] * a.E);
-    const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
-    uint4 *dst = reinterpret_cast<uint4 *>(a.a1 + (size_t)r * K1);
-    const uint32_t nx = a.E / 8, nh = a.H / 8;
-    for (uint32_t i = lane; i < nx; i += 32) dst[i] = __ldg(x + i);
-    for (uint32_t i = lane; i < nh; i += 32) {
-      const float4 u = h[2 * i], v = h[2 * i + 1];
-      __nv_bfloat162 b0 = __floats2bfloat162_rn(u.x, u.y), b1 = __floats2bfloat162_rn(u.z, u.w);
-      __nv_bfloat162 b2 = __floats2bfloat162_rn(v.x, v.y), b3 = __floats2bfloat162_rn(v.z, v.w);
-      dst[nx + i] = make_uint4(*reinterpret_cast<uint32_t *>(&b0), *reinterpret_cast<uint32_t *>(&b1),
-                               *reinterpret_cast<uint32_t *>(&b2), *reinterpret_cast<uint32_t *>(&b3));
+    if constexpr (sizeof(T) == 2) {
+      const uint4 *x = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)a.row_word[r] * a.E);
+      const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
+      uint4 *dst = reinterpret_cast<uint4 *>(a.a1 + (size_t)r * K1);
+      const uint32_t nx = a.E / 8, nh = a.H / 8;
+      for (uint32_t i = lane; i < nx; i += 32) dst[i] = __ldg(x + i);
+      for (uint32_t i = lane; i < nh; i += 32) {
+        const float4 u = h[2 * i], v = h[2 * i + 1];
+        __nv_bfloat162 b0 = __floats2bfloat162_rn(u.x, u.y), b1 = __floats2bfloat162_rn(u.z, u.w);
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(v.x, v.y), b3 = __floats2bfloat162_rn(v.z, v.w);
+        dst[nx + i] = make_uint4(*reinterpret_cast<uint32_t *>(&b0), *reinterpret_cast<uint32_t *>(&b1),
+                                 *reinterpret_cast<uint32_t *>(&b2), *reinterpret_cast<uint32_t *>(&b3));
+      }
+    } else {
+      // TF32 operands are the fp32 values themselves (the MMA reads their TF32 part)
+      const float4 *x = reinterpret_cast<const float4 *>(a.emb + (size_t)a.row_word[r] * a.E);
+      const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
+      float4 *dst = reinterpret_cast<float4 *>(a.a1f + (size_t)r * K1);
+      const uint32_t nx = a.E / 4, nh = a.H / 4;
+      for (uint32_t i = lane; i < nx; i += 32) dst[i] = to_tf32(__ldg(x + i));
+      for (uint32_t i = lane; i < nh; i += 32) dst[nx + i] = to_tf32(h[i]);
     }
   }
 }
@@ -322,11 +378,12 @@ __device__ __forceinline__ uint32_t next_tile(const Smem &m, uint32_t it, bool r
   return t;
 }
 
-// MMA issuer: KC chunks of 4 x (M=128, N=256, K=16) per tile, both phases.
+// MMA issuer: KC chunks of 4 x (M=128, N=256, K=32 bytes) per tile, both phases.
+template <typename T>
 __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, int lane,
                                          uint32_t diag) {
   uint32_t stage = 0, phase = 0;
-  const uint32_t id = idesc_bf16(BM, BN);
+  const uint32_t id = idesc_of(Op<T>::FMT, BM, BN);
   for (uint32_t it = 0;; ++it) {
     if (next_tile(m, it, lane == 0) == NO_TILE) break;
     const uint32_t acc = it & 1;
@@ -340,8 +397,8 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
         const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
 #pragma unroll
         if (diag != 1)
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+          for (int k = 0; k < 4; ++k)
+            Op<T>::mma(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
         umma_commit(&m.empty[stage]);
         if (kc == KC - 1) umma_commit(&m.tfull[acc]);
       }
@@ -407,20 +464,40 @@ __device__ __forceinline__ unsigned long long encode16(const TcArgs &a, const fl
 
 
 // Phase-1 epilogue of one thread: row r_in of the tile, the 128 z columns
-// (gate 0) or r columns (gate 1) of unit block ub.
+// (gate 0) or r columns (gate 1) of unit block ub.  The parent state h of
+// r.h is, on the bf16 path, the bf16 copy in the row's A1 row (the value
+// phase 1 multiplied); on the TF32 path the exact fp32 state.
+template <typename T>
 __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid,
                                            int gate, uint32_t ub) {
   const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB;
   const size_t o = (size_t)(valid ? row : 0) * a.H + ub * UB;
-  // bf16 parent state = the recurrent half of the row's gathered A1 row
-  const __nv_bfloat16 *h16 = a.a1 + (size_t)(valid ? row : 0) * (a.E + a.H) + a.E + ub * UB;
+  const size_t ho = (size_t)(valid ? row : 0) * (a.E + a.H) + a.E + ub * UB;
+  const float *hs = nullptr;                         // TF32 path: the exact fp32 parent state
+  if constexpr (sizeof(T) == 4) hs = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * UB;
   auto process = [&](int g, const float *v) {
     float bias16[16];
     ld_bias16(bias + g * 16, bias16);
-    uint4 hb[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-    if (gate == 1 && valid) {
-      hb[0] = *reinterpret_cast<const uint4 *>(h16 + g * 16);
-      hb[1] = *reinterpret_cast<const uint4 *>(h16 + g * 16 + 8);
+    float hv[16];
+    if constexpr (sizeof(T) == 2) {
+      uint4 hb[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      if (gate == 1 && valid) {
+        hb[0] = *reinterpret_cast<const uint4 *>(a.a1 + ho + g * 16);
+        hb[1] = *reinterpret_cast<const uint4 *>(a.a1 + ho + g * 16 + 8);
+      }
+      const uint32_t *hw = reinterpret_cast<const uint32_t *>(hb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        hv[2 * j] = __uint_as_float(hw[j] << 16);
+        hv[2 * j + 1] = __uint_as_float(hw[j] & 0xFFFF0000u);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float4 t4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gate == 1 && valid) t4 = *reinterpret_cast<const float4 *>(hs + g * 16 + 4 * j);
+        hv[4 * j] = t4.x; hv[4 * j + 1] = t4.y; hv[4 * j + 2] = t4.z; hv[4 * j + 3] = t4.w;
+      }
     }
     float sg[16];
 #pragma unroll
@@ -430,19 +507,23 @@ __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint
       float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
 #pragma unroll
       for (int j = 0; j < 4; ++j) gz[j] = make_float4(sg[4 * j], sg[4 * j + 1], sg[4 * j + 2], sg[4 * j + 3]);
-    } else {
-      const uint32_t *hw = reinterpret_cast<const uint32_t *>(hb);
+    } else if constexpr (sizeof(T) == 2) {
       uint4 pk[2];
       uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float h0 = __uint_as_float(hw[j] << 16), h1 = __uint_as_float(hw[j] & 0xFFFF0000u);
-        __nv_bfloat162 t2 = __floats2bfloat162_rn(sg[2 * j] * h0, sg[2 * j + 1] * h1);
+        __nv_bfloat162 t2 = __floats2bfloat162_rn(sg[2 * j] * hv[2 * j], sg[2 * j + 1] * hv[2 * j + 1]);
         pw[j] = *reinterpret_cast<uint32_t *>(&t2);
       }
       uint4 *gr = reinterpret_cast<uint4 *>(a.g_rh16 + o + g * 16);
       gr[0] = pk[0];
       gr[1] = pk[1];
+    } else {
+      float4 *gr = reinterpret_cast<float4 *>(a.g_rhf + o + g * 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        gr[j] = to_tf32(make_float4(sg[4 * j] * hv[4 * j], sg[4 * j + 1] * hv[4 * j + 1],
+                                    sg[4 * j + 2] * hv[4 * j + 2], sg[4 * j + 3] * hv[4 * j + 3]));
     }
   };
   float va[16], vb[16];
@@ -523,6 +604,7 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
 // warp 0: TMA producer (waits on the phase-1 counter before a phase-2 tile);
 // warp 1: TMEM allocation + MMA issue; warps 2-9: epilogue, TMEM lane quarter
 // = warp % 4, column half = (warp - 2) / 4.
+template <typename T>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gru_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1,
              const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2,
@@ -531,7 +613,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const Smem m = carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t n1 = a.nub, n2 = a.H / BN;
-  const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
+  constexpr int BKE = Op<T>::BKE;
+  const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE;
   const uint32_t target = n1 * EPI_WARPS;               // phase-1 arrivals per M-tile
   if (threadIdx.x == 0) {
     prefetch_map(&map_a1); prefetch_map(&map_w1); prefetch_map(&map_rh); prefetch_map(&map_w2);
@@ -571,19 +654,19 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
           const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * B_BYTES);
           if (x.kind == 0) {
-            tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
-            tma_load_2d(dB, &map_w1, &m.full[stage], (int)(kc * BK), (int)(x.j * BN));
+            tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BKE), (int)m0);
+            tma_load_2d(dB, &map_w1, &m.full[stage], (int)(kc * BKE), (int)(x.j * BN));
           } else {
-            if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
-            else tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BK), (int)m0);
-            tma_load_2d(dB, &map_w2, &m.full[stage], (int)(kc * BK), (int)(x.j * BN));
+            if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BKE), (int)m0);
+            else tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BKE), (int)m0);
+            tma_load_2d(dB, &map_w2, &m.full[stage], (int)(kc * BKE), (int)(x.j * BN));
           }
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    mma_loop(m, tmem_base, KC, lane, a.diag);
+    mma_loop<T>(m, tmem_base, KC, lane, a.diag);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -599,7 +682,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = row < Q;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
       if (x.kind == 0) {
-        epi_phase1(a, tbase, row, valid, half, x.j);
+        epi_phase1<T>(a, tbase, row, valid, half, x.j);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
         // publish this warp's z / r.h columns to the phase-2 tiles of the M-tile
@@ -869,7 +952,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = row < Q;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
       if (x.kind == 0) {
-        epi_phase1(a, tbase, row, valid, half, x.j);
+        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
@@ -1034,7 +1117,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = row < Q;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
       if (x.kind == 0) {
-        epi_phase1(a, tbase, row, valid, half, x.j);
+        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&m.tempty[acc]);
@@ -1074,7 +1157,8 @@ typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, 
 
 struct TcState {
   uint32_t E = 0, H = 0, nub = 0, bmax = 0;
-  __nv_bfloat16 *w1 = nullptr, *w2 = nullptr, *rh16 = nullptr, *a1 = nullptr;
+  bool tf32 = false;               // operands fp32 read as TF32 (else bf16)
+  void *w1 = nullptr, *w2 = nullptr, *rh = nullptr, *a1 = nullptr;
   uint32_t *done1 = nullptr;
   int pair = 0;                    // 0: one-CTA kernel; 1: cta_group::2 pair; 2: B multicast in a cluster of 2 (RNNLM_TC_PAIR)
   uint32_t diag = 0;               // RNNLM_TC_DIAG: timing diagnostics, results invalid (1 no MMA, 2 no TMA)
@@ -1095,15 +1179,19 @@ static EncodeTiled get_encode() {
   return fn;
 }
 
-// 2D bf16 tensor [outer][inner], box {64, box_outer}, 128-byte swizzle.
-static bool make_map(CUtensorMap *m, void *base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+// 2D tensor [outer][inner] of bf16 (or fp32 when f32), box {one 128-byte
+// swizzle atom of K, box_outer}, 128-byte swizzle.
+static bool make_map(CUtensorMap *m, void *base, uint64_t inner, uint64_t outer, uint32_t box_outer,
+                     bool f32 = false) {
   EncodeTiled enc = get_encode();
   if (!enc) return false;
+  const uint32_t es_bytes = f32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, box_outer};
+  cuuint64_t strides[1] = {inner * es_bytes};
+  cuuint32_t box[2] = {128 / es_bytes, box_outer};
   cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+  return enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims,
+             strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1117,44 +1205,69 @@ int gru_tc_supported(uint32_t E, uint32_t H) {
   return E % BK == 0 && H % BN == 0 && E >= BK && H >= BN;
 }
 
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_out) {
-  *state_out = nullptr;
-  TcState *t = new TcState;
-  t->E = E; t->H = H; t->nub = H / UB;
-  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = atoi(e);
-  if (const char *e = getenv("RNNLM_TC_DIAG")) t->diag = (uint32_t)atoi(e);
+template <typename T>
+static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H) {
   const size_t K1 = E + H;
-  std::vector<__nv_bfloat16> w1((size_t)2 * H * K1), w2((size_t)H * K1);
-  std::vector<float> bzr((size_t)2 * H), bh(H);
+  std::vector<T> w1((size_t)2 * H * K1), w2((size_t)H * K1);
+  auto cv = [](float v) -> T {
+    if constexpr (sizeof(T) == 2) {
+      return __float2bfloat16_rn(v);
+    } else {  // round to TF32 (nearest, ties away; same as cvt.rna.tf32.f32 on the activations)
+      uint32_t b;
+      std::memcpy(&b, &v, 4);
+      b = (b + 0x1000u) & 0xFFFFE000u;
+      float r;
+      std::memcpy(&r, &b, 4);
+      return r;
+    }
+  };
   const float *Wg[2] = {w->Wz, w->Wr};
   const float *Ug[2] = {w->Uz, w->Ur};
-  const float *bg[2] = {w->bz, w->br};
   for (size_t u = 0; u < H; ++u) {
     const size_t ub = u / UB, uu = u % UB;
     for (int g = 0; g < 2; ++g) {
-      __nv_bfloat16 *row = w1.data() + (ub * BN + g * UB + uu) * K1;
-      for (size_t k = 0; k < E; ++k) row[k] = __float2bfloat16_rn(Wg[g][u * E + k]);
-      for (size_t k = 0; k < H; ++k) row[E + k] = __float2bfloat16_rn(Ug[g][u * H + k]);
-      bzr[ub * BN + g * UB + uu] = bg[g][u];
+      T *row = w1.data() + (ub * BN + g * UB + uu) * K1;
+      for (size_t k = 0; k < E; ++k) row[k] = cv(Wg[g][u * E + k]);
+      for (size_t k = 0; k < H; ++k) row[E + k] = cv(Ug[g][u * H + k]);
     }
-    __nv_bfloat16 *row2 = w2.data() + u * K1;
-    for (size_t k = 0; k < E; ++k) row2[k] = __float2bfloat16_rn(w->Wh[u * E + k]);
-    for (size_t k = 0; k < H; ++k) row2[E + k] = __float2bfloat16_rn(w->Uh[u * H + k]);
+    T *row2 = w2.data() + u * K1;
+    for (size_t k = 0; k < E; ++k) row2[k] = cv(w->Wh[u * E + k]);
+    for (size_t k = 0; k < H; ++k) row2[E + k] = cv(w->Uh[u * H + k]);
+  }
+  return cudaMalloc(&t->w1, w1.size() * sizeof(T)) == cudaSuccess &&
+         cudaMalloc(&t->w2, w2.size() * sizeof(T)) == cudaSuccess &&
+         cudaMemcpy(t->w1, w1.data(), w1.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(t->w2, w2.data(), w2.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
+}
+
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, void **state_out) {
+  *state_out = nullptr;
+  TcState *t = new TcState;
+  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0;
+  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = t->tf32 ? 0 : atoi(e);   // pair/multicast: bf16 only
+  if (const char *e = getenv("RNNLM_TC_DIAG")) t->diag = (uint32_t)atoi(e);
+  const size_t K1 = E + H;
+  std::vector<float> bzr((size_t)2 * H), bh(H);
+  const float *bg[2] = {w->bz, w->br};
+  for (size_t u = 0; u < H; ++u) {
+    const size_t ub = u / UB, uu = u % UB;
+    for (int g = 0; g < 2; ++g) bzr[ub * BN + g * UB + uu] = bg[g][u];
     bh[u] = w->bh[u];
   }
-  bool ok = cudaMalloc(&t->w1, w1.size() * 2) == cudaSuccess &&
-            cudaMalloc(&t->w2, w2.size() * 2) == cudaSuccess &&
-            cudaMalloc(&t->bzr, bzr.size() * 4) == cudaSuccess &&
-            cudaMalloc(&t->bh, bh.size() * 4) == cudaSuccess;
-  ok = ok && cudaMemcpy(t->w1, w1.data(), w1.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess;
-  ok = ok && cudaMemcpy(t->w2, w2.data(), w2.size() * 2, cudaMemcpyHostToDevice) == cudaSuccess;
+  bool ok = t->tf32 ? upload_w<float>(t, w, E, H) : upload_w<__nv_bfloat16>(t, w, E, H);
+  ok = ok && cudaMalloc(&t->bzr, bzr.size() * 4) == cudaSuccess &&
+       cudaMalloc(&t->bh, bh.size() * 4) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bzr, bzr.data(), bzr.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bh, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
-  ok = ok && make_map(&t->map_w1, t->w1, K1, 2 * (uint64_t)H, BN) &&
-       make_map(&t->map_w2, t->w2, K1, H, BN) &&
-       make_map(&t->map_w1h, t->w1, K1, 2 * (uint64_t)H, BN / 2) &&
-       make_map(&t->map_w2h, t->w2, K1, H, BN / 2);
-  ok = ok && cudaFuncSetAttribute(k_gru_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && make_map(&t->map_w1, t->w1, K1, 2 * (uint64_t)H, BN, t->tf32) &&
+       make_map(&t->map_w2, t->w2, K1, H, BN, t->tf32);
+  if (!t->tf32)
+    ok = ok && make_map(&t->map_w1h, t->w1, K1, 2 * (uint64_t)H, BN / 2) &&
+         make_map(&t->map_w2h, t->w2, K1, H, BN / 2);
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PAIR) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   *state_out = t;
@@ -1166,17 +1279,18 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, void **state_
 }
 
 // The activation maps need the engine's scratch; bound once per engine.
-int gru_tc_bind(void *state, __nv_bfloat16 *rh16, uint32_t bmax) {
+int gru_tc_bind(void *state, void *rh, uint32_t bmax) {
   TcState *t = static_cast<TcState *>(state);
-  t->rh16 = rh16;
+  t->rh = rh;
   t->bmax = bmax;
-  if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * 2) != cudaSuccess ||
+  const size_t es = t->tf32 ? 4 : 2;
+  if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * es) != cudaSuccess ||
       cudaMalloc(&t->done1, ((size_t)bmax / BM + 4) * sizeof(uint32_t)) != cudaSuccess) {
     (void)cudaGetLastError();
     return -1;
   }
-  t->bound = make_map(&t->map_rh, rh16, t->H, bmax, BM) &&
-             make_map(&t->map_a1, t->a1, t->E + t->H, bmax, BM);
+  t->bound = make_map(&t->map_rh, rh, t->H, bmax, BM, t->tf32) &&
+             make_map(&t->map_a1, t->a1, t->E + t->H, bmax, BM, t->tf32);
   return t->bound ? 0 : -1;
 }
 
@@ -1201,7 +1315,8 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.emb16 = P.emb16; a.state = P.state; a.bzr = t->bzr; a.bh = t->bh;
   a.state_out = P.state;
   a.row_src = P.row_src; a.row_dst = P.row_dst; a.row_word = P.row_word; a.counts = P.counts;
-  a.g_z = P.g_z; a.g_rh16 = P.g_rh16; a.a1 = t->a1;
+  a.g_z = P.g_z; a.g_rh16 = P.g_rh16; a.g_rhf = P.g_rh;
+  a.a1 = static_cast<__nv_bfloat16 *>(t->a1); a.a1f = static_cast<float *>(t->a1); a.emb = P.emb;
   a.cache = P.cache; a.key_mode = P.key_mode; a.round_digits = P.round_digits;
   a.cstride = P.cstride; a.round_scale = P.round_scale; a.codes = P.codes; a.codehash = P.codehash;
   a.done1 = t->done1;
@@ -1213,7 +1328,8 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
   uint32_t gg = (max_rows + 7) / 8;
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
-  launch_pdl(k_gather_a1, gg, 256, 0, s, a);
+  if (t->tf32) launch_pdl(k_gather_a1<float>, gg, 256, 0, s, a);
+  else launch_pdl(k_gather_a1<__nv_bfloat16>, gg, 256, 0, s, a);
   if (ev_gathered) cudaEventRecord(ev_gathered, s);
   if (t->pair) {
     uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / BN) * 2;
@@ -1226,7 +1342,8 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
       launch_pdl_cluster(k_gru_tc_mc, gp, THREADS, SMEM, s, 2, t->map_a1, t->map_w1h, t->map_rh,
                          t->map_w2h, a);
   } else {
-    launch_pdl(k_gru_tc, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+    if (t->tf32) launch_pdl(k_gru_tc<float>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+    else launch_pdl(k_gru_tc<__nv_bfloat16>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
   }
   if (ev_phase1) cudaEventRecord(ev_phase1, s);
   return 2;

@@ -2,7 +2,7 @@
 
 Bar (BASELINE.json north_star): bit-exact keys, MaxEnt indices, outcomes,
 handles, slots, stats; scores and states within 1e-5 (FP32 path) / 1e-3
-(BF16 tensor-core path).  Inputs: seeded synth/ generators with the shapes of
+(BF16 and TF32 tensor-core paths).  Inputs: seeded synth/ generators with the shapes of
 the BASELINE.json configs.
 """
 import numpy as np
@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import oracle as O
-from paper_1801_09866_b200 import (KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, RNNLM,
+from paper_1801_09866_b200 import (KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32, RNNLM,
                                    INVALID, MISS, QHIT, SHIT)
 from synth import generate_model, generate_workload, model_dims
 from synth.model import ModelDims
@@ -18,7 +18,7 @@ from tests.parity_util import _dev, replay_compare
 
 pytestmark = pytest.mark.gpu
 
-TOL = {MATH_FP32: 1e-5, MATH_BF16: 1e-3}
+TOL = {MATH_FP32: 1e-5, MATH_BF16: 1e-3, MATH_TF32: 1e-3}   # 1e-3 for bf16/tf32
 _models = {}
 
 
@@ -277,6 +277,46 @@ def test_multisession_bf16_sample():
     wl = generate_workload(4, 3, 2048, d.V, seed=7)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16)
     replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+
+
+# ---------------------------------------------------------------- TF32 tensor-core path (tcgen05 kind::tf32)
+@pytest.mark.parametrize("mode", [KEY_OFF, KEY_SIGN])
+def test_moderate_tf32_tensor_core(mode):
+    d, m = model("moderate")
+    wl = generate_workload(1, 40, 256, d.V, seed=17)
+    eng, orc = pair(d, m, wl, mode, math=MATH_TF32)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_TF32], tol_state=TOL[MATH_TF32])
+    assert rep["miss"] > 300
+
+
+def test_large_tf32_cache_off_full_tiles():
+    d, m = model("large")
+    wl = generate_workload(1, 2, 2048, d.V, seed=5)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_TF32, cache=False)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_TF32], tol_state=TOL[MATH_TF32])
+    assert rep["miss"] == wl.n_total
+
+
+def test_large_tf32_ragged_multisession():
+    d, m = model("large")
+    wl = generate_workload(3, 3, 300, d.V, seed=6)
+    eng, orc = pair(d, m, wl, KEY_ROUND, k=2, math=MATH_TF32)
+    replay_compare(eng, orc, wl, tol_score=TOL[MATH_TF32], tol_state=TOL[MATH_TF32])
+
+
+def test_tf32_more_accurate_than_bf16():
+    """TF32 operands keep 11 significant bits (bf16: 8), so with weights that
+    are NOT on the bf16 grid the TF32 path's state error vs the fp64 oracle is
+    several times below the bf16 path's on the same rows (replay mode)."""
+    d = ModelDims(V=1000, E=256, H=256, maxent_log2=16, N=3)
+    m = generate_model(d, seed=3, scale=0.1, bf16_grid=False)
+    wl = generate_workload(1, 6, 256, d.V, seed=8)
+    errs = {}
+    for math in (MATH_BF16, MATH_TF32):
+        eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cache=False)
+        errs[math] = replay_compare(eng, orc, wl, tol_score=1e-2, tol_state=1e-2)["max_state_err"]
+    assert errs[MATH_TF32] < 0.3 * errs[MATH_BF16], errs
+    assert errs[MATH_TF32] < 1e-4, errs
 
 
 def test_per_query_calls_equal_per_frame_batches():
