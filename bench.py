@@ -103,7 +103,8 @@ def time_oracle(dims, model, wl, mode, k, cache, budget_s, max_steps=None):
     import oracle as O
     one = wl.select_sessions(0, 1)
     cfg = O.make_config(dims.V, dims.E, dims.H, dims.maxent_log2, dims.N, mode, k,
-                        1 if cache else 0, 1, one.max_histories_hint())
+                        1 if cache else 0, 1,
+                        one.max_histories_hint() if cache else one.frames * one.B_s + 2)
     orc = O.Oracle(cfg, model)
     child = np.zeros(one.n_total, np.uint32)
     done_q, t_total, f = 0, 0.0, 0
@@ -225,7 +226,9 @@ def run_ours(args):
     mode, k = key_mode(args.key)
     math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32}[args.math]
     n = wl.n_per_frame
-    cap = wl.max_histories_hint()
+    # cache off: every valid query makes a new history (reading 23), so the
+    # per-session pool must hold one per query of the run
+    cap = wl.max_histories_hint() if not args.no_cache else frames * B_s + 2
     eng = R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math,
                             cache_enabled=not args.no_cache, num_sessions=S,
                             max_queries_per_call=n, max_histories_per_session=cap, device=local)

@@ -274,7 +274,8 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   chk(dalloc(h, &P.tile_status, (B + rnnlm_host::SCAN_TILE - 1) / rnnlm_host::SCAN_TILE));
   chk(dalloc(h, &P.tile_ticket, 1));
   chk(dalloc(h, &P.counts, 4));
-  chk(dalloc(h, &P.g_z, B * H));
+  // z: the tensor-core path keeps it in 128-row blocks (k_gru_tc.cu zq4), so whole blocks
+  chk(dalloc(h, &P.g_z, (B + 127) / 128 * 128 * H));
   if (c.math == RNNLM_MATH_FP32) chk(dalloc(h, &P.g_wxb, B * H));
   if (c.math == RNNLM_MATH_BF16) chk(dalloc(h, &P.g_rh16, B * H));
   else chk(dalloc(h, &P.g_rh, B * H));

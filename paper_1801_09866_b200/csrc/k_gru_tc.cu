@@ -54,6 +54,7 @@ constexpr int ST = RNNLM_TC_ST;  // smem pipeline stages
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES = BN * BK * 2;          // 32 KB
 constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 columns
+constexpr int STG_BYTES = 32 * 128;           // epilogue staging buffer per epilogue warp
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -228,7 +229,7 @@ struct TcArgs {
   uint32_t *done1;                 // per M-tile phase-1 epilogue arrivals (zeroed by the gather)
   uint32_t *tile_ctr;              // dynamic tile scheduler (zeroed by the gather)
   uint32_t lag;                    // phase-2 tiles trail phase-1 tiles by this many M-tiles
-  uint32_t diag;                   // timing diagnostics only (results invalid): 1 no MMA, 2 no TMA
+  uint32_t diag;                   // timing diagnostics only (results invalid): 1 no MMA, 2 no TMA, 3 no epilogue, 4 = 3 + no phase dependency
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
   float round_scale;
@@ -284,7 +285,7 @@ constexpr int TQ = 4;            // depth of the tile-id ring (producer -> MMA /
 constexpr uint32_t NO_TILE = 0xFFFFFFFFu;
 
 struct Smem {
-  uint8_t *sA, *sB;
+  uint8_t *sA, *sB, *stg;
   uint64_t *full, *empty, *tfull, *tempty, *qfull, *qempty;
   uint32_t *tmem_base;
   uint32_t *tile_q;
@@ -295,7 +296,8 @@ __device__ __forceinline__ Smem carve(uint8_t *raw) {
   Smem m;
   m.sA = smem;
   m.sB = smem + ST * A_BYTES;
-  m.full = reinterpret_cast<uint64_t *>(m.sB + ST * B_BYTES);
+  m.stg = m.sB + ST * B_BYTES;
+  m.full = reinterpret_cast<uint64_t *>(m.stg + EPI_WARPS * STG_BYTES);
   m.empty = m.full + ST;
   m.tfull = m.empty + ST;
   m.tempty = m.tfull + 2;
@@ -395,8 +397,8 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
       tc_fence_after();
       if (lane == 0) {
         const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
-#pragma unroll
         if (diag != 1)
+#pragma unroll
           for (int k = 0; k < 4; ++k)
             Op<T>::mma(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
         umma_commit(&m.empty[stage]);
@@ -463,143 +465,198 @@ __device__ __forceinline__ unsigned long long encode16(const TcArgs &a, const fl
 }
 
 
-// Phase-1 epilogue of one thread: row r_in of the tile, the 128 z columns
+// ---------------------------------------------------------------- epilogue I/O
+// An epilogue thread owns one tile row (its TMEM lane) and walks its columns
+// in chunks of 32.  Row-per-thread global accesses would touch 32 different
+// lines per warp instruction (the L1 wavefront rate then bounds the epilogue,
+// not the MMAs), so:
+//  * z (internal scratch) lives in 128-row blocks, zq4() below, in which a
+//    warp's 32 rows x 4 units are 512 contiguous bytes;
+//  * rows the layout is not ours to choose (parent states, the new states,
+//    the r.h / A1 rows) move through a per-warp 32-row staging buffer in
+//    shared memory: the warp reads / writes RB contiguous bytes of each of
+//    512 / RB rows per instruction, and each thread exchanges its own row
+//    with the buffer.  16-byte chunks are XOR-swizzled so both access
+//    patterns are bank-conflict-free.
+
+// float4 index of z(row, u), u a multiple of 4: blocks of 128 rows x 4 units
+__device__ __forceinline__ size_t zq4(uint32_t row, uint32_t u, uint32_t H) {
+  return ((((size_t)(row >> 7) * (H >> 4) + (u >> 4)) * 4 + ((u & 15) >> 2)) << 7) + (row & 127);
+}
+
+template <int RB>
+__device__ __forceinline__ uint32_t stg_off(uint32_t r, uint32_t c) {
+  if constexpr (RB == 128) return r * 128 + ((c ^ (r & 7)) << 4);
+  else return r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+}
+
+// rows -> staging: lane l contributes its row's pointer (nullptr: not loaded)
+template <int RB>
+__device__ __forceinline__ void coop_load(uint8_t *stg, const void *row_ptr, uint32_t lane) {
+  constexpr int CPR = RB / 16, RPI = 32 / CPR;         // 16-B chunks per row, rows per instruction
+  uint4 v[CPR];
+#pragma unroll
+  for (int i = 0; i < CPR; ++i) {
+    const uint32_t r = i * RPI + lane / CPR, c = lane % CPR;
+    const uint8_t *p = reinterpret_cast<const uint8_t *>(
+        __shfl_sync(0xFFFFFFFFu, reinterpret_cast<unsigned long long>(row_ptr), r));
+    v[i] = p ? *reinterpret_cast<const uint4 *>(p + c * 16) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int i = 0; i < CPR; ++i) {
+    const uint32_t r = i * RPI + lane / CPR, c = lane % CPR;
+    *reinterpret_cast<uint4 *>(stg + stg_off<RB>(r, c)) = v[i];
+  }
+  __syncwarp();
+}
+// staging -> rows (after each lane wrote its own row); nullptr rows are skipped
+template <int RB>
+__device__ __forceinline__ void coop_store(uint8_t *stg, void *row_ptr, uint32_t lane) {
+  constexpr int CPR = RB / 16, RPI = 32 / CPR;
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < CPR; ++i) {
+    const uint32_t r = i * RPI + lane / CPR, c = lane % CPR;
+    uint8_t *p = reinterpret_cast<uint8_t *>(
+        __shfl_sync(0xFFFFFFFFu, reinterpret_cast<unsigned long long>(row_ptr), r));
+    const uint4 v = *reinterpret_cast<const uint4 *>(stg + stg_off<RB>(r, c));
+    if (p) *reinterpret_cast<uint4 *>(p + c * 16) = v;
+  }
+  __syncwarp();
+}
+// this lane's row of the staging buffer, as 32 fp32 / 32 bf16 values
+__device__ __forceinline__ void own_row_f32(const uint8_t *stg, uint32_t lane, float *x) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 t = *reinterpret_cast<const float4 *>(stg + stg_off<128>(lane, c));
+    x[4 * c] = t.x; x[4 * c + 1] = t.y; x[4 * c + 2] = t.z; x[4 * c + 3] = t.w;
+  }
+}
+__device__ __forceinline__ void put_row_f32(uint8_t *stg, uint32_t lane, const float *x) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4 *>(stg + stg_off<128>(lane, c)) =
+        make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+}
+__device__ __forceinline__ void own_row_bf16(const uint8_t *stg, uint32_t lane, float *x) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 t = *reinterpret_cast<const uint4 *>(stg + stg_off<64>(lane, c));
+    const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x[8 * c + 2 * j] = __uint_as_float(w[j] << 16);
+      x[8 * c + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+    }
+  }
+}
+__device__ __forceinline__ void put_row_bf16(uint8_t *stg, uint32_t lane, const float *x) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 t2 = __floats2bfloat162_rn(x[8 * c + 2 * j], x[8 * c + 2 * j + 1]);
+      w[j] = *reinterpret_cast<uint32_t *>(&t2);
+    }
+    *reinterpret_cast<uint4 *>(stg + stg_off<64>(lane, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+// 32 consecutive accumulator columns of this thread's TMEM lane (wait separately)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+  tmem_ld16(taddr, v);
+  tmem_ld16(taddr + 16, v + 16);
+}
+
+// Phase-1 epilogue of one thread: row `row` of the tile, the 128 z columns
 // (gate 0) or r columns (gate 1) of unit block ub.  The parent state h of
 // r.h is, on the bf16 path, the bf16 copy in the row's A1 row (the value
 // phase 1 multiplied); on the TF32 path the exact fp32 state.
 template <typename T>
 __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid,
-                                           int gate, uint32_t ub) {
+                                           int gate, uint32_t ub, uint8_t *stg, uint32_t lane) {
   const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB;
-  const size_t o = (size_t)(valid ? row : 0) * a.H + ub * UB;
-  const size_t ho = (size_t)(valid ? row : 0) * (a.E + a.H) + a.E + ub * UB;
-  const float *hs = nullptr;                         // TF32 path: the exact fp32 parent state
-  if constexpr (sizeof(T) == 4) hs = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + ub * UB;
-  auto process = [&](int g, const float *v) {
-    float bias16[16];
-    ld_bias16(bias + g * 16, bias16);
-    float hv[16];
-    if constexpr (sizeof(T) == 2) {
-      uint4 hb[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-      if (gate == 1 && valid) {
-        hb[0] = *reinterpret_cast<const uint4 *>(a.a1 + ho + g * 16);
-        hb[1] = *reinterpret_cast<const uint4 *>(a.a1 + ho + g * 16 + 8);
-      }
-      const uint32_t *hw = reinterpret_cast<const uint32_t *>(hb);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        hv[2 * j] = __uint_as_float(hw[j] << 16);
-        hv[2 * j + 1] = __uint_as_float(hw[j] & 0xFFFF0000u);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float4 t4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gate == 1 && valid) t4 = *reinterpret_cast<const float4 *>(hs + g * 16 + 4 * j);
-        hv[4 * j] = t4.x; hv[4 * j + 1] = t4.y; hv[4 * j + 2] = t4.z; hv[4 * j + 3] = t4.w;
-      }
-    }
-    float sg[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) sg[j] = sigm(v[j] + bias16[j]);
-    if (!valid) return;
-    if (gate == 0) {
-      float4 *gz = reinterpret_cast<float4 *>(a.g_z + o + g * 16);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) gz[j] = make_float4(sg[4 * j], sg[4 * j + 1], sg[4 * j + 2], sg[4 * j + 3]);
-    } else if constexpr (sizeof(T) == 2) {
-      uint4 pk[2];
-      uint32_t *pw = reinterpret_cast<uint32_t *>(pk);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        __nv_bfloat162 t2 = __floats2bfloat162_rn(sg[2 * j] * hv[2 * j], sg[2 * j + 1] * hv[2 * j + 1]);
-        pw[j] = *reinterpret_cast<uint32_t *>(&t2);
-      }
-      uint4 *gr = reinterpret_cast<uint4 *>(a.g_rh16 + o + g * 16);
-      gr[0] = pk[0];
-      gr[1] = pk[1];
-    } else {
-      float4 *gr = reinterpret_cast<float4 *>(a.g_rhf + o + g * 16);
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        gr[j] = to_tf32(make_float4(sg[4 * j] * hv[4 * j], sg[4 * j + 1] * hv[4 * j + 1],
-                                    sg[4 * j + 2] * hv[4 * j + 2], sg[4 * j + 3] * hv[4 * j + 3]));
-    }
-  };
-  float va[16], vb[16];
-  tmem_ld16(tbase, va);
-  tmem_ld_wait();
+  const uint32_t u0 = ub * UB;
 #pragma unroll 1
-  for (int g = 0; g < UB / 16; g += 2) {
-    tmem_ld16(tbase + (g + 1) * 16, vb);
-    process(g, va);
-    tmem_ld_wait();
-    if (g + 2 < UB / 16) tmem_ld16(tbase + (g + 2) * 16, va);
-    process(g + 1, vb);
-    tmem_ld_wait();
+  for (int c = 0; c < UB / 32; ++c) {
+    float v[32], b[32];
+    tmem_ld32(tbase + c * 32, v);
+    ld_bias16(bias + c * 32, b);
+    ld_bias16(bias + c * 32 + 16, b + 16);
+    if (gate == 0) {
+      tmem_ld_wait();
+      if (valid) {
+        float4 *zq = reinterpret_cast<float4 *>(a.g_z) + zq4(row, u0 + c * 32, a.H);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          zq[j << 7] = make_float4(sigm(v[4 * j] + b[4 * j]), sigm(v[4 * j + 1] + b[4 * j + 1]),
+                                   sigm(v[4 * j + 2] + b[4 * j + 2]), sigm(v[4 * j + 3] + b[4 * j + 3]));
+      }
+    } else {
+      float hv[32];
+      if constexpr (sizeof(T) == 2) {
+        coop_load<64>(stg, valid ? a.a1 + (size_t)row * (a.E + a.H) + a.E + u0 + c * 32 : nullptr, lane);
+        own_row_bf16(stg, lane, hv);
+      } else {
+        coop_load<128>(stg, valid ? a.state + (size_t)a.row_src[row] * a.H + u0 + c * 32 : nullptr, lane);
+        own_row_f32(stg, lane, hv);
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) hv[j] *= sigm(v[j] + b[j]);
+      __syncwarp();
+      if constexpr (sizeof(T) == 2) {
+        put_row_bf16(stg, lane, hv);
+        coop_store<64>(stg, valid ? a.g_rh16 + (size_t)row * a.H + u0 + c * 32 : nullptr, lane);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hv[j] = to_tf32(hv[j]);
+        put_row_f32(stg, lane, hv);
+        coop_store<128>(stg, valid ? a.g_rhf + (size_t)row * a.H + u0 + c * 32 : nullptr, lane);
+      }
+    }
   }
 }
 
-// Phase-2 epilogue of one thread: row r_in, 128 units starting at n0.
+// Phase-2 epilogue of one thread: row `row`, 128 units starting at n0.
 __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid,
-                                           uint32_t n0) {
+                                           uint32_t n0, uint8_t *stg, uint32_t lane) {
   const uint32_t dst = valid ? a.row_dst[row] : NONE;
-  const float *hp = a.state + (size_t)(valid ? a.row_src[row] : 0) * a.H + n0;
-  const size_t o = (size_t)(valid ? row : 0) * a.H + n0;
-  uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && dst != NONE)
-                      ? a.codes + (size_t)dst * a.cstride : nullptr;
+  const bool live = dst != NONE;
+  const float *hp = live ? a.state + (size_t)a.row_src[row] * a.H + n0 : nullptr;
+  float *hout = live ? a.state_out + (size_t)dst * a.H + n0 : nullptr;
+  uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && live) ? a.codes + (size_t)dst * a.cstride : nullptr;
+  const float4 *zq = reinterpret_cast<const float4 *>(a.g_z) + zq4(live ? row : 0, n0, a.H);
   unsigned long long hs = 0;
   uint32_t signacc = 0;
-  // global operands of group g+1 (z, h, bias) are loaded while group g is
-  // processed; TMEM loads are double-buffered the same way
-  auto fetch = [&](int g, float4 *z4, float4 *h4, float *bias16) {
-    if (dst == NONE) return;
-    ld_bias16(a.bh + n0 + g * 16, bias16);
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {                  // 4 chunks of 32 units
+    float v[32], b[32], z[32], h[32];
+    tmem_ld32(tbase + c * 32, v);
+    if (live) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      z4[j] = *reinterpret_cast<const float4 *>(a.g_z + o + g * 16 + 4 * j);
-      h4[j] = *reinterpret_cast<const float4 *>(hp + g * 16 + 4 * j);
-    }
-  };
-  auto process = [&](int g, const float *vu, const float4 *z4, const float4 *h4, const float *bias16) {
-    if (dst == NONE) return;
-    float hn[16];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float zz[4] = {z4[j].x, z4[j].y, z4[j].z, z4[j].w};
-      const float hh[4] = {h4[j].x, h4[j].y, h4[j].z, h4[j].w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float c = tanh_fast(vu[4 * j + t] + bias16[4 * j + t]);
-        hn[4 * j + t] = (1.0f - zz[t]) * hh[t] + zz[t] * c;
+      for (int j = 0; j < 8; ++j) {
+        const float4 t = zq[(c * 8 + j) << 7];
+        z[4 * j] = t.x; z[4 * j + 1] = t.y; z[4 * j + 2] = t.z; z[4 * j + 3] = t.w;
       }
     }
-    float4 *so = reinterpret_cast<float4 *>(a.state_out + (size_t)dst * a.H + n0 + g * 16);
+    ld_bias16(a.bh + n0 + c * 32, b);
+    ld_bias16(a.bh + n0 + c * 32 + 16, b + 16);
+    coop_load<128>(stg, hp ? hp + c * 32 : nullptr, lane);
+    own_row_f32(stg, lane, h);
+    tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 4; ++j) so[j] = make_float4(hn[4 * j], hn[4 * j + 1], hn[4 * j + 2], hn[4 * j + 3]);
-    if (a.cache) hs += encode16(a, hn, n0 + g * 16, code, signacc);
-  };
-  float va[16], vb[16], ba[16], bb2[16];
-  float4 za[4], ha[4], zb[4], hb[4];
-  fetch(0, za, ha, ba);
-  tmem_ld16(tbase, va);
-  tmem_ld_wait();
-#pragma unroll 1
-  for (int g = 0; g < BN / 32; g += 2) {
-    tmem_ld16(tbase + (g + 1) * 16, vb);
-    fetch(g + 1, zb, hb, bb2);
-    process(g, va, za, ha, ba);
-    tmem_ld_wait();
-    if (g + 2 < BN / 32) {
-      tmem_ld16(tbase + (g + 2) * 16, va);
-      fetch(g + 2, za, ha, ba);
+    for (int j = 0; j < 32; ++j) h[j] = (1.0f - z[j]) * h[j] + z[j] * tanh_fast(v[j] + b[j]);
+    __syncwarp();
+    put_row_f32(stg, lane, h);
+    coop_store<128>(stg, hout ? hout + c * 32 : nullptr, lane);
+    if (a.cache && live) {
+      hs += encode16(a, h, n0 + c * 32, code, signacc);
+      hs += encode16(a, h + 16, n0 + c * 32 + 16, code, signacc);
     }
-    process(g + 1, vb, zb, hb, bb2);
-    tmem_ld_wait();
   }
-  if (a.cache && dst != NONE) atomicAdd(&a.codehash[dst], hs);
+  if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
 }
-
 // =============================================================== fused GRU kernel
 // warp 0: TMA producer (waits on the phase-1 counter before a phase-2 tile);
 // warp 1: TMEM allocation + MMA issue; warps 2-9: epilogue, TMEM lane quarter
@@ -640,7 +697,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (t == NO_TILE) break;
         const Tile x = tile_of(t, mt, n1, n2, L);
         const uint32_t m0 = x.m * BM;
-        if (x.kind == 1) {
+        if (x.kind == 1 && a.diag != 4) {
           wait_phase1(a.done1 + x.m, target);
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
@@ -681,8 +738,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t row = x.m * BM + r_in;
       const bool valid = row < Q;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
+      if (a.diag >= 3) {                                  // timing only: no epilogue work
+        float v[16];
+        tmem_ld16(tbase, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&m.tempty[acc]);
+        if (x.kind == 0) {
+          __syncwarp();
+          if (lane == 0) { __threadfence(); atomicAdd(a.done1 + x.m, 1u); }
+        }
+        continue;
+      }
       if (x.kind == 0) {
-        epi_phase1<T>(a, tbase, row, valid, half, x.j);
+        epi_phase1<T>(a, tbase, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
         // publish this warp's z / r.h columns to the phase-2 tiles of the M-tile
@@ -694,7 +763,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       } else {
         wait_phase1(a.done1 + x.m, target);               // acquire z of this M-tile
-        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2));
+        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
       }
@@ -774,7 +843,7 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols
 }
 
 struct SmemP {
-  uint8_t *sA, *sB;
+  uint8_t *sA, *sB, *stg;
   uint64_t *full, *empty, *tfull, *tempty, *qfull, *qempty;
   uint32_t *tmem_base, *tile_q;
 };
@@ -784,7 +853,8 @@ __device__ __forceinline__ SmemP carve_pair(uint8_t *raw) {
   SmemP m;
   m.sA = smem;
   m.sB = smem + STP * A_BYTES;
-  m.full = reinterpret_cast<uint64_t *>(m.sB + STP * BP_BYTES);
+  m.stg = m.sB + STP * BP_BYTES;
+  m.full = reinterpret_cast<uint64_t *>(m.stg + EPI_WARPS * STG_BYTES);
   m.empty = m.full + STP;
   m.tfull = m.empty + STP;
   m.tempty = m.tfull + 2;
@@ -952,7 +1022,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = row < Q;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
       if (x.kind == 0) {
-        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j);
+        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
@@ -964,7 +1034,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       } else {
         wait_phase1(a.done1 + x.m, target);
-        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2));
+        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
@@ -1117,7 +1187,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = row < Q;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
       if (x.kind == 0) {
-        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j);
+        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&m.tempty[acc]);
@@ -1129,7 +1199,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       } else {
         wait_phase1(a.done1 + x.m, target);
-        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2));
+        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&m.tempty[acc]);
@@ -1145,9 +1215,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-constexpr size_t SMEM_PAIR = 1024 + STP * (A_BYTES + BP_BYTES) + 256;
+constexpr size_t SMEM_PAIR = 1024 + STP * (A_BYTES + BP_BYTES) + EPI_WARPS * STG_BYTES + 256;
 
-constexpr size_t SMEM = 1024 + ST * (A_BYTES + B_BYTES) + 256;
+constexpr size_t SMEM = 1024 + ST * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 256;
 
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
