@@ -34,6 +34,7 @@
 // discarded.
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -229,7 +230,9 @@ struct TcArgs {
   uint32_t *done1;                 // per M-tile phase-1 epilogue arrivals (zeroed by the gather)
   uint32_t *tile_ctr;              // dynamic tile scheduler (zeroed by the gather)
   uint32_t lag;                    // phase-2 tiles trail phase-1 tiles by this many M-tiles
-  uint32_t diag;                   // timing diagnostics only (results invalid): 1 no MMA, 2 no TMA, 3 no epilogue, 4 = 3 + no phase dependency
+  uint32_t diag;                   // timing diagnostics: 1 no MMA, 2 no TMA, 3 no epilogue, 4 = 3 + no phase
+                                   // dependency, 6 = 1 + 2 (results invalid); 5 cycle counters (results valid)
+  unsigned long long *prof;        // diag 5: per-CTA cycle counters, else nullptr
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
   float round_scale;
@@ -383,21 +386,26 @@ __device__ __forceinline__ uint32_t next_tile(const Smem &m, uint32_t it, bool r
 // MMA issuer: KC chunks of 4 x (M=128, N=256, K=32 bytes) per tile, both phases.
 template <typename T>
 __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, int lane,
-                                         uint32_t diag) {
+                                         uint32_t diag, unsigned long long *prof) {
   uint32_t stage = 0, phase = 0;
   const uint32_t id = idesc_of(Op<T>::FMT, BM, BN);
+  unsigned long long w_full = 0, w_tempty = 0, t0;
   for (uint32_t it = 0;; ++it) {
     if (next_tile(m, it, lane == 0) == NO_TILE) break;
     const uint32_t acc = it & 1;
+    t0 = clock64();
     mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
+    w_tempty += clock64() - t0;
     tc_fence_after();
     const uint32_t tm = tmem_base + acc * BN;
     for (uint32_t kc = 0; kc < KC; ++kc) {
+      t0 = clock64();
       mbar_wait(&m.full[stage], phase);
+      w_full += clock64() - t0;
       tc_fence_after();
       if (lane == 0) {
         const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
-        if (diag != 1)
+        if (diag != 1 && diag != 6)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             Op<T>::mma(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
@@ -408,6 +416,7 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
       if (++stage == ST) { stage = 0; phase ^= 1; }
     }
   }
+  if (prof && lane == 0) { prof[2] = w_full; prof[3] = w_tempty; }
 }
 
 // Compression code words of 16 consecutive new-state elements starting at
@@ -683,10 +692,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t L = mt < a.lag ? mt : a.lag;
   const uint32_t ntiles = mt * (n1 + n2);
   const uint32_t tmem_base = *m.tmem_base;
+  unsigned long long *prof = a.prof ? a.prof + blockIdx.x * 16 : nullptr;
+  const unsigned long long k_t0 = clock64();
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      unsigned long long w_empty = 0, w_dep = 0, t0;
       for (uint32_t it = 0;; ++it) {
         const uint32_t slot = it % TQ;
         mbar_wait(&m.qempty[slot], ((it / TQ) & 1) ^ 1);
@@ -698,12 +710,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         const Tile x = tile_of(t, mt, n1, n2, L);
         const uint32_t m0 = x.m * BM;
         if (x.kind == 1 && a.diag != 4) {
+          t0 = clock64();
           wait_phase1(a.done1 + x.m, target);
+          w_dep += clock64() - t0;
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
+        if (prof) prof[9 + x.kind] += 1;
         for (uint32_t kc = 0; kc < KC; ++kc) {
+          t0 = clock64();
           mbar_wait(&m.empty[stage], phase ^ 1);
-          if (a.diag == 2) {
+          w_empty += clock64() - t0;
+          if (a.diag == 2 || a.diag == 6) {
             mbar_arrive(&m.full[stage]);
             if (++stage == ST) { stage = 0; phase ^= 1; }
             continue;
@@ -721,24 +738,29 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
       }
+      if (prof) { prof[0] = w_empty; prof[1] = w_dep; }
     }
   } else if (warp == 1) {
-    mma_loop<T>(m, tmem_base, KC, lane, a.diag);
+    mma_loop<T>(m, tmem_base, KC, lane, a.diag, prof);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r_in = q * 32 + lane;
+    unsigned long long w_tfull = 0, b1 = 0, b2 = 0, t0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t t = next_tile(m, it, lane == 0);
       if (t == NO_TILE) break;
       const Tile x = tile_of(t, mt, n1, n2, L);
       const uint32_t acc = it & 1;
+      t0 = clock64();
       mbar_wait(&m.tfull[acc], (it >> 1) & 1);
+      w_tfull += clock64() - t0;
+      t0 = clock64();
       tc_fence_after();
       const uint32_t row = x.m * BM + r_in;
       const bool valid = row < Q;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
-      if (a.diag >= 3) {                                  // timing only: no epilogue work
+      if (a.diag == 3 || a.diag == 4) {                   // timing only: no epilogue work
         float v[16];
         tmem_ld16(tbase, v);
         tmem_ld_wait();
@@ -761,14 +783,21 @@ __global__ void __launch_bounds__(THREADS, 1)
           __threadfence();
           atomicAdd(a.done1 + x.m, 1u);
         }
+        b1 += clock64() - t0;
       } else {
         wait_phase1(a.done1 + x.m, target);               // acquire z of this M-tile
         epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
+        b2 += clock64() - t0;
       }
     }
+    if (prof && lane == 0 && (warp == 2 || warp == 6)) {
+      const int o = warp == 2 ? 4 : 11;
+      prof[o] = w_tfull; prof[o + 1] = b1; prof[o + 2] = b2;
+    }
   }
+  if (prof && threadIdx.x == 0) prof[8] = clock64() - k_t0;
   teardown(m, warp, tmem_base);
 }
 
@@ -865,9 +894,13 @@ __device__ __forceinline__ SmemP carve_pair(uint8_t *raw) {
   return m;
 }
 
-// warp 0: TMA producer (both CTAs; the leader also claims tiles);
+// warp 0: TMA producer (both CTAs; the leader also claims the tiles);
 // warp 1: TMEM allocation (both) + MMA issue (leader only);
 // warps 2-9: epilogue of this CTA's 128 rows.
+// Both CTAs' TMA loads of a stage complete on the LEADER's full barrier
+// (cp.async.bulk.tensor .cta_group::2), which the leader arms with the bytes
+// of both halves; the MMA commit releases the stage in both CTAs at once
+// (multicast), so no CTA-to-CTA handshake sits on the K loop.
 __global__ void __launch_bounds__(THREADS, 1)
     k_gru_tc2(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1h,
               const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2h,
@@ -880,10 +913,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t n1 = a.nub, n2 = a.H / BN;
   const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
   const uint32_t target = n1 * 2 * EPI_WARPS;           // phase-1 arrivals per 256-row tile
+  // tile-ring consumers (arrivals on the leader's qempty per slot): the
+  // leader's MMA lane, the peer's producer, both CTAs' epilogue warps
+  constexpr uint32_t RING_CONSUMERS = 2 + 2 * EPI_WARPS;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STP; ++s) { mbar_init(&m.full[s], leader ? 2 : 1); mbar_init(&m.empty[s], 1); }
+    for (int s = 0; s < STP; ++s) { mbar_init(&m.full[s], 1); mbar_init(&m.empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&m.tfull[s], 1); mbar_init(&m.tempty[s], 2 * EPI_WARPS); }
-    for (int s = 0; s < TQ; ++s) { mbar_init(&m.qfull[s], 1); mbar_init(&m.qempty[s], 2 * (2 + EPI_WARPS)); }
+    for (int s = 0; s < TQ; ++s) { mbar_init(&m.qfull[s], 1); mbar_init(&m.qempty[s], RING_CONSUMERS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&map_a1); prefetch_map(&map_w1h); prefetch_map(&map_rh); prefetch_map(&map_w2h);
   }
@@ -898,208 +934,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t L = mt < a.lag / 2 ? mt : a.lag / 2;
   const uint32_t ntiles = mt * (n1 + n2);
   const uint32_t tmem_base = *m.tmem_base;
-  const uint32_t full0 = mapa(smem_u32(&m.full[0]), 0);       // leader's barriers
+  const uint32_t full0 = mapa(smem_u32(&m.full[0]), 0);       // the leader's barriers
   const uint32_t tempty0 = mapa(smem_u32(&m.tempty[0]), 0);
   const uint32_t qempty0 = mapa(smem_u32(&m.qempty[0]), 0);
+  unsigned long long *prof = a.prof ? a.prof + blockIdx.x * 16 : nullptr;
+  const unsigned long long k_t0 = clock64();
 
-  // tile id of ring slot `it` for a consumer warp; one lane releases the slot
-  // on the leader's qempty (ring consumers: both CTAs' producer + epilogue warps)
-  auto take = [&](uint32_t it, bool release) -> uint32_t {
-    const uint32_t slot = it % TQ;
-    mbar_wait_cl(&m.qfull[slot], (it / TQ) & 1);
-    const uint32_t t = *reinterpret_cast<volatile uint32_t *>(&m.tile_q[slot]);
-    __syncwarp(__activemask());                      // the producer calls this from one lane
-    if (release) mbar_arrive_cl(qempty0 + slot * 8);
-    return t;
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (uint32_t it = 0;; ++it) {
-        uint32_t t;
-        if (leader) {
-          const uint32_t slot = it % TQ;
-          mbar_wait_cl(&m.qempty[slot], ((it / TQ) & 1) ^ 1);
-          t = atomicAdd(a.tile_ctr, 1u);
-          if (t >= ntiles) t = NO_TILE;
-          m.tile_q[slot] = t;
-          st_cl_u32(mapa(smem_u32(&m.tile_q[slot]), 1), t);
-          mbar_arrive(&m.qfull[slot]);
-          mbar_arrive_cl(mapa(smem_u32(&m.qfull[slot]), 1));
-          mbar_arrive_cl(qempty0 + slot * 8);          // the leader's producer is a ring consumer too
-        } else {
-          t = take(it, true);
-        }
-        if (t == NO_TILE) break;
-        const Tile x = tile_of(t, mt, n1, n2, L);
-        const uint32_t m0 = x.m * 2 * BM + rank * BM;
-        const uint32_t b0row = x.j * BN + rank * (BN / 2);
-        if (x.kind == 1) {
-          wait_phase1(a.done1 + x.m, target);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
-        for (uint32_t kc = 0; kc < KC; ++kc) {
-          mbar_wait(&m.empty[stage], phase ^ 1);
-          if (a.diag == 2) {
-            mbar_arrive(&m.full[stage]);
-            if (++stage == STP) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          // each CTA's TMA signals its own full barrier; the peer's landing is
-          // forwarded to the leader by the peer's warp 1
-          uint64_t *fb = &m.full[stage];
-          mbar_expect_tx(fb, A_BYTES + BP_BYTES);
-          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
-          if (x.kind == 0) {
-            tma_load_2d(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
-            tma_load_2d(dB, &map_w1h, fb, (int)(kc * BK), (int)b0row);
-          } else {
-            if (kc < kx) tma_load_2d(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
-            else tma_load_2d(dA, &map_rh, fb, (int)((kc - kx) * BK), (int)m0);
-            tma_load_2d(dB, &map_w2h, fb, (int)(kc * BK), (int)b0row);
-          }
-          if (++stage == STP) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (leader) {
-      uint32_t stage = 0, phase = 0;
-      const uint32_t id = idesc_bf16(2 * BM, BN);
-      for (uint32_t it = 0;; ++it) {
-        const uint32_t slot = it % TQ;                  // the leader MMA lane reads its own ring
-        mbar_wait(&m.qfull[slot], (it / TQ) & 1);
-        const uint32_t t = *reinterpret_cast<volatile uint32_t *>(&m.tile_q[slot]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cl(qempty0 + slot * 8);
-        if (t == NO_TILE) break;
-        const uint32_t acc = it & 1;
-        mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t tm = tmem_base + acc * BN;
-        for (uint32_t kc = 0; kc < KC; ++kc) {
-          mbar_wait_cl(&m.full[stage], phase);
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              if (a.diag != 1) umma_bf16_pair(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
-            umma_commit_pair(&m.empty[stage]);
-            if (kc == KC - 1) umma_commit_pair(&m.tfull[acc]);
-          }
-          __syncwarp();
-          if (++stage == STP) { stage = 0; phase ^= 1; }
-        }
-      }
-    } else {
-      // the peer's warp 1 forwards "this CTA's half of the stage has landed"
-      // to the leader's full barrier (second arrival), tile by tile
-      uint32_t stage = 0, phase = 0;
-      for (uint32_t it = 0;; ++it) {
-        if (take(it, lane == 0) == NO_TILE) break;
-        for (uint32_t kc = 0; kc < KC; ++kc) {
-          mbar_wait(&m.full[stage], phase);
-          if (lane == 0) mbar_arrive_cl(full0 + stage * 8);
-          __syncwarp();
-          if (++stage == STP) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else {
-    const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int r_in = q * 32 + lane;
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t t = take(it, lane == 0);
-      if (t == NO_TILE) break;
-      const Tile x = tile_of(t, mt, n1, n2, L);
-      const uint32_t acc = it & 1;
-      mbar_wait(&m.tfull[acc], (it >> 1) & 1);
-      tc_fence_after();
-      const uint32_t row = x.m * 2 * BM + rank * BM + r_in;
-      const bool valid = row < Q;
-      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
-      if (x.kind == 0) {
-        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(a.done1 + x.m, 1u);
-        }
-      } else {
-        wait_phase1(a.done1 + x.m, target);
-        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem_base, TMEM_COLS);
-  }
-}
-
-// =============================================================== multicast variant
-// Cluster of 2 CTAs on two M-tiles with the SAME weight tile: each CTA runs its
-// own one-CTA MMAs (M = 128, N = 256) but TMA-loads only half of the B chunk
-// and multicasts it into both CTAs' shared memory, so each SM pulls 32 KB per
-// K-chunk from L2 instead of 48 KB.  A stage is refilled only after both CTAs'
-// MMAs released it (commit multicast to both empty barriers).
-__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap *map, uint64_t *bar,
-                                               int c0, int c1, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit_mc(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   smem_u32(bar)), "h"((uint16_t)3)
-               : "memory");
-}
-
-__global__ void __launch_bounds__(THREADS, 1)
-    k_gru_tc_mc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1h,
-                const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2h,
-                TcArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const Smem m = carve(smem_raw);                      // 4 stages x (16 KB A + 32 KB B)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
-  const uint32_t n1 = a.nub, n2 = a.H / BN;
-  const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
-  const uint32_t target = n1 * 2 * EPI_WARPS;           // phase-1 arrivals per 256-row pair tile
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) { mbar_init(&m.full[s], 1); mbar_init(&m.empty[s], 2); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&m.tfull[s], 1); mbar_init(&m.tempty[s], EPI_WARPS); }
-    for (int s = 0; s < TQ; ++s) { mbar_init(&m.qfull[s], 1); mbar_init(&m.qempty[s], 2 * (2 + EPI_WARPS)); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    prefetch_map(&map_a1); prefetch_map(&map_w1h); prefetch_map(&map_rh); prefetch_map(&map_w2h);
-  }
-  if (warp == 1) tmem_alloc(m.tmem_base, TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  cluster_sync();
-  pdl_entry();
-  const uint32_t Q = a.counts[1];
-  const uint32_t mt = (Q + 2 * BM - 1) / (2 * BM);
-  const uint32_t L = mt < a.lag / 2 ? mt : a.lag / 2;
-  const uint32_t ntiles = mt * (n1 + n2);
-  const uint32_t tmem_base = *m.tmem_base;
-  const uint32_t qempty0 = mapa(smem_u32(&m.qempty[0]), 0);
+  // tile id of ring slot `it`; one lane releases the slot on the leader's qempty
   auto take = [&](uint32_t it, bool release) -> uint32_t {
     const uint32_t slot = it % TQ;
     mbar_wait_cl(&m.qfull[slot], (it / TQ) & 1);
@@ -1112,6 +953,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      unsigned long long w_empty = 0, w_dep = 0, t0;
       for (uint32_t it = 0;; ++it) {
         uint32_t t;
         if (leader) {
@@ -1123,7 +965,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           st_cl_u32(mapa(smem_u32(&m.tile_q[slot]), 1), t);
           mbar_arrive(&m.qfull[slot]);
           mbar_arrive_cl(mapa(smem_u32(&m.qfull[slot]), 1));
-          mbar_arrive_cl(qempty0 + slot * 8);
         } else {
           t = take(it, true);
         }
@@ -1131,90 +972,135 @@ __global__ void __launch_bounds__(THREADS, 1)
         const Tile x = tile_of(t, mt, n1, n2, L);
         const uint32_t m0 = x.m * 2 * BM + rank * BM;
         const uint32_t b0row = x.j * BN + rank * (BN / 2);
-        if (x.kind == 1) {
+        if (x.kind == 1 && a.diag != 4) {
+          t0 = clock64();
           wait_phase1(a.done1 + x.m, target);
+          w_dep += clock64() - t0;
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
+        if (prof) prof[9 + x.kind] += 1;
         for (uint32_t kc = 0; kc < KC; ++kc) {
+          t0 = clock64();
           mbar_wait(&m.empty[stage], phase ^ 1);
-          mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
-          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES);
-          const uint32_t dB = smem_u32(m.sB + stage * B_BYTES) + rank * BP_BYTES;
-          const CUtensorMap *mb = x.kind == 0 ? &map_w1h : &map_w2h;
-          if (x.kind == 1 && kc >= kx) tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BK), (int)m0);
-          else tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BK), (int)m0);
-          tma_load_2d_mc(dB, mb, &m.full[stage], (int)(kc * BK), (int)b0row, (uint16_t)3);
-          if (++stage == ST) { stage = 0; phase ^= 1; }
+          w_empty += clock64() - t0;
+          if (a.diag == 2 || a.diag == 6) {
+            if (leader) mbar_arrive(&m.full[stage]);
+            if (++stage == STP) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          if (leader) mbar_expect_tx(&m.full[stage], 2 * (A_BYTES + BP_BYTES));
+          const uint32_t fb = full0 + stage * 8;
+          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
+          if (x.kind == 0) {
+            tma_load_2d_pair(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
+            tma_load_2d_pair(dB, &map_w1h, fb, (int)(kc * BK), (int)b0row);
+          } else {
+            if (kc < kx) tma_load_2d_pair(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
+            else tma_load_2d_pair(dA, &map_rh, fb, (int)((kc - kx) * BK), (int)m0);
+            tma_load_2d_pair(dB, &map_w2h, fb, (int)(kc * BK), (int)b0row);
+          }
+          if (++stage == STP) { stage = 0; phase ^= 1; }
         }
       }
+      if (prof) { prof[0] = w_empty; prof[1] = w_dep; }
     }
   } else if (warp == 1) {
-    uint32_t stage = 0, phase = 0;
-    const uint32_t id = idesc_bf16(BM, BN);
-    for (uint32_t it = 0;; ++it) {
-      if (take(it, lane == 0) == NO_TILE) break;
-      const uint32_t acc = it & 1;
-      mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t tm = tmem_base + acc * BN;
-      for (uint32_t kc = 0; kc < KC; ++kc) {
-        mbar_wait(&m.full[stage], phase);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
-          umma_commit_mc(&m.empty[stage]);
-          if (kc == KC - 1) umma_commit(&m.tfull[acc]);
-        }
+    if (leader) {
+      uint32_t stage = 0, phase = 0;
+      const uint32_t id = idesc_bf16(2 * BM, BN);
+      unsigned long long w_full = 0, w_tempty = 0, t0;
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t slot = it % TQ;                  // the leader MMA lane reads its own ring
+        mbar_wait(&m.qfull[slot], (it / TQ) & 1);
+        const uint32_t t = *reinterpret_cast<volatile uint32_t *>(&m.tile_q[slot]);
         __syncwarp();
-        if (++stage == ST) { stage = 0; phase ^= 1; }
+        if (lane == 0) mbar_arrive_cl(qempty0 + slot * 8);
+        if (t == NO_TILE) break;
+        const uint32_t acc = it & 1;
+        t0 = clock64();
+        mbar_wait_cl(&m.tempty[acc], ((it >> 1) & 1) ^ 1);   // arrivals from both CTAs
+        w_tempty += clock64() - t0;
+        tc_fence_after();
+        const uint32_t tm = tmem_base + acc * BN;
+        for (uint32_t kc = 0; kc < KC; ++kc) {
+          t0 = clock64();
+          mbar_wait_cl(&m.full[stage], phase);            // both CTAs' bytes landed
+          w_full += clock64() - t0;
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
+            if (a.diag != 1 && a.diag != 6)
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                umma_bf16_pair(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+            umma_commit_pair(&m.empty[stage]);
+            if (kc == KC - 1) umma_commit_pair(&m.tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == STP) { stage = 0; phase ^= 1; }
+        }
       }
+      if (prof && lane == 0) { prof[2] = w_full; prof[3] = w_tempty; }
     }
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r_in = q * 32 + lane;
+    uint8_t *stg = m.stg + (warp - 2) * STG_BYTES;
+    unsigned long long w_tfull = 0, b1 = 0, b2 = 0, t0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t t = take(it, lane == 0);
       if (t == NO_TILE) break;
       const Tile x = tile_of(t, mt, n1, n2, L);
       const uint32_t acc = it & 1;
+      t0 = clock64();
       mbar_wait(&m.tfull[acc], (it >> 1) & 1);
+      w_tfull += clock64() - t0;
+      t0 = clock64();
       tc_fence_after();
       const uint32_t row = x.m * 2 * BM + rank * BM + r_in;
       const bool valid = row < Q;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
+      if (a.diag == 3 || a.diag == 4) {                   // timing only: no epilogue work
+        float v[16];
+        tmem_ld16(tbase, v);
+        tmem_ld_wait();
+      } else if (x.kind == 0) {
+        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j, stg, lane);
+      } else {
+        wait_phase1(a.done1 + x.m, target);
+        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), stg, lane);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
       if (x.kind == 0) {
-        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&m.tempty[acc]);
+        // publish this warp's z / r.h columns to the phase-2 tiles of the pair tile
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
           __threadfence();
           atomicAdd(a.done1 + x.m, 1u);
         }
+        b1 += clock64() - t0;
       } else {
-        wait_phase1(a.done1 + x.m, target);
-        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&m.tempty[acc]);
+        b2 += clock64() - t0;
       }
     }
+    if (prof && lane == 0 && (warp == 2 || warp == 6)) {
+      const int o = warp == 2 ? 4 : 11;
+      prof[o] = w_tfull; prof[o + 1] = b1; prof[o + 2] = b2;
+    }
   }
+  if (prof && threadIdx.x == 0) prof[8] = clock64() - k_t0;
   tc_fence_before();
   __syncthreads();
   cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc_pair(tmem_base, TMEM_COLS);
   }
 }
-
 constexpr size_t SMEM_PAIR = 1024 + STP * (A_BYTES + BP_BYTES) + EPI_WARPS * STG_BYTES + 256;
 
 constexpr size_t SMEM = 1024 + ST * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 256;
@@ -1230,8 +1116,9 @@ struct TcState {
   bool tf32 = false;               // operands fp32 read as TF32 (else bf16)
   void *w1 = nullptr, *w2 = nullptr, *rh = nullptr, *a1 = nullptr;
   uint32_t *done1 = nullptr;
-  int pair = 0;                    // 0: one-CTA kernel; 1: cta_group::2 pair; 2: B multicast in a cluster of 2 (RNNLM_TC_PAIR)
-  uint32_t diag = 0;               // RNNLM_TC_DIAG: timing diagnostics, results invalid (1 no MMA, 2 no TMA)
+  int pair = 0;                    // 0: one-CTA kernel; 1: cta_group::2 pair (RNNLM_TC_PAIR)
+  uint32_t diag = 0;               // RNNLM_TC_DIAG: timing diagnostics (see TcArgs::diag)
+  unsigned long long *prof = nullptr;
   float *bzr = nullptr, *bh = nullptr;
   CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h;
   bool bound = false;
@@ -1339,7 +1226,6 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, voi
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PAIR) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   *state_out = t;
   if (!ok) {
     (void)cudaGetLastError();
@@ -1371,6 +1257,7 @@ void gru_tc_release(void *state) {
   cudaFree(t->w2);
   cudaFree(t->a1);
   cudaFree(t->done1);
+  cudaFree(t->prof);
   cudaFree(t->bzr);
   cudaFree(t->bh);
   delete t;
@@ -1393,6 +1280,12 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.tile_ctr = t->done1 + (t->bmax / BM + 2);
   a.lag = 48;
   a.diag = t->diag;
+  a.prof = nullptr;
+  if (t->diag == 5) {
+    if (!t->prof) cudaMalloc(&t->prof, 1024 * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(t->prof, 0, 1024 * 16 * sizeof(unsigned long long), s);
+    a.prof = t->prof;
+  }
   const uint32_t mt = (max_rows + BM - 1) / BM;
   uint32_t g1 = mt * (t->nub + P.H / BN);
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
@@ -1405,17 +1298,36 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / BN) * 2;
     const uint32_t cap = (uint32_t)num_sms & ~1u;
     if (gp > cap) gp = cap;
-    if (t->pair == 1)
-      launch_pdl_cluster(k_gru_tc2, gp, THREADS, SMEM_PAIR, s, 2, t->map_a1, t->map_w1h, t->map_rh,
-                         t->map_w2h, a);
-    else
-      launch_pdl_cluster(k_gru_tc_mc, gp, THREADS, SMEM, s, 2, t->map_a1, t->map_w1h, t->map_rh,
-                         t->map_w2h, a);
+    launch_pdl_cluster(k_gru_tc2, gp, THREADS, SMEM_PAIR, s, 2, t->map_a1, t->map_w1h, t->map_rh,
+                       t->map_w2h, a);
   } else {
     if (t->tf32) launch_pdl(k_gru_tc<float>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
     else launch_pdl(k_gru_tc<__nv_bfloat16>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
   }
   if (ev_phase1) cudaEventRecord(ev_phase1, s);
+  if (a.prof) {
+    // diag 5: per-CTA cycle counters, averaged over the CTAs, to stderr
+    std::vector<unsigned long long> h(1024 * 16);
+    cudaMemcpyAsync(h.data(), t->prof, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    int nb = 0;
+    double sum[16] = {0};
+    for (int b = 0; b < 1024; ++b) {
+      if (!h[b * 16 + 8]) continue;
+      ++nb;
+      for (int k = 0; k < 16; ++k) sum[k] += (double)h[b * 16 + k];
+    }
+    if (nb) {
+      static const char *nm[16] = {"prod_wait_empty", "prod_wait_dep", "mma_wait_full", "mma_wait_tempty",
+                                   "epi_z_wait_tfull", "epi_z_body_p1", "epi_z_body_p2", "-", "total",
+                                   "tiles_p1", "tiles_p2", "epi_r_wait_tfull", "epi_r_body_p1", "epi_r_body_p2",
+                                   "-", "-"};
+      fprintf(stderr, "[gru_tc prof] pair=%d ctas=%d", t->pair, nb);
+      for (int k = 0; k < 14; ++k)
+        if (nm[k][0] != '-') fprintf(stderr, " %s=%.0f", nm[k], sum[k] / nb);
+      fprintf(stderr, "\n");
+    }
+  }
   return 2;
 }
 }  // namespace rnnlm_host
