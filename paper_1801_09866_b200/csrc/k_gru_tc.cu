@@ -283,6 +283,10 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
 
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
+// Register cap of the fused kernels: three of its warps share an SM sub-partition,
+// and 3 x 152 x 32 registers leave room for one warp of k_score (48 registers)
+// per sub-partition, so the side-stream scoring runs beside the GRU.
+#define GRU_MAXREG 152
 
 constexpr int TQ = 4;            // depth of the tile-id ring (producer -> MMA / epilogue)
 constexpr uint32_t NO_TILE = 0xFFFFFFFFu;
@@ -671,7 +675,7 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
 // warp 1: TMEM allocation + MMA issue; warps 2-9: epilogue, TMEM lane quarter
 // = warp % 4, column half = (warp - 2) / 4.
 template <typename T>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __maxnreg__(GRU_MAXREG)
     k_gru_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1,
              const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2,
              TcArgs a) {
@@ -901,7 +905,7 @@ __device__ __forceinline__ SmemP carve_pair(uint8_t *raw) {
 // (cp.async.bulk.tensor .cta_group::2), which the leader arms with the bytes
 // of both halves; the MMA commit releases the stage in both CTAs at once
 // (multicast), so no CTA-to-CTA handshake sits on the K loop.
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __maxnreg__(GRU_MAXREG)
     k_gru_tc2(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1h,
               const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2h,
               TcArgs a) {

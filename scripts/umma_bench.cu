@@ -110,10 +110,10 @@ __device__ __forceinline__ void commit(uint32_t bar) {
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-template <int PAIR, int ST>
+template <int PAIR, int ST, bool G = false>
 __global__ void __launch_bounds__(192, 1)
     kbench(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
-           int K, float *out) {
+           int K, float *out, const int *gidx = nullptr) {
   constexpr int BH = BN / PAIR;                // B rows this CTA loads
   constexpr int B_BYTES = BH * BK * 2;
   extern __shared__ __align__(1024) uint8_t raw[];
@@ -150,7 +150,29 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t full_l = PAIR == 2 ? mapa(su32(full), 0) : su32(full);
   const uint32_t tempty_l = PAIR == 2 ? mapa(su32(tempty), 0) : su32(tempty);
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && G) {
+    // gathered A: lane l issues the tile::gather4 of rows 4l..4l+3 of every stage
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int t = unit; t < ntiles; t += nunits) {
+      const int m = t / nt, j = t % nt;
+      const int m0 = m * BM, n0 = j * BN;
+      const int4 r = *reinterpret_cast<const int4 *>(gidx + m0 + 4 * lane);
+      for (int kc = 0; kc < KC; ++kc) {
+        if (lane == 0) {
+          mbar_wait(su32(&empty[stage]), ph ^ 1);
+          mbar_expect_tx(su32(&full[stage]), A_BYTES + B_BYTES);
+        }
+        __syncwarp();
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(su32(sA + stage * A_BYTES) + 512 * lane),
+            "l"((uint64_t)&mapA), "r"(full_l + stage * 8), "r"(kc * BK), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w)
+            : "memory");
+        if (lane == 0) tma2d<PAIR>(su32(sB + stage * B_BYTES), &mapB, full_l + stage * 8, kc * BK, n0);
+        if (++stage == ST) { stage = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 0 && lane == 0) {
     int stage = 0;
     uint32_t ph = 0;
     for (int t = unit; t < ntiles; t += nunits) {
@@ -250,14 +272,16 @@ static void make_map(CUtensorMap *m, void *base, uint64_t inner, uint64_t outer,
   }
 }
 
-template <int PAIR, int ST>
+template <int PAIR, int ST, bool G = false>
 static void run(const char *name, int M, int N, int K, __nv_bfloat16 *dA, __nv_bfloat16 *dB, float *dout,
-                const std::vector<float> &hA, const std::vector<float> &hB, int nsm) {
+                const std::vector<float> &hA, const std::vector<float> &hB, int nsm, const int *gidx = nullptr,
+                int table_rows = 0, const std::vector<int> *hidx = nullptr) {
   CUtensorMap mA, mB;
-  make_map(&mA, dA, K, M, BM);
+  if (G) make_map(&mA, dA, K, table_rows, 1);
+  else make_map(&mA, dA, K, M, BM);
   make_map(&mB, dB, K, N, BN / PAIR);
   const size_t smem = 1024 + ST * (A_BYTES + (BN / PAIR) * BK * 2) + 256;
-  CK(cudaFuncSetAttribute(kbench<PAIR, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(kbench<PAIR, ST, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = PAIR;
@@ -270,14 +294,14 @@ static void run(const char *name, int M, int N, int K, __nv_bfloat16 *dA, __nv_b
   cfg.attrs = at;
   cfg.numAttrs = 1;
   CK(cudaMemset(dout, 0, (size_t)M * (N / BN) * 4));
-  for (int i = 0; i < 3; ++i) CK(cudaLaunchKernelEx(&cfg, kbench<PAIR, ST>, mA, mB, M, N, K, dout));
+  for (int i = 0; i < 3; ++i) CK(cudaLaunchKernelEx(&cfg, kbench<PAIR, ST, G>, mA, mB, M, N, K, dout, gidx));
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int R = 20;
   cudaEventRecord(e0);
-  for (int i = 0; i < R; ++i) CK(cudaLaunchKernelEx(&cfg, kbench<PAIR, ST>, mA, mB, M, N, K, dout));
+  for (int i = 0; i < R; ++i) CK(cudaLaunchKernelEx(&cfg, kbench<PAIR, ST, G>, mA, mB, M, N, K, dout, gidx));
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms = 0;
@@ -290,7 +314,10 @@ static void run(const char *name, int M, int N, int K, __nv_bfloat16 *dA, __nv_b
     const int row = (int)(((long long)s * 7919) % M), j = s % (N / BN);
     double ref = 0;
     for (int n = j * BN; n < j * BN + BN; ++n)
-      for (int k = 0; k < K; ++k) ref += (double)hA[(size_t)row * K + k] * hB[(size_t)n * K + k];
+      for (int k = 0; k < K; ++k) {
+        const size_t ar = G ? (size_t)(*hidx)[row] : (size_t)row;
+        ref += (double)hA[ar * K + k] * hB[(size_t)n * K + k];
+      }
     maxerr = fmax(maxerr, fabs(ref - out[(size_t)row * (N / BN) + j]));
   }
   const double tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12;
@@ -320,6 +347,15 @@ int main(int argc, char **argv) {
   CK(cudaMemcpy(dA, bA.data(), bA.size() * 2, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, bB.data(), bB.size() * 2, cudaMemcpyHostToDevice));
   run<1, 4>("one-cta st4", M, N, K, dA, dB, dout, hA, hB, nsm);
+  {
+    // gathered A: M random rows of the same A table (indices a permutation-free random draw)
+    std::vector<int> idx(M);
+    for (int i = 0; i < M; ++i) idx[i] = (int)(((unsigned long long)i * 2654435761ull + 12345) % (unsigned long long)M);
+    int *didx;
+    CK(cudaMalloc(&didx, M * 4));
+    CK(cudaMemcpy(didx, idx.data(), M * 4, cudaMemcpyHostToDevice));
+    run<1, 4, true>("one-cta st4 gather4-A", M, N, K, dA, dB, dout, hA, hB, nsm, didx, M, &idx);
+  }
   run<2, 4>("pair st4", M, N, K, dA, dB, dout, hA, hB, nsm);
   run<2, 6>("pair st6", M, N, K, dA, dB, dout, hA, hB, nsm);
   return 0;
