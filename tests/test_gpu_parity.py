@@ -255,6 +255,35 @@ def test_moderate_bf16_tensor_core(mode):
     assert rep["miss"] > 300
 
 
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_moderate_bf16_round_codes(k):
+    """round:k keys (int8 codes for k <= 2, int16 for k = 3) are encoded inside
+    the tcgen05 phase-2 epilogue; codes bit-exact vs the oracle's compress() of
+    the same GPU vector, lossy hidden-cache hits identical (replay protocol)."""
+    d, m = model("moderate")
+    wl = generate_workload(1, 40, 256, d.V, seed=19)
+    eng, orc = pair(d, m, wl, KEY_ROUND, k=k, math=MATH_BF16)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_BF16], tol_state=TOL[MATH_BF16])
+    assert rep["miss"] > 300
+
+
+@pytest.mark.parametrize("shape", ["full", "ragged_multisession"])
+def test_bf16_cta_pair_kernel(shape, monkeypatch):
+    """The CTA-pair variant (cta_group::2, M = 256; RNNLM_TC_PAIR=1) against the
+    oracle: full 256-row pair tiles and a ragged multi-session batch."""
+    monkeypatch.setenv("RNNLM_TC_PAIR", "1")
+    d, m = model("large")
+    if shape == "full":
+        wl = generate_workload(1, 2, 2048, d.V, seed=5)
+        eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16, cache=False)
+        rep = replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+        assert rep["miss"] == wl.n_total
+    else:
+        wl = generate_workload(3, 3, 300, d.V, seed=6)
+        eng, orc = pair(d, m, wl, KEY_ROUND, k=2, math=MATH_BF16)
+        replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+
+
 def test_large_bf16_cache_off_full_tiles():
     """All-miss stress: 2,048 GRU rows per frame = 16 full M-tiles + ragged frames."""
     d, m = model("large")
