@@ -98,6 +98,12 @@ def lib():
         L.orc_read_ctx.restype = ctypes.c_int
         L.orc_read_ctx.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, _u32p, _u32p,
                                    _u32p]
+        L.orc_log_normalizer.restype = ctypes.c_double
+        L.orc_log_normalizer.argtypes = [ctypes.POINTER(OrcConfig), ctypes.POINTER(OrcWeights), _f32p,
+                                         _u32p, ctypes.c_uint32]
+        L.orc_log_normalizer_handles.restype = ctypes.c_int
+        L.orc_log_normalizer_handles.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32,
+                                                 _u32p, _f64p]
         L.orc_overwrite_state.restype = ctypes.c_int
         L.orc_overwrite_state.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, _f32p]
         _lib = L
@@ -170,6 +176,15 @@ def score(cfg: OrcConfig, weights: dict, h, ctx, w: int) -> float:
                                  _p(c, _u32p), len(ctx), w))
 
 
+def log_normalizer(cfg: OrcConfig, weights: dict, h, ctx) -> float:
+    """Exact log sum_v exp(score_v) (fp64) for state h and context (most recent LAST)."""
+    W = _Weights(weights)
+    h = _f32(h)
+    c = _u32(ctx if len(ctx) else [0])
+    return float(lib().orc_log_normalizer(ctypes.byref(cfg), ctypes.byref(W.c), _p(h, _f32p),
+                                          _p(c, _u32p), len(ctx)))
+
+
 class Oracle:
     """One oracle engine over ``num_sessions`` utterance streams."""
 
@@ -231,6 +246,12 @@ class Oracle:
         ln = np.zeros(len(h), dtype=np.uint32)
         lib().orc_read_ctx(self._h, s, len(h), _p(h, _u32p), _p(ctx, _u32p), _p(ln, _u32p))
         return [list(ctx[i, :ln[i]]) for i in range(len(h))]
+
+    def log_normalizer(self, s: int, handles):
+        h = _u32(handles)
+        out = np.zeros(len(h), dtype=np.float64)
+        assert lib().orc_log_normalizer_handles(self._h, s, len(h), _p(h, _u32p), _p(out, _f64p)) == 0
+        return out
 
     def overwrite_state(self, s: int, handle: int, h):
         h = _f32(h)

@@ -172,6 +172,35 @@ float orc_score(const orc_config *cfg, const orc_weights *wt, const float *h,
   return (float)acc;
 }
 
+// Exact log-normaliser of the combined score over the whole vocabulary: the
+// normalisation NCE avoids at run time ("they need to be normalized over
+// different word sequences ... a highly computationally intensive task",
+// P:73-74; SPEC exact_log_prob S:201-209).
+//   log Z(h, ctx) = log sum_{v < V} exp(s_v),
+//   s_v = Theta_v . h + b_v + sum_k maxent[idx_k(ctx, v)]
+// i.e. orc_score's sum for every word v, kept in fp64 (no fp32 rounding),
+// then max-subtraction: log Z = m + log sum_v exp(s_v - m), m = max_v s_v,
+// words in ascending order.
+double orc_log_normalizer(const orc_config *cfg, const orc_weights *wt, const float *h,
+                          const uint32_t *ctx, uint32_t ctx_len) {
+  const uint32_t H = cfg->H, V = cfg->V;
+  std::vector<double> s(V);
+  uint64_t idx[16];
+  for (uint32_t v = 0; v < V; ++v) {
+    double acc = 0.0;
+    for (uint32_t i = 0; i < H; ++i) acc += (double)wt->nce_w[(size_t)v * H + i] * (double)h[i];
+    acc += (double)wt->nce_b[v];
+    const uint32_t K = orc_maxent_indices(ctx, ctx_len, v, cfg->N, 1ull << cfg->maxent_log2, idx);
+    for (uint32_t k = 0; k < K; ++k) acc += (double)wt->maxent[idx[k]];
+    s[v] = acc;
+  }
+  double m = -INFINITY;
+  for (uint32_t v = 0; v < V; ++v) m = s[v] > m ? s[v] : m;
+  double z = 0.0;
+  for (uint32_t v = 0; v < V; ++v) z += std::exp(s[v] - m);
+  return m + std::log(z);
+}
+
 static int check_finite(const float *p, size_t n) {
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) return 0;
@@ -384,6 +413,23 @@ int orc_read_ctx(orc_t *o, uint32_t s, uint32_t n, const uint32_t *handles, uint
     const Record &r = S.rec[handles[i]];
     ctx_len[i] = (uint32_t)r.ctx.size();
     for (size_t j = 0; j < r.ctx.size(); ++j) ctx7[7 * i + j] = r.ctx[j];
+  }
+  return ORC_OK;
+}
+
+// log Z of each history handle of session s (its stored state and context);
+// NaN for a handle that does not exist.
+int orc_log_normalizer_handles(orc_t *o, uint32_t s, uint32_t n, const uint32_t *handles, double *out) {
+  if (!o || s >= o->cfg.num_sessions) return ORC_E_INVALID_ARG;
+  const Session &S = o->sess[s];
+  for (uint32_t i = 0; i < n; ++i) {
+    if (handles[i] >= S.rec.size()) {
+      out[i] = NAN;
+      continue;
+    }
+    const Record &r = S.rec[handles[i]];
+    out[i] = orc_log_normalizer(&o->cfg, &o->w, S.state[r.slot].data(), r.ctx.data(),
+                                (uint32_t)r.ctx.size());
   }
   return ORC_OK;
 }

@@ -75,6 +75,11 @@ int orc_read_ctx(orc_t *o, uint32_t s, uint32_t n, const uint32_t *handles, uint
                  uint32_t *ctx_len);
 /* Replay protocol: overwrite the state owned by handle's slot. */
 int orc_overwrite_state(orc_t *o, uint32_t s, uint32_t handle, const float *h);
+/* Exact log-normaliser log sum_v exp(score_v) over the vocabulary, fp64
+ * (S:201-209), of a state + context, or of stored handles. */
+double orc_log_normalizer(const orc_config *cfg, const orc_weights *wt, const float *h,
+                          const uint32_t *ctx, uint32_t ctx_len);
+int orc_log_normalizer_handles(orc_t *o, uint32_t s, uint32_t n, const uint32_t *handles, double *out);
 
 #ifdef __cplusplus
 }

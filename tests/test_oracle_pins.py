@@ -238,3 +238,73 @@ def test_gru_bounded_state_S129():
             h64 = O.gru(cfg, m, rng.uniform(-1, 1, 6).astype(np.float32), h, fp64=True)
             assert np.all(np.abs(h64) < 1.0)
             h = h64.astype(np.float32)
+
+
+# ----------------------------------------------------------------------------- exact log-normaliser (8(f)-2)
+def test_log_normalizer_two_equal_words_S206():
+    # V=2 with equal scores -> log p = log 0.5 for each word, so
+    # log Z = s + ln 2.  Scores set through the bias only (Theta = 0, MaxEnt = 0).
+    d, m = _score_model(2, 2, 10)
+    m["nce_b"][:] = 0.375
+    cfg = O.make_config(2, 1, 2, 10, 2)
+    assert O.log_normalizer(cfg, m, [0.3, -0.8], [5]) == pytest.approx(0.375 + math.log(2), abs=1e-12)
+
+
+def test_log_normalizer_hand_softmax_S208():
+    # V=3, combined scores (0, 0, ln 2) -> probabilities (1/4, 1/4, 1/2),
+    # i.e. Z = 4.  The third score is ln 2 rounded to fp32 (b_nce is fp32).
+    d, m = _score_model(2, 3, 10)
+    m["nce_b"][2] = np.float32(math.log(2))
+    cfg = O.make_config(3, 1, 2, 10, 2)
+    lz = O.log_normalizer(cfg, m, [0.0, 0.0], [])
+    assert lz == pytest.approx(math.log(2 + math.exp(float(np.float32(math.log(2))))), abs=1e-12)
+    assert lz == pytest.approx(math.log(4), abs=1e-7)
+    assert math.exp(float(np.float32(math.log(2))) - lz) == pytest.approx(0.5, abs=1e-7)
+
+
+def test_log_normalizer_zero_model_is_log_V():
+    # every score 0 -> Z = V exactly
+    d, m = _score_model(4, 1000, 12)
+    cfg = O.make_config(1000, 1, 4, 12, 2)
+    assert O.log_normalizer(cfg, m, [0.5, -0.5, 0.25, 1.0], [17]) == pytest.approx(math.log(1000), abs=1e-12)
+
+
+def test_log_normalizer_single_feature_closed_form():
+    # one order-2 MaxEnt weight c at idx_2(ctx=[7], w=42) (M = 1024, N = 2), all
+    # else zero: only word 42 hits it (unigram slots of other words are 0 and
+    # no other word's order-2 index collides with 382 -- checked), so
+    # Z = (V - 1) + e^c.
+    d, m = _score_model(2, 64, 10)
+    c = 1.5
+    m["maxent"][382] = c
+    hits = [v for v in range(64) if 382 in O.maxent_indices([7], v, 2, 1024)]
+    assert hits == [42]
+    cfg = O.make_config(64, 1, 2, 10, 2)
+    assert O.log_normalizer(cfg, m, [0.1, 0.2], [7]) == pytest.approx(math.log(63 + math.exp(c)), abs=1e-12)
+
+
+def test_log_normalizer_sums_to_one_S218():
+    # the exact distribution sums to 1 (random models, V <= 1000);
+    # per-word scores from the pinned orc_score (fp32-rounded, so ~1e-7 each).
+    d = ModelDims(V=300, E=4, H=16, maxent_log2=12, N=4)
+    m = generate_model(d, seed=9, scale=1.0)
+    cfg = O.make_config(300, 4, 16, 12, 4)
+    rng = np.random.default_rng(2)
+    h = rng.uniform(-1, 1, 16).astype(np.float32)
+    ctx = [11, 250, 3]
+    lz = O.log_normalizer(cfg, m, h, ctx)
+    p = [math.exp(O.score(cfg, m, h, ctx, v) - lz) for v in range(300)]
+    assert sum(p) == pytest.approx(1.0, abs=1e-5)
+    assert max(O.score(cfg, m, h, ctx, v) for v in range(300)) <= lz
+
+
+def test_log_normalizer_shift_invariance():
+    # adding c to every NCE bias shifts log Z by exactly c (up to fp32 storage of b + c)
+    d = ModelDims(V=64, E=4, H=8, maxent_log2=10, N=3)
+    m = generate_model(d, seed=4, scale=1.0)
+    cfg = O.make_config(64, 4, 8, 10, 3)
+    h = np.linspace(-1, 1, 8).astype(np.float32)
+    base = O.log_normalizer(cfg, m, h, [1, 2])
+    m2 = dict(m)
+    m2["nce_b"] = (m["nce_b"] + np.float32(2.0)).astype(np.float32)
+    assert O.log_normalizer(cfg, m2, h, [1, 2]) == pytest.approx(base + 2.0, abs=1e-6)
