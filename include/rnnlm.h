@@ -183,6 +183,22 @@ rnnlm_status rnnlm_maxent_indices(rnnlm_t *h, uint32_t n, const uint32_t *d_sess
                                   rnnlm_stream_t stream);
 uint32_t rnnlm_code_bytes(const rnnlm_t *h);
 
+/* Exact log-normaliser of n stored histories: the
+ * normalisation over the vocabulary that NCE avoids ("they need to be
+ * normalized ... a highly computationally intensive task considering the
+ * vocabulary size"; SPEC exact_log_prob S:201-209):
+ *   d_log_z[i] = log sum_{v < V} exp(s_v),  s_v = the step-(a6) score of word v
+ *   for history d_history[i] of session d_session[i] (NCE + all MaxEnt orders),
+ * so score - log Z is the exact log-probability.  n <= max_queries_per_call;
+ * d_session, d_history: n u32 (device); d_log_z: n f32 (device), NaN for a
+ * history that does not exist.  Tensor-core contraction in every math mode
+ * (state split into two bf16 halves against bf16 output rows; engines whose
+ * output rows are not bf16-exact use a rounded bf16 copy made at the first
+ * call).  The first call allocates its scratch (synchronous).  Requires
+ * hidden % 64 == 0 (else RNNLM_E_DIMENSION). */
+rnnlm_status rnnlm_log_normalizer(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
+                                  const uint32_t *d_history, float *d_log_z, rnnlm_stream_t stream);
+
 /* Workload plumbing (not part of the method): d_parent[i] = d_ref[i] < 0 ? 0
  * : d_log[d_ref[i]], i.e. map "child of earlier query j" references to the
  * handles the engine returned for those queries. */

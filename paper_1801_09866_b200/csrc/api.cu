@@ -20,6 +20,12 @@ void gru_tc_release(void *state);
 int gru_tc_bind(void *state, void *rh, uint32_t bmax);
 int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s,
                   cudaEvent_t ev_gathered, cudaEvent_t ev_phase1);
+// Exact log-normaliser (k_norm.cu).
+int norm_supported(uint32_t H, uint32_t N);
+int norm_prepare(const Params &P, uint32_t bmax, void **state_out, cudaStream_t s);
+void norm_release(void *state);
+int launch_norm(const Params &P, void *state, uint32_t n, const uint32_t *sess, const uint32_t *hist,
+                float *log_z, int num_sms, cudaStream_t s);
 }  // namespace rnnlm_host
 
 struct rnnlm {
@@ -28,6 +34,7 @@ struct rnnlm {
   int num_sms = 148;
   std::vector<void *> allocs;
   void *tc = nullptr;                 // tensor-core GRU state (descriptors, weights)
+  void *norm = nullptr;               // log-normaliser scratch (first rnnlm_log_normalizer call)
   uint32_t epoch = 0;
   uint64_t launches = 0;
   // scoring + result write run on a side stream, concurrently with the GRU
@@ -109,6 +116,8 @@ rnnlm_status upload_bf16(rnnlm *h, __nv_bfloat16 **dst, const float *src, size_t
 void free_all(rnnlm *h) {
   if (h->tc) rnnlm_host::gru_tc_release(h->tc);
   h->tc = nullptr;
+  if (h->norm) rnnlm_host::norm_release(h->norm);
+  h->norm = nullptr;
   for (void *p : h->allocs) cudaFree(p);
   h->allocs.clear();
   for (auto &v : h->ev_pending)
@@ -465,6 +474,23 @@ rnnlm_status rnnlm_maxent_indices(rnnlm_t *h, uint32_t n, const uint32_t *d_sess
   h->launches += rnnlm_host::launch_maxent_indices(
       h->P, n, d_session, d_parent, d_word, reinterpret_cast<unsigned long long *>(d_idx),
       reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_log_normalizer(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
+                                  const uint32_t *d_history, float *d_log_z, rnnlm_stream_t stream) {
+  if (!h) return RNNLM_E_INVALID_ARG;
+  if (n == 0) return RNNLM_OK;
+  if (n > h->cfg.max_queries_per_call || !d_session || !d_history || !d_log_z) return RNNLM_E_INVALID_ARG;
+  if (!rnnlm_host::norm_supported(h->P.H, h->P.N)) return RNNLM_E_DIMENSION;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!h->norm) {
+    if (rnnlm_host::norm_prepare(h->P, h->cfg.max_queries_per_call, &h->norm, s) != 0) return RNNLM_E_OOM;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  h->launches += (uint64_t)rnnlm_host::launch_norm(h->P, h->norm, n, d_session, d_history, d_log_z,
+                                                   h->num_sms, s);
   return cuda_status(cudaGetLastError());
 }
 

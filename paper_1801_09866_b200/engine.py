@@ -87,6 +87,16 @@ class RNNLM:
                                             _stream(stream)), "rnnlm_query_batch")
         return score, child, outcome
 
+    def log_normalizer(self, session: torch.Tensor, history: torch.Tensor, out: torch.Tensor | None = None,
+                       stream=None) -> torch.Tensor:
+        """Exact log sum_v exp(score_v) of stored histories (rnnlm_log_normalizer)."""
+        n = int(history.numel())
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=self.device)
+        check(_lib.load().rnnlm_log_normalizer(self._h, n, _ptr(session), _ptr(history), _ptr(out),
+                                               _stream(stream)), "rnnlm_log_normalizer")
+        return out
+
     def reset_session(self, session: int = ALL, stream=None):
         check(_lib.load().rnnlm_reset_session(self._h, session, _stream(stream)), "reset_session")
 
