@@ -20,7 +20,7 @@ fi
 if [[ $what == ncu || $what == all ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline "$@" > gpurun_out/ncu_launch_bench.json 2> gpurun_out/ncu_launch.err
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_gru1_tc|k_gru2_tc|k_score|k_qprobe|k_scan' -s 10 -c 5 \
-    -o gpurun_out/prof_full -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline "$@" > gpurun_out/ncu_full.log 2>&1
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_resolve_parents|k_qcache|k_hcache|k_scan|k_commit|k_gather_a1|k_final|k_gru_tc|k_score|k_dup_scores' -s 430 -c 10 \
+    -o gpurun_out/prof_full -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline "$@" > gpurun_out/ncu_full.log 2>&1
 fi
 ls -la gpurun_out
