@@ -407,41 +407,38 @@ def run_ours(args):
 
 
 def run_e2e(args, eng, wl, dev, world):
-    """Host-buffer path: per step H2D of (session, parent, word) from pinned
-    memory, rnnlm_query_batch, D2H of (score, child); parents of the next frame
-    are resolved on the host from the returned handles (as a decoder would)."""
+    """Host-buffer path through the public C ABI: per step H2D of the decoder's
+    queries (session, parent reference = index of the earlier query whose child
+    is the parent, word) from pinned memory, rnnlm_resolve_parents (reference
+    -> handle, on the device, from the children the engine returned),
+    rnnlm_query_batch, D2H of (score, child) into pinned memory, synchronise."""
     import torch
     import torch.distributed as dist
     n = wl.n_per_frame
     eng.reset_session()
-    # the decoder's query stream (session, word) sits in pinned host memory; the
-    # parent handle of each query is looked up from the children returned so far
-    # (child_log[n_total] = 0 is the root sentinel, so one gather resolves all)
+    import paper_1801_09866_b200 as R
     h_sess_all = torch.from_numpy(wl.session.view(np.int32).copy()).pin_memory()
     h_word_all = torch.from_numpy(wl.word.view(np.int32).copy()).pin_memory()
-    ref_idx = np.where(wl.parent_ref >= 0, wl.parent_ref, wl.n_total).astype(np.int64)
-    h_par = torch.empty(n, dtype=torch.int32).pin_memory()
+    h_ref_all = torch.from_numpy(np.ascontiguousarray(wl.parent_ref, dtype=np.int64)).pin_memory()
     h_score = torch.empty(n, dtype=torch.float32).pin_memory()
     h_child = torch.empty(n, dtype=torch.int32).pin_memory()
     d_sess = torch.empty(n, dtype=torch.int32, device=dev)
-    d_par = torch.empty(n, dtype=torch.int32, device=dev)
     d_word = torch.empty(n, dtype=torch.int32, device=dev)
+    d_ref = torch.empty(n, dtype=torch.int64, device=dev)
+    d_par = torch.empty(n, dtype=torch.int32, device=dev)
     d_score = torch.empty(n, dtype=torch.float32, device=dev)
-    d_child = torch.empty(n, dtype=torch.int32, device=dev)
-    child_log = np.zeros(wl.n_total + 1, np.int32)
-    par_np, child_np = h_par.numpy(), h_child.numpy()
+    d_child_log = torch.zeros(wl.n_total, dtype=torch.int32, device=dev)
 
     def host_step(t):
         sl = wl.frame_slice(t)
-        np.take(child_log, ref_idx[sl], out=par_np)
         d_sess.copy_(h_sess_all[sl], non_blocking=True)
-        d_par.copy_(h_par, non_blocking=True)
+        d_ref.copy_(h_ref_all[sl], non_blocking=True)
         d_word.copy_(h_word_all[sl], non_blocking=True)
-        eng.query_batch(d_sess, d_par, d_word, score=d_score, child=d_child, want_outcome=False)
+        R.resolve_parents(d_ref, d_child_log, d_par)
+        eng.query_batch(d_sess, d_par, d_word, score=d_score, child=d_child_log[sl], want_outcome=False)
         h_score.copy_(d_score, non_blocking=True)
-        h_child.copy_(d_child, non_blocking=True)
+        h_child.copy_(d_child_log[sl], non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        child_log[sl] = child_np
 
     F0 = args.prefill
     for t in range(F0 + args.warmup):
@@ -459,8 +456,10 @@ def run_e2e(args, eng, wl, dev, world):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         secs = float(tt[0])
     return {"value": n * args.steps * world / secs, "unit": UNIT,
-            "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 8 * n,
-            "note": "wall clock incl. host-side parent resolution; per rank, max over ranks"}
+            "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n,
+            "note": "wall clock per step: H2D (session u32, parent reference i64, word u32) from pinned "
+                    "memory, device-side reference -> handle resolution, the step, D2H (score, child), "
+                    "synchronise; per rank, max over ranks"}
 
 
 def run_normalizer(args):
