@@ -22,6 +22,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.cpp")
 
 KEY_OFF, KEY_ROUND, KEY_SIGN = 0, 1, 2
+CELL_GRU, CELL_GRU_LBR = 0, 1
 QHIT, SHIT, MISS, INVALID = 0, 1, 2, 255
 ALL_SESSIONS = 0xFFFFFFFF
 
@@ -35,7 +36,7 @@ _u8p = ctypes.POINTER(ctypes.c_uint8)
 class OrcConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in (
         "V", "E", "H", "maxent_log2", "N", "key_mode", "round_digits",
-        "cache_enabled", "num_sessions", "max_histories")]
+        "cache_enabled", "num_sessions", "max_histories", "cell")]
 
 
 class OrcWeights(ctypes.Structure):
@@ -123,9 +124,9 @@ def _u32(a):
 
 
 def make_config(V, E, H, maxent_log2, N, key_mode=KEY_OFF, round_digits=0, cache_enabled=1,
-                num_sessions=1, max_histories=1 << 16) -> OrcConfig:
+                num_sessions=1, max_histories=1 << 16, cell=CELL_GRU) -> OrcConfig:
     return OrcConfig(V, E, H, maxent_log2, N, key_mode, round_digits, cache_enabled,
-                     num_sessions, max_histories)
+                     num_sessions, max_histories, cell)
 
 
 class _Weights:

@@ -308,3 +308,54 @@ def test_log_normalizer_shift_invariance():
     m2 = dict(m)
     m2["nce_b"] = (m["nce_b"] + np.float32(2.0)).astype(np.float32)
     assert O.log_normalizer(cfg, m2, h, [1, 2]) == pytest.approx(base + 2.0, abs=1e-6)
+
+
+# ----------------------------------------------------------------------------- cell variant (8(f)-3)
+def test_gru_lbr_is_torch_grucell():
+    """The linear-before-reset cell IS torch.nn.GRUCell's formulation
+    (n = tanh(W_in x + b_in + r . (W_hn h + b_hn))), for arbitrary reset
+    gates: with b_hn = 0, b_in = bh and the update gate negated (torch uses
+    h' = (1 - z_t) n + z_t h), the library cell is the reference."""
+    E, H = 5, 3
+    rng = np.random.default_rng(8)
+    m = {k: rng.uniform(-1, 1, s).astype(np.float32) for k, s in
+         dict(Wz=(H, E), Uz=(H, H), bz=(H,), Wr=(H, E), Ur=(H, H), br=(H,), Wh=(H, E), Uh=(H, H),
+              bh=(H,)).items()}
+    m.update(emb=np.zeros((2, E), np.float32), nce_w=np.zeros((2, H), np.float32),
+             nce_b=np.zeros(2, np.float32), maxent=np.zeros(2, np.float32))
+    x = rng.uniform(-1, 1, E).astype(np.float32)
+    h = rng.uniform(-1, 1, H).astype(np.float32)
+    cfg = O.make_config(2, E, H, 1, 1, cell=O.CELL_GRU_LBR)
+    ours = O.gru(cfg, m, x, h, fp64=True)
+    cell = torch.nn.GRUCell(E, H).double()
+    t = lambda a: torch.tensor(a, dtype=torch.float64)
+    with torch.no_grad():
+        cell.weight_ih.copy_(torch.cat([t(m["Wr"]), -t(m["Wz"]), t(m["Wh"])]))
+        cell.weight_hh.copy_(torch.cat([t(m["Ur"]), -t(m["Uz"]), t(m["Uh"])]))
+        cell.bias_ih.copy_(torch.cat([t(m["br"]), -t(m["bz"]), t(m["bh"])]))
+        cell.bias_hh.zero_()
+        ref = cell(t(x)[None], t(h)[None])[0].numpy()
+    np.testing.assert_allclose(ours, ref, atol=1e-13, rtol=0)
+    # ... and the default (Chung) cell is NOT that routine when r varies
+    chung = O.gru(O.make_config(2, E, H, 1, 1), m, x, h, fp64=True)
+    assert np.max(np.abs(chung - ref)) > 1e-3
+
+
+def test_gru_cells_hand_case_reset_placement():
+    """H = 2, E = 1, all weights zero except Uh[0][1] = 1 and br = (0, 40):
+    r = (1/2, 1), z = 1/2, x-terms 0.  Unit 0's candidate reads h_1 through Uh:
+      Chung: tanh(Uh (r . h))_0 = tanh(r_1 h_1) = tanh(h_1)
+      LBR:   tanh(r_0 (Uh h)_0) = tanh(h_1 / 2)
+    h'_0 = h_0 / 2 + c_0 / 2; unit 1 has no recurrent input: h'_1 = h_1 / 2."""
+    E, H = 1, 2
+    m = {k: np.zeros(s, np.float32) for k, s in
+         dict(Wz=(H, E), Uz=(H, H), bz=(H,), Wr=(H, E), Ur=(H, H), br=(H,), Wh=(H, E), Uh=(H, H),
+              bh=(H,), emb=(2, E), nce_w=(2, H), nce_b=(2,), maxent=(2,)).items()}
+    m["Uh"][0, 1] = 1.0
+    m["br"][1] = 40.0
+    h = np.array([0.25, -0.75], np.float32)
+    x = np.array([0.5], np.float32)
+    for cell, c0 in ((O.CELL_GRU, math.tanh(-0.75)), (O.CELL_GRU_LBR, math.tanh(-0.375))):
+        out = O.gru(O.make_config(2, E, H, 1, 1, cell=cell), m, x, h, fp64=True)
+        assert out[0] == pytest.approx(0.125 + 0.5 * c0, abs=1e-15)
+        assert out[1] == pytest.approx(-0.375, abs=1e-15)
