@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--math", default="bf16", choices=["bf16", "tf32", "fp32"])
     ap.add_argument("--key", default="sign", help="off | sign | round:K")
+    ap.add_argument("--cell", default="gru", choices=["gru", "lbr"],
+                    help="recurrent cell (SURVEY 8(f)-3): gru = Chung GRU (the paper's), lbr = linear before reset")
     ap.add_argument("--no-cache", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -103,14 +105,14 @@ def cpu_model():
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def time_oracle(dims, model, wl, mode, k, cache, budget_s, max_steps=None):
+def time_oracle(dims, model, wl, mode, k, cache, budget_s, max_steps=None, cell=0):
     """The CPU oracle as it stands (single thread), on a bounded prefix of the
     workload's first session.  Returns (queries, seconds, frames)."""
     import oracle as O
     one = wl.select_sessions(0, 1)
     cfg = O.make_config(dims.V, dims.E, dims.H, dims.maxent_log2, dims.N, mode, k,
                         1 if cache else 0, 1,
-                        one.max_histories_hint() if cache else one.frames * one.B_s + 2)
+                        one.max_histories_hint() if cache else one.frames * one.B_s + 2, cell=cell)
     orc = O.Oracle(cfg, model)
     child = np.zeros(one.n_total, np.uint32)
     done_q, t_total, f = 0, 0.0, 0
@@ -141,7 +143,7 @@ def run_reference(args):
     wl = generate_workload(1, steps, c["B_s"], dims.V, seed=7)
     # each step = one frame of one utterance stream (bounded sample of the workload)
     q, secs, frames, per = time_oracle(dims, model, wl, mode, k, not args.no_cache, 1e30,
-                                       max_steps=steps)
+                                       max_steps=steps, cell=1 if args.cell == "lbr" else 0)
     timed = per[args.warmup:]
     tq = c["B_s"] * len(timed)
     value = tq / sum(timed)
@@ -238,6 +240,7 @@ def run_ours(args):
     # per-session pool must hold one per query of the run
     cap = wl.max_histories_hint() if not args.no_cache else frames * B_s + 2
     eng = R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math,
+                            cell=R.CELL_GRU_LBR if args.cell == "lbr" else R.CELL_GRU,
                             cache_enabled=not args.no_cache, num_sessions=S,
                             max_queries_per_call=n, max_histories_per_session=cap, device=local)
 
@@ -370,7 +373,7 @@ def run_ours(args):
         "config": {"workload": args.workload, "sessions_per_gpu": S, "queries_per_session_frame": B_s,
                    "queries_per_step": total_queries // args.steps, "V": dims.V, "E": dims.E,
                    "H": dims.H, "maxent": f"2^{dims.maxent_log2} {dims.N}-gram", "key": args.key,
-                   "cache": not args.no_cache, "math": args.math,
+                   "cache": not args.no_cache, "math": args.math, "cell": args.cell,
                    "l2": "flushed between timed steps (256 MiB write outside the event pair)",
                    "timed_frames": f"value: frames {tA}..{tB - 1}; roofline pass (library kernel events on): frames {tB}..{frames - 1} ({F0} prefill + {args.warmup} warm-up frames untimed)",
                    "parallelism": f"dp{world} (sessions sharded, weights replicated, NCCL all-gather of (score, child))"},
@@ -395,7 +398,8 @@ def run_ours(args):
         e2e = run_e2e(args, eng, wl, dev, world)
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        q, secs, f, _ = time_oracle(dims, model, wl, mode, k, not args.no_cache, args.cpu_seconds)
+        q, secs, f, _ = time_oracle(dims, model, wl, mode, k, not args.no_cache, args.cpu_seconds,
+                                    cell=1 if args.cell == "lbr" else 0)
         line["cpu_baseline"] = {"value": q / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": f"session 0, frames 0..{f - 1} ({q} queries, {secs:.1f} s)",
                                 "cpu": cpu_model(), "host_cores": host_cores()}

@@ -91,6 +91,13 @@ typedef enum {
 
 typedef enum { RNNLM_QHIT = 0, RNNLM_SHIT = 1, RNNLM_MISS = 2, RNNLM_INVALID = 255 } rnnlm_outcome;
 
+/* Recurrent cell of step (a5).  GRU: the cited GRU (Chung
+ * 2014, reading 1), c = tanh(Wh x + Uh (r . h) + bh).
+ * GRU_LBR: "linear before reset", c = tanh(Wh x + bh + r . (Uh h)) (the
+ * torch.nn.GRUCell form with no inner bias); z, r, the update
+ * h' = (1 - z) h + z c and everything else are identical. */
+typedef enum { RNNLM_CELL_GRU = 0, RNNLM_CELL_GRU_LBR = 1 } rnnlm_cell;
+
 typedef struct {
   uint32_t vocab, embed, hidden;        /* 2 <= V < 2^31 (word 0 = <s>), E, H; E and H multiples of 8 */
   uint32_t maxent_log2, maxent_order;   /* MaxEnt table M = 2^maxent_log2 floats (<= 2^31); order N in 1..8 */
@@ -101,6 +108,7 @@ typedef struct {
   uint32_t max_queries_per_call;        /* B_max: fixes scratch sizes */
   uint32_t max_histories_per_session;   /* handle/state capacity per session (>= 2); no eviction */
   int32_t device;                       /* CUDA device ordinal */
+  uint32_t cell;                        /* rnnlm_cell (0 = GRU) */
 } rnnlm_config;
 
 /* Host fp32 row-major weights, copied at create (caller may free on return).

@@ -123,6 +123,9 @@ struct TcArgs {
   uint32_t diag;                   // timing diagnostics: 1 no MMA, 2 no TMA, 3 no epilogue, 4 = 3 + no phase
                                    // dependency, 6 = 1 + 2 (results invalid); 5 cycle counters (results valid)
   unsigned long long *prof;        // diag 5: per-CTA cycle counters, else nullptr
+  // cell variant GRU_LBR: one phase, tiles of 64 units x
+  // (z | r | Wh x | Uh h), B = W3 [(H/64) x 192 rows][E+H]
+  const float *bz, *br;            // [H] (LBR epilogue)
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
   float round_scale;
@@ -278,11 +281,17 @@ __device__ __forceinline__ uint32_t next_tile(const Smem &m, uint32_t it, bool r
 }
 
 // MMA issuer: KC chunks of 4 x (M=128, N=256, K=32 bytes) per tile, both phases.
-template <typename T>
-__device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, int lane,
+// LBR tiles (lbr != 0): K-chunks of the x part issue N = 192 (z | r | Wh x
+// into columns 0-191); K-chunks of the h part issue N = 128 (z | r, columns
+// 0-127, B rows 0-127) and N = 64 (Uh h into columns 192-255, B rows
+// 128-191), so no product of a zero block is ever formed.
+template <typename T, bool LBR>
+__device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, uint32_t kx, int lane,
                                          uint32_t diag, unsigned long long *prof) {
   uint32_t stage = 0, phase = 0;
   const uint32_t id = idesc_of(Op<T>::FMT, BM, BN);
+  const uint32_t id192 = idesc_of(Op<T>::FMT, BM, 192), id128 = idesc_of(Op<T>::FMT, BM, 128),
+                 id64 = idesc_of(Op<T>::FMT, BM, 64);
   unsigned long long w_full = 0, w_tempty = 0, t0;
   for (uint32_t it = 0;; ++it) {
     if (next_tile(m, it, lane == 0) == NO_TILE) break;
@@ -299,10 +308,24 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
       tc_fence_after();
       if (lane == 0) {
         const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
-        if (diag != 1 && diag != 6)
+        if (diag != 1 && diag != 6) {
+          if constexpr (!LBR) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            Op<T>::mma(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+            for (int k = 0; k < 4; ++k)
+              Op<T>::mma(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
+          } else if (kc < kx) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              Op<T>::mma(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id192, (kc | k) != 0);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              Op<T>::mma(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id128, 1u);
+              Op<T>::mma(tm + 192, sdesc(a0 + k * 32), sdesc(b0 + 16384 + k * 32), id64,
+                         (kc != kx || k != 0) ? 1u : 0u);
+            }
+          }
+        }
         umma_commit(&m.empty[stage]);
         if (kc == KC - 1) umma_commit(&m.tfull[acc]);
       }
@@ -560,11 +583,65 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
   }
   if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
 }
+// LBR epilogue of one thread (cell variant): row `row`, the 32
+// units [64 ub + 32 half, +32) of the tile's 64; accumulator columns: z at
+// 0-63, r at 64-127, Wh x at 128-191, Uh h at 192-255 (tacc = the lane
+// quarter's column 0).  c = tanh(Wh x + bh + r . (Uh h)), h' = (1 - z) h + z c,
+// the new fp32 state (staged row store) and its compression code.
+__device__ __forceinline__ void epi_lbr(const TcArgs &a, uint32_t tacc, uint32_t row, bool valid, int half,
+                                        uint32_t ub, uint8_t *stg, uint32_t lane) {
+  const uint32_t dst = valid ? a.row_dst[row] : NONE;
+  const bool live = dst != NONE;
+  const uint32_t u0 = ub * 64 + half * 32, c0 = half * 32;
+  coop_load<128>(stg, live ? a.state + (size_t)a.row_src[row] * a.H + u0 : nullptr, lane);
+  uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && live) ? a.codes + (size_t)dst * a.cstride : nullptr;
+  unsigned long long hs = 0;
+  uint32_t signacc = 0;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    float vz[16], vr[16], vx[16], vu[16], h[16];
+    tmem_ld16(tacc + c0 + g * 16, vz);
+    tmem_ld16(tacc + 64 + c0 + g * 16, vr);
+    tmem_ld16(tacc + 128 + c0 + g * 16, vx);
+    tmem_ld16(tacc + 192 + c0 + g * 16, vu);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {                   // this lane's 16 staged state values of group g
+      const float4 t4 = *reinterpret_cast<const float4 *>(stg + stg_off<128>(lane, 4 * g + c));
+      h[4 * c] = t4.x; h[4 * c + 1] = t4.y; h[4 * c + 2] = t4.z; h[4 * c + 3] = t4.w;
+    }
+    tmem_ld_wait();
+    const float4 *bz4 = reinterpret_cast<const float4 *>(a.bz + u0 + g * 16);
+    const float4 *br4 = reinterpret_cast<const float4 *>(a.br + u0 + g * 16);
+    const float4 *bh4 = reinterpret_cast<const float4 *>(a.bh + u0 + g * 16);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float4 z4 = __ldg(bz4 + c), r4 = __ldg(br4 + c), h4 = __ldg(bh4 + c);
+      const float bz[4] = {z4.x, z4.y, z4.z, z4.w}, br[4] = {r4.x, r4.y, r4.z, r4.w},
+                  bh[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = 4 * c + t;
+        const float z = sigm(vz[j] + bz[t]), r = sigm(vr[j] + br[t]);
+        const float cand = tanh_fast(vx[j] + bh[t] + r * vu[j]);
+        h[j] = (1.0f - z) * h[j] + z * cand;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      *reinterpret_cast<float4 *>(stg + stg_off<128>(lane, 4 * g + c)) =
+          make_float4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+    if (a.cache && live) hs += encode16(a, h, u0 + g * 16, code, signacc);
+  }
+  coop_store<128>(stg, live ? a.state_out + (size_t)dst * a.H + u0 : nullptr, lane);
+  if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
+}
+
 // =============================================================== fused GRU kernel
 // warp 0: TMA producer (waits on the phase-1 counter before a phase-2 tile);
 // warp 1: TMEM allocation + MMA issue; warps 2-9: epilogue, TMEM lane quarter
 // = warp % 4, column half = (warp - 2) / 4.
-template <typename T>
+template <typename T, bool LBR>
 __global__ void __maxnreg__(GRU_MAXREG)
     k_gru_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1,
              const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2,
@@ -572,7 +649,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Smem m = carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t n1 = a.nub, n2 = a.H / BN;
+  // GRU: per M-tile nub phase-1 + H/256 phase-2 tiles; LBR: H/64 one-phase tiles
+  const uint32_t n1 = LBR ? a.H / 64 : a.nub, n2 = LBR ? 0u : a.H / BN;
+  const uint32_t b_bytes = LBR ? 192 * 128 : B_BYTES;
   constexpr int BKE = Op<T>::BKE;
   const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE;
   const uint32_t target = n1 * EPI_WARPS;               // phase-1 arrivals per M-tile
@@ -619,11 +698,11 @@ __global__ void __maxnreg__(GRU_MAXREG)
             if (++stage == ST) { stage = 0; phase ^= 1; }
             continue;
           }
-          mbar_expect_tx(&m.full[stage], A_BYTES + B_BYTES);
+          mbar_expect_tx(&m.full[stage], A_BYTES + b_bytes);
           const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * B_BYTES);
           if (x.kind == 0) {
             tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BKE), (int)m0);
-            tma_load_2d(dB, &map_w1, &m.full[stage], (int)(kc * BKE), (int)(x.j * BN));
+            tma_load_2d(dB, &map_w1, &m.full[stage], (int)(kc * BKE), (int)(x.j * (LBR ? 192u : BN)));
           } else {
             if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BKE), (int)m0);
             else tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BKE), (int)m0);
@@ -635,7 +714,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
       if (prof) { prof[0] = w_empty; prof[1] = w_dep; }
     }
   } else if (warp == 1) {
-    mma_loop<T>(m, tmem_base, KC, lane, a.diag, prof);
+    mma_loop<T, LBR>(m, tmem_base, KC, kx, lane, a.diag, prof);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -666,7 +745,12 @@ __global__ void __maxnreg__(GRU_MAXREG)
         }
         continue;
       }
-      if (x.kind == 0) {
+      if constexpr (LBR) {
+        epi_lbr(a, tbase - half * (BN / 2), row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
+        tc_fence_before();
+        mbar_arrive(&m.tempty[acc]);
+        b1 += clock64() - t0;
+      } else if (x.kind == 0) {
         epi_phase1<T>(a, tbase, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
@@ -1009,7 +1093,10 @@ struct TcState {
   uint32_t diag = 0;               // RNNLM_TC_DIAG: timing diagnostics (see TcArgs::diag)
   unsigned long long *prof = nullptr;
   float *bzr = nullptr, *bh = nullptr;
-  CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h;
+  bool lbr = false;                // cell GRU_LBR: one-phase tiles over W3
+  void *w3 = nullptr;
+  float *bz = nullptr, *br = nullptr;
+  CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h, map_w3;
   bool bound = false;
 };
 
@@ -1020,6 +1107,38 @@ using namespace rnnlm_tc;
 
 int gru_tc_supported(uint32_t E, uint32_t H) {
   return E % BK == 0 && H % BN == 0 && E >= BK && H >= BN;
+}
+
+template <typename T>
+static T cv_op(float v) {
+  if constexpr (sizeof(T) == 2) {
+    return __float2bfloat16_rn(v);
+  } else {  // round to TF32 (nearest, ties away; same as cvt.rna.tf32.f32 on the activations)
+    uint32_t b;
+    std::memcpy(&b, &v, 4);
+    b = (b + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &b, 4);
+    return r;
+  }
+}
+
+// LBR cell: W3 = per 64-unit block, 64 rows [Wz | Uz], 64 rows [Wr | Ur],
+// 64 rows [Wh | Uh] (K-major, E + H columns).
+template <typename T>
+static bool upload_w3(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H) {
+  const size_t K1 = E + H;
+  std::vector<T> w3((size_t)3 * H * K1);
+  const float *Wg[3] = {w->Wz, w->Wr, w->Wh};
+  const float *Ug[3] = {w->Uz, w->Ur, w->Uh};
+  for (size_t u = 0; u < H; ++u)
+    for (int g = 0; g < 3; ++g) {
+      T *row = w3.data() + ((u / 64) * 192 + g * 64 + u % 64) * K1;
+      for (size_t k = 0; k < E; ++k) row[k] = cv_op<T>(Wg[g][u * E + k]);
+      for (size_t k = 0; k < H; ++k) row[E + k] = cv_op<T>(Ug[g][u * H + k]);
+    }
+  return cudaMalloc(&t->w3, w3.size() * sizeof(T)) == cudaSuccess &&
+         cudaMemcpy(t->w3, w3.data(), w3.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
 }
 
 template <typename T>
@@ -1057,11 +1176,11 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
          cudaMemcpy(t->w2, w2.data(), w2.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
 }
 
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, void **state_out) {
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int lbr, void **state_out) {
   *state_out = nullptr;
   TcState *t = new TcState;
-  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0;
-  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = t->tf32 ? 0 : atoi(e);   // pair/multicast: bf16 only
+  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0; t->lbr = lbr != 0;
+  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = (t->tf32 || t->lbr) ? 0 : atoi(e);   // pair: bf16 GRU only
   if (const char *e = getenv("RNNLM_TC_DIAG")) t->diag = (uint32_t)atoi(e);
   const size_t K1 = E + H;
   std::vector<float> bzr((size_t)2 * H), bh(H);
@@ -1072,6 +1191,13 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, voi
     bh[u] = w->bh[u];
   }
   bool ok = t->tf32 ? upload_w<float>(t, w, E, H) : upload_w<__nv_bfloat16>(t, w, E, H);
+  if (t->lbr) {
+    ok = ok && (t->tf32 ? upload_w3<float>(t, w, E, H) : upload_w3<__nv_bfloat16>(t, w, E, H));
+    ok = ok && cudaMalloc(&t->bz, (size_t)H * 4) == cudaSuccess && cudaMalloc(&t->br, (size_t)H * 4) == cudaSuccess &&
+         cudaMemcpy(t->bz, w->bz, (size_t)H * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(t->br, w->br, (size_t)H * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         make_map(&t->map_w3, t->w3, K1, (uint64_t)H / 64 * 192, 192, t->tf32);
+  }
   ok = ok && cudaMalloc(&t->bzr, bzr.size() * 4) == cudaSuccess &&
        cudaMalloc(&t->bh, bh.size() * 4) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bzr, bzr.data(), bzr.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -1081,9 +1207,13 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, voi
   if (!t->tf32)
     ok = ok && make_map(&t->map_w1h, t->w1, K1, 2 * (uint64_t)H, BN / 2) &&
          make_map(&t->map_w2h, t->w2, K1, H, BN / 2);
-  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)SMEM) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PAIR) == cudaSuccess;
   *state_out = t;
@@ -1115,6 +1245,9 @@ void gru_tc_release(void *state) {
   if (!t) return;
   cudaFree(t->w1);
   cudaFree(t->w2);
+  cudaFree(t->w3);
+  cudaFree(t->bz);
+  cudaFree(t->br);
   cudaFree(t->a1);
   cudaFree(t->done1);
   cudaFree(t->prof);
@@ -1140,6 +1273,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.tile_ctr = t->done1 + (t->bmax / BM + 2);
   a.lag = 48;
   a.diag = t->diag;
+  a.bz = t->bz; a.br = t->br;
   a.prof = nullptr;
   if (t->diag == 5) {
     if (!t->prof) cudaMalloc(&t->prof, 1024 * 16 * sizeof(unsigned long long));
@@ -1147,7 +1281,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     a.prof = t->prof;
   }
   const uint32_t mt = (max_rows + BM - 1) / BM;
-  uint32_t g1 = mt * (t->nub + P.H / BN);
+  uint32_t g1 = t->lbr ? mt * (P.H / 64) : mt * (t->nub + P.H / BN);
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
   uint32_t gg = (max_rows + 7) / 8;
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
@@ -1161,8 +1295,13 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     launch_pdl_cluster(k_gru_tc2, gp, THREADS, SMEM_PAIR, s, 2, t->map_a1, t->map_w1h, t->map_rh,
                        t->map_w2h, a);
   } else {
-    if (t->tf32) launch_pdl(k_gru_tc<float>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
-    else launch_pdl(k_gru_tc<__nv_bfloat16>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+    if (t->lbr) {
+      if (t->tf32) launch_pdl(k_gru_tc<float, true>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
+      else launch_pdl(k_gru_tc<__nv_bfloat16, true>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
+    } else {
+      if (t->tf32) launch_pdl(k_gru_tc<float, false>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+      else launch_pdl(k_gru_tc<__nv_bfloat16, false>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+    }
   }
   if (ev_phase1) cudaEventRecord(ev_phase1, s);
   if (a.prof) {

@@ -62,6 +62,7 @@ struct Params {
   uint32_t V, E, H, N, S, cap;
   uint32_t qmask, hmask;          // table capacity - 1 (power of two)
   uint32_t key_mode, round_digits, cache, math;
+  uint32_t cell;                  // rnnlm_cell
   unsigned long long M_mask;
   uint32_t cstride;               // bytes per stored code row (multiple of 16)
   uint32_t code_bytes, code_words;

@@ -30,13 +30,13 @@ def model(name_or_dims, seed=1234, scale=None):
     return _models[key]
 
 
-def pair(d, m, wl, mode=KEY_OFF, k=0, math=MATH_FP32, cache=True, B=None, cap=None):
+def pair(d, m, wl, mode=KEY_OFF, k=0, math=MATH_FP32, cache=True, B=None, cap=None, cell=0):
     cap = cap or (wl.max_histories_hint() if cache else wl.n_total // wl.S + 2)
     B = B or wl.n_per_frame
     eng = RNNLM.from_dims(d, m, key_mode=mode, round_digits=k, math=math, cache_enabled=cache,
-                          num_sessions=wl.S, max_queries_per_call=B, max_histories_per_session=cap)
+                          num_sessions=wl.S, max_queries_per_call=B, max_histories_per_session=cap, cell=cell)
     orc = O.Oracle(O.make_config(d.V, d.E, d.H, d.maxent_log2, d.N, mode, k, 1 if cache else 0,
-                                 wl.S, cap), m)
+                                 wl.S, cap, cell=cell), m)
     return eng, orc
 
 
@@ -380,3 +380,49 @@ def test_per_query_calls_equal_per_frame_batches():
     for a, b in zip(outs[0][2], outs[1][2]):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
     assert outs[0][3]["gru_computations"] == outs[1][3]["gru_computations"]
+
+
+# ---------------------------------------------------------------- cell variant GRU_LBR
+@pytest.mark.parametrize("math", [MATH_FP32, MATH_BF16, MATH_TF32])
+def test_lbr_cell_moderate(math):
+    """Linear-before-reset cell on every math path: FP32 SIMT (phase 1 keeps r,
+    phase 2 contracts h), BF16 / TF32 one-phase tcgen05 tiles (N = 192 over
+    the x part, N = 128 + 64 over the h part)."""
+    d, m = model("moderate")
+    wl = generate_workload(1, 30, 256, d.V, seed=23)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=O.CELL_GRU_LBR)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
+    assert rep["miss"] > 200
+
+
+def test_lbr_cell_large_full_tiles_and_round_codes():
+    """Large model, all-miss (16 full M-tiles, 16 unit tiles each) and a ragged
+    multi-session round:2 batch, LBR on the bf16 tensor-core path."""
+    d, m = model("large")
+    wl = generate_workload(1, 2, 2048, d.V, seed=5)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16, cache=False, cell=O.CELL_GRU_LBR)
+    rep = replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+    assert rep["miss"] == wl.n_total
+    wl = generate_workload(3, 3, 300, d.V, seed=6)
+    eng, orc = pair(d, m, wl, KEY_ROUND, k=2, math=MATH_BF16, cell=O.CELL_GRU_LBR)
+    replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+
+
+def test_lbr_differs_from_gru():
+    """The two cells are different functions (same weights, same stream):
+    children of the root agree (h = 0 makes both recurrent terms vanish),
+    deeper histories do not."""
+    d, m = model("moderate")
+    wl = generate_workload(1, 30, 64, d.V, seed=29)
+    outs = []
+    for cell in (0, O.CELL_GRU_LBR):
+        eng, _ = pair(d, m, wl, KEY_OFF, math=MATH_FP32, cell=cell)
+        child = np.zeros(wl.n_total, np.uint32)
+        for t in range(wl.frames):
+            sl = wl.frame_slice(t)
+            par = O.resolve_parents(wl.parent_ref[sl], child)
+            _, ch, _ = eng.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]))
+            child[sl] = ch.cpu().numpy().view(np.uint32)
+        last = int(child.max())
+        outs.append(eng.read_states(0, np.arange(last - 7, last + 1, dtype=np.uint32)).cpu().numpy())
+    assert np.max(np.abs(outs[0] - outs[1])) > 1e-4
