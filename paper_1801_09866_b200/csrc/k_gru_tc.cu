@@ -281,10 +281,11 @@ __device__ __forceinline__ uint32_t next_tile(const Smem &m, uint32_t it, bool r
 }
 
 // MMA issuer: KC chunks of 4 x (M=128, N=256, K=32 bytes) per tile, both phases.
-// LBR tiles (lbr != 0): K-chunks of the x part issue N = 192 (z | r | Wh x
-// into columns 0-191); K-chunks of the h part issue N = 128 (z | r, columns
-// 0-127, B rows 0-127) and N = 64 (Uh h into columns 192-255, B rows
-// 128-191), so no product of a zero block is ever formed.
+// LBR tiles: accumulator columns [Wh x | z | r | Uh h] (64 each).  W3 rows
+// carry [Wh; Wz; Wr] in their x half and [Uz; Ur; Uh] in their h half, so
+// every K-chunk is ONE N = 192 MMA: x chunks into columns 0-191, h chunks
+// into columns 64-255 (no product of a zero block).  The first h K-step
+// splits into N = 128 (accumulate into z | r) + N = 64 (initialise Uh h).
 template <typename T, bool LBR>
 __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, uint32_t kx, int lane,
                                          uint32_t diag, unsigned long long *prof) {
@@ -320,9 +321,12 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
           } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              Op<T>::mma(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id128, 1u);
-              Op<T>::mma(tm + 192, sdesc(a0 + k * 32), sdesc(b0 + 16384 + k * 32), id64,
-                         (kc != kx || k != 0) ? 1u : 0u);
+              if (kc == kx && k == 0) {
+                Op<T>::mma(tm + 64, sdesc(a0), sdesc(b0), id128, 1u);
+                Op<T>::mma(tm + 192, sdesc(a0), sdesc(b0 + 16384), id64, 0u);
+              } else {
+                Op<T>::mma(tm + 64, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id192, 1u);
+              }
             }
           }
         }
@@ -584,8 +588,8 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
   if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
 }
 // LBR epilogue of one thread (cell variant): row `row`, the 32
-// units [64 ub + 32 half, +32) of the tile's 64; accumulator columns: z at
-// 0-63, r at 64-127, Wh x at 128-191, Uh h at 192-255 (tacc = the lane
+// units [64 ub + 32 half, +32) of the tile's 64; accumulator columns: Wh x
+// at 0-63, z at 64-127, r at 128-191, Uh h at 192-255 (tacc = the lane
 // quarter's column 0).  c = tanh(Wh x + bh + r . (Uh h)), h' = (1 - z) h + z c,
 // the new fp32 state (staged row store) and its compression code.
 __device__ __forceinline__ void epi_lbr(const TcArgs &a, uint32_t tacc, uint32_t row, bool valid, int half,
@@ -600,9 +604,9 @@ __device__ __forceinline__ void epi_lbr(const TcArgs &a, uint32_t tacc, uint32_t
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
     float vz[16], vr[16], vx[16], vu[16], h[16];
-    tmem_ld16(tacc + c0 + g * 16, vz);
-    tmem_ld16(tacc + 64 + c0 + g * 16, vr);
-    tmem_ld16(tacc + 128 + c0 + g * 16, vx);
+    tmem_ld16(tacc + c0 + g * 16, vx);
+    tmem_ld16(tacc + 64 + c0 + g * 16, vz);
+    tmem_ld16(tacc + 128 + c0 + g * 16, vr);
     tmem_ld16(tacc + 192 + c0 + g * 16, vu);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {                   // this lane's 16 staged state values of group g
@@ -1123,13 +1127,14 @@ static T cv_op(float v) {
   }
 }
 
-// LBR cell: W3 = per 64-unit block, 64 rows [Wz | Uz], 64 rows [Wr | Ur],
-// 64 rows [Wh | Uh] (K-major, E + H columns).
+// LBR cell: W3 = per 64-unit block 192 rows (K-major, E + H columns); row
+// g * 64 + i carries [Wh, Wz, Wr][g] row i in its x half and [Uz, Ur, Uh][g]
+// row i in its h half (see mma_loop).
 template <typename T>
 static bool upload_w3(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H) {
   const size_t K1 = E + H;
   std::vector<T> w3((size_t)3 * H * K1);
-  const float *Wg[3] = {w->Wz, w->Wr, w->Wh};
+  const float *Wg[3] = {w->Wh, w->Wz, w->Wr};
   const float *Ug[3] = {w->Uz, w->Ur, w->Uh};
   for (size_t u = 0; u < H; ++u)
     for (int g = 0; g < 3; ++g) {
