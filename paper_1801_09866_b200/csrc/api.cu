@@ -19,7 +19,7 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int
 void gru_tc_release(void *state);
 int gru_tc_bind(void *state, void *rh, uint32_t bmax);
 int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s,
-                  cudaEvent_t ev_gathered, cudaEvent_t ev_phase1);
+                  cudaEvent_t ev_gathered, cudaEvent_t ev_phase1, cudaEvent_t ev_fork);
 // Exact log-normaliser (k_norm.cu).
 int norm_supported(uint32_t H, uint32_t N);
 int norm_prepare(const Params &P, uint32_t bmax, void **state_out, cudaStream_t s);
@@ -379,10 +379,19 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
   k += rnnlm_host::launch_cache_front(P, A, s);
   k += rnnlm_host::launch_commit(P, A, s);
   // fork: (a6) scoring and (a7) result write depend only on the commit; the
-  // GRU (a5) too.  Scoring + result write go to the side stream and overlap
-  // the tensor-core GRU; the caller's stream joins them before returning.
-  cudaEvent_t fork = h->timing ? ev[1] : h->ev_fork;
-  cudaEventRecord(fork, s);
+  // GRU (a5) too.  Scoring + result write go to the side stream and run
+  // beside the tensor-core GRU (co-resident CTAs); on the tensor-core path the
+  // fork is taken after the A1 gather, so the memory-bound gather has the GPU
+  // to itself.  The caller's stream joins the side stream before returning.
+  cudaEvent_t fork = h->ev_fork;
+  if (h->timing) cudaEventRecord(ev[1], s);             // ms_cache ends at the commit
+  if (P.math != RNNLM_MATH_FP32) {
+    k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s, h->timing >= 2 ? ev[4] : nullptr,
+                                   nullptr, fork);
+  } else {
+    cudaEventRecord(fork, s);
+    k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
+  }
   cudaStreamWaitEvent(h->side, fork, 0);
   k += rnnlm_host::launch_final(P, A, h->side);
   if (h->timing) cudaEventRecord(ev[2], h->side);
@@ -390,12 +399,6 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
   k += rnnlm_host::launch_dup_scores(P, A, h->num_sms, h->side);
   if (h->timing) cudaEventRecord(ev[3], h->side);
   cudaEventRecord(h->ev_join, h->side);
-  if (P.math != RNNLM_MATH_FP32) {
-    k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s, h->timing >= 2 ? ev[4] : nullptr,
-                                   nullptr);
-  } else {
-    k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
-  }
   if (h->timing) cudaEventRecord(ev[5], s);
   if (P.math == RNNLM_MATH_FP32)                      // the tcgen05 epilogue encodes in place
     k += rnnlm_host::launch_encode_rows(P, n, h->num_sms, s);

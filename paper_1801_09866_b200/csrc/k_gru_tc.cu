@@ -1262,7 +1262,7 @@ void gru_tc_release(void *state) {
 }
 
 int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, cudaStream_t s,
-                  cudaEvent_t ev_gathered, cudaEvent_t ev_phase1) {
+                  cudaEvent_t ev_gathered, cudaEvent_t ev_phase1, cudaEvent_t ev_fork) {
   TcState *t = static_cast<TcState *>(state);
   if (!max_rows || !t || !t->bound) return 0;
   TcArgs a;
@@ -1293,6 +1293,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   if (t->tf32) launch_pdl(k_gather_a1<float>, gg, 256, 0, s, a);
   else launch_pdl(k_gather_a1<__nv_bfloat16>, gg, 256, 0, s, a);
   if (ev_gathered) cudaEventRecord(ev_gathered, s);
+  if (ev_fork) cudaEventRecord(ev_fork, s);
   if (t->pair) {
     uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / BN) * 2;
     const uint32_t cap = (uint32_t)num_sms & ~1u;
