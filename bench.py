@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--normalizer", action="store_true",
                     help="SURVEY 8(f)-2 workload: exact log-normalisers/s instead of the query step")
     ap.add_argument("--histories", type=int, default=2048, help="(--normalizer) histories per call")
+    ap.add_argument("--offline", action="store_true",
+                    help="SURVEY 8(f)-4 workload: whole utterances rescored level by level (2-pass) vs frame by frame")
+    ap.add_argument("--frames", type=int, default=None, help="(--offline) frames per utterance (default: config)")
     ap.add_argument("--trace", default=None,
                     help="(diagnostics) write a CUPTI kernel timeline of the timed steps (chrome trace JSON); "
                          "the printed numbers of such a run are not bench values")
@@ -561,9 +564,92 @@ def run_normalizer(args):
     print(json.dumps(line), flush=True)
 
 
+def run_offline(args):
+    """whole utterances known in advance (2-pass lattice
+    rescoring) scheduled level by level (paper_1801_09866_b200.offline)
+    instead of one call per frame.  Both schedules run the same synthetic
+    utterances on the same engine settings; each is device-timed with CUDA
+    events around the whole stream (after one untimed warm-up pass)."""
+    import torch
+
+    import paper_1801_09866_b200 as R
+    from paper_1801_09866_b200.offline import OfflineRunner
+
+    c = CONFIGS[args.workload]
+    dims = model_dims(args.workload)
+    S = args.sessions or c["S"]
+    frames = args.frames or c["frames"]
+    model = generate_model(dims, seed=1234)
+    wl = generate_workload(S, frames, c["B_s"], dims.V, seed=7)
+    mode, k = key_mode(args.key)
+    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32}[args.math]
+    dev = torch.device("cuda", 0)
+    Bmax = 32768
+    cap = wl.max_histories_hint()
+
+    def engine(B):
+        return R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math, num_sessions=S,
+                                 max_queries_per_call=B, max_histories_per_session=cap)
+
+    d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
+    d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
+    d_ref = torch.as_tensor(wl.parent_ref, device=dev)
+    on = engine(wl.n_per_frame)
+    d_child = torch.zeros(wl.n_total, dtype=torch.int32, device=dev)
+    d_score = torch.zeros(wl.n_total, dtype=torch.float32, device=dev)
+    d_par = torch.zeros(wl.n_per_frame, dtype=torch.int32, device=dev)
+
+    def online():
+        on.reset_session()
+        for t in range(wl.frames):
+            sl = wl.frame_slice(t)
+            R.resolve_parents(d_ref[sl], d_child, d_par)
+            on.query_batch(d_sess[sl], d_par, d_word[sl], score=d_score[sl], child=d_child[sl], want_outcome=False)
+
+    off = engine(Bmax)
+    runner = OfflineRunner(off, wl, max_batch=Bmax)
+
+    def offline():
+        off.reset_session()
+        runner.run()
+
+    def timed(fn):
+        fn()                                                     # warm-up pass
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    ms_on = timed(online)
+    ms_off = timed(offline)
+    same = bool(torch.equal(d_score, runner.score)) if mode == R.KEY_OFF else None
+    nb = len(runner.batches)
+    line = {
+        "metric": "RNNLM queries/sec (offline level-batched rescoring of whole utterances)",
+        "value": wl.n_total / (ms_off * 1e-3), "unit": "queries/s", "n_gpus": 1, "steps": 1, "warmup": 1,
+        "ms_per_step": ms_off, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32": "f32"}[args.math], "data": "synthetic",
+        "config": {"workload": args.workload, "sessions": S, "frames": frames, "queries": int(wl.n_total),
+                   "key": args.key, "math": args.math, "offline_calls": nb, "online_calls": frames,
+                   "mean_queries_per_offline_call": wl.n_total / max(1, nb),
+                   "step": "one pass over the whole query stream"},
+        "online": {"value": wl.n_total / (ms_on * 1e-3), "ms": ms_on},
+        "speedup_vs_online": ms_on / ms_off,
+        "scores_bitwise_equal_online": same,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
-    if args.normalizer:
+    if args.offline:
+        if args.impl == "reference" or dist_env()[1] > 1:
+            raise SystemExit("--offline: one GPU, our implementation only")
+        run_offline(args)
+    elif args.normalizer:
         if args.impl == "reference" or dist_env()[1] > 1:
             raise SystemExit("--normalizer: one GPU, our implementation only")
         run_normalizer(args)

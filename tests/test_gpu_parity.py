@@ -426,3 +426,37 @@ def test_lbr_differs_from_gru():
         last = int(child.max())
         outs.append(eng.read_states(0, np.arange(last - 7, last + 1, dtype=np.uint32)).cpu().numpy())
     assert np.max(np.abs(outs[0] - outs[1])) > 1e-4
+
+
+# ---------------------------------------------------------------- offline level batching
+@pytest.mark.parametrize("math", [MATH_BF16, MATH_FP32])
+def test_offline_level_batches_equal_online(math):
+    """The same utterances run level by level (paper_1801_09866_b200.offline)
+    instead of frame by frame: with lossless keys every query gets bitwise the
+    same score and its child bitwise the same state (batch-invariant kernels)."""
+    from paper_1801_09866_b200.offline import OfflineRunner
+    d, m = model("moderate")
+    wl = generate_workload(2, 40, 128, d.V, seed=43)
+    cap = wl.max_histories_hint()
+    mk = lambda B: RNNLM.from_dims(d, m, key_mode=KEY_OFF, math=math, num_sessions=wl.S,
+                                   max_queries_per_call=B, max_histories_per_session=cap)
+    on = mk(wl.n_per_frame)
+    child_on = np.zeros(wl.n_total, np.uint32)
+    score_on = np.zeros(wl.n_total, np.float32)
+    for t in range(wl.frames):
+        sl = wl.frame_slice(t)
+        par = O.resolve_parents(wl.parent_ref[sl], child_on)
+        sc, ch, _ = on.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]))
+        score_on[sl] = sc.cpu().numpy()
+        child_on[sl] = ch.cpu().numpy().view(np.uint32)
+    off = mk(4096)
+    runner = OfflineRunner(off, wl, max_batch=4096)
+    sc, ch = runner.run()
+    assert len(runner.batches) < wl.frames
+    assert np.array_equal(score_on.view(np.uint32), sc.cpu().numpy().view(np.uint32))
+    child_off = ch.cpu().numpy().view(np.uint32)
+    for s in range(wl.S):
+        msk = wl.session == s
+        a = on.read_states(s, child_on[msk]).cpu().numpy()
+        b = off.read_states(s, child_off[msk]).cpu().numpy()
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
