@@ -48,8 +48,9 @@ def parse():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--math", default="bf16", choices=["bf16", "tf32", "fp32"])
     ap.add_argument("--key", default="sign", help="off | sign | round:K")
-    ap.add_argument("--cell", default="gru", choices=["gru", "lbr"],
-                    help="recurrent cell (SURVEY 8(f)-3): gru = Chung GRU (the paper's), lbr = linear before reset")
+    ap.add_argument("--cell", default="gru", choices=["gru", "lbr", "rnn"],
+                    help="recurrent cell (SURVEY 8(f)-3): gru = Chung GRU (the paper's), lbr = linear before "
+                         "reset, rnn = the paper's comparison vanilla RNN (Elman, logistic)")
     ap.add_argument("--no-cache", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -146,7 +147,7 @@ def run_reference(args):
     wl = generate_workload(1, steps, c["B_s"], dims.V, seed=7)
     # each step = one frame of one utterance stream (bounded sample of the workload)
     q, secs, frames, per = time_oracle(dims, model, wl, mode, k, not args.no_cache, 1e30,
-                                       max_steps=steps, cell=1 if args.cell == "lbr" else 0)
+                                       max_steps=steps, cell={"gru": 0, "lbr": 1, "rnn": 2}[args.cell])
     timed = per[args.warmup:]
     tq = c["B_s"] * len(timed)
     value = tq / sum(timed)
@@ -243,7 +244,7 @@ def run_ours(args):
     # per-session pool must hold one per query of the run
     cap = wl.max_histories_hint() if not args.no_cache else frames * B_s + 2
     eng = R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math,
-                            cell=R.CELL_GRU_LBR if args.cell == "lbr" else R.CELL_GRU,
+                            cell={"gru": R.CELL_GRU, "lbr": R.CELL_GRU_LBR, "rnn": R.CELL_RNN}[args.cell],
                             cache_enabled=not args.no_cache, num_sessions=S,
                             max_queries_per_call=n, max_histories_per_session=cap, device=local)
 
@@ -343,7 +344,8 @@ def run_ours(args):
     total_queries = queries_rank * world
     value = total_queries / (total_ms / 1e3)
     rows = d_B["gru_computations"]
-    flops = 6.0 * dims.H * (dims.E + dims.H) * rows       # [Q, E+H] x [E+H, 3H], 2 flop/MAC
+    gates = 1 if args.cell == "rnn" else 3                 # vanilla RNN: one gate
+    flops = 2.0 * gates * dims.H * (dims.E + dims.H) * rows   # [Q, E+H] x [E+H, gates*H], 2 flop/MAC
     gru_s = timing["ms_gru"] / 1e3
     peaks = {}
     try:
@@ -384,7 +386,7 @@ def run_ours(args):
                      "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                      "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic": f"6*H*(E+H) flop x {rows} GRU rows over {args.steps} steps",
+                     "algorithmic": f"{2 * gates}*H*(E+H) flop x {rows} GRU rows over {args.steps} steps",
                      "gru_ms_per_step": timing["ms_gru"] / args.steps,
                      "share_of_step": (timing["ms_gru"] / ms_B) if ms_B else None},
         "kernel_ms_per_step": {kk: timing[kk] / args.steps for kk in
@@ -402,7 +404,7 @@ def run_ours(args):
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         q, secs, f, _ = time_oracle(dims, model, wl, mode, k, not args.no_cache, args.cpu_seconds,
-                                    cell=1 if args.cell == "lbr" else 0)
+                                    cell={"gru": 0, "lbr": 1, "rnn": 2}[args.cell])
         line["cpu_baseline"] = {"value": q / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": f"session 0, frames 0..{f - 1} ({q} queries, {secs:.1f} s)",
                                 "cpu": cpu_model(), "host_cores": host_cores()}

@@ -95,8 +95,11 @@ typedef enum { RNNLM_QHIT = 0, RNNLM_SHIT = 1, RNNLM_MISS = 2, RNNLM_INVALID = 2
  * 2014, reading 1), c = tanh(Wh x + Uh (r . h) + bh).
  * GRU_LBR: "linear before reset", c = tanh(Wh x + bh + r . (Uh h)) (the
  * torch.nn.GRUCell form with no inner bias); z, r, the update
- * h' = (1 - z) h + z c and everything else are identical. */
-typedef enum { RNNLM_CELL_GRU = 0, RNNLM_CELL_GRU_LBR = 1 } rnnlm_cell;
+ * h' = (1 - z) h + z c and everything else are identical.
+ * RNN: the paper's comparison "vanilla-RNNLM" as an Elman layer with
+ * the logistic activation of the RNNLM it cites, h' = sigma(Wh x + Uh h + bh)
+ * (Wz, Uz, bz, Wr, Ur, br are not used). */
+typedef enum { RNNLM_CELL_GRU = 0, RNNLM_CELL_GRU_LBR = 1, RNNLM_CELL_RNN = 2 } rnnlm_cell;
 
 typedef struct {
   uint32_t vocab, embed, hidden;        /* 2 <= V < 2^31 (word 0 = <s>), E, H; E and H multiples of 8 */

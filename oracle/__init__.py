@@ -22,7 +22,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.cpp")
 
 KEY_OFF, KEY_ROUND, KEY_SIGN = 0, 1, 2
-CELL_GRU, CELL_GRU_LBR = 0, 1
+CELL_GRU, CELL_GRU_LBR, CELL_RNN = 0, 1, 2
 QHIT, SHIT, MISS, INVALID = 0, 1, 2, 255
 ALL_SESSIONS = 0xFFFFFFFF
 

@@ -131,6 +131,8 @@ static double sigmoid(double a) { return 1.0 / (1.0 + std::exp(-a)); }
 // applied AFTER the recurrent product ("linear before reset"):
 //   h~ = tanh(Wh x + bh + r . (Uh h))
 // with the same z, r and update; every other step of the method is unchanged.
+// Cell variant ORC_CELL_RNN: the paper's comparison "vanilla-RNNLM"
+// as the Elman layer of the RNNLM it cites, h' = sigma(Wh x + Uh h + bh).
 void orc_gru(const orc_config *cfg, const orc_weights *w, const float *x, const float *h,
              double *out64, float *out32) {
   const uint32_t H = cfg->H, E = cfg->E;
@@ -148,14 +150,14 @@ void orc_gru(const orc_config *cfg, const orc_weights *w, const float *x, const 
     z[i] = sigmoid(az + uz + (double)w->bz[i]);
     r[i] = sigmoid(ar + ur + (double)w->br[i]);
   }
-  const bool lbr = cfg->cell == ORC_CELL_GRU_LBR;
-  for (uint32_t j = 0; j < H; ++j) rh[j] = lbr ? (double)h[j] : r[j] * (double)h[j];
+  const bool lbr = cfg->cell == ORC_CELL_GRU_LBR, rnn = cfg->cell == ORC_CELL_RNN;
+  for (uint32_t j = 0; j < H; ++j) rh[j] = (lbr || rnn) ? (double)h[j] : r[j] * (double)h[j];
   for (uint32_t i = 0; i < H; ++i) {
     double ax = 0.0, au = 0.0;
     for (uint32_t j = 0; j < E; ++j) ax += (double)w->Wh[(size_t)i * E + j] * (double)x[j];
     for (uint32_t j = 0; j < H; ++j) au += (double)w->Uh[(size_t)i * H + j] * rh[j];
     double cand = lbr ? std::tanh(ax + (double)w->bh[i] + r[i] * au) : std::tanh(ax + au + (double)w->bh[i]);
-    double hn = (1.0 - z[i]) * (double)h[i] + z[i] * cand;
+    double hn = rnn ? sigmoid(ax + au + (double)w->bh[i]) : (1.0 - z[i]) * (double)h[i] + z[i] * cand;
     if (out64) out64[i] = hn;
     if (out32) out32[i] = (float)hn;
   }

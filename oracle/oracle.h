@@ -18,7 +18,7 @@ extern "C" {
 #endif
 
 enum { ORC_KEY_OFF = 0, ORC_KEY_ROUND = 1, ORC_KEY_SIGN = 2 };
-enum { ORC_CELL_GRU = 0, ORC_CELL_GRU_LBR = 1 };   /* Chung GRU (reading 1) / linear-before-reset */
+enum { ORC_CELL_GRU = 0, ORC_CELL_GRU_LBR = 1, ORC_CELL_RNN = 2 };   /* Chung GRU / linear-before-reset / Elman */
 enum { ORC_QHIT = 0, ORC_SHIT = 1, ORC_MISS = 2, ORC_INVALID = 255 };
 enum { ORC_OK = 0, ORC_E_INVALID_ARG = 1, ORC_E_DIMENSION = 2, ORC_E_NONFINITE = 3,
        ORC_E_VOCAB = 4, ORC_E_HISTORY = 5, ORC_E_CAPACITY = 6 };

@@ -15,7 +15,7 @@ namespace rnnlm_host {
 // Tensor-core path (k_gru_tc.cu).  Returns kernels launched, or -1 if the
 // configuration is not supported by it.
 int gru_tc_supported(uint32_t E, uint32_t H);
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int lbr, void **state_out);
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int cell, void **state_out);
 void gru_tc_release(void *state);
 int gru_tc_bind(void *state, void *rh, uint32_t bmax);
 int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s,
@@ -182,7 +182,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   if (c.key_mode == RNNLM_KEY_ROUND && (c.round_digits < 1 || c.round_digits > 4))
     return RNNLM_E_INVALID_ARG;
   if (c.math > RNNLM_MATH_BF16) return RNNLM_E_INVALID_ARG;
-  if (c.cell > RNNLM_CELL_GRU_LBR) return RNNLM_E_INVALID_ARG;
+  if (c.cell > RNNLM_CELL_RNN) return RNNLM_E_INVALID_ARG;
   const bool tc = c.math != RNNLM_MATH_FP32;           // tcgen05 path (BF16 or TF32 operands)
   if (tc && !rnnlm_host::gru_tc_supported(c.embed, c.hidden))
     return RNNLM_E_DIMENSION;
@@ -260,7 +260,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
       chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.emb16), w->emb, V * E));
     if (st == RNNLM_OK &&
         rnnlm_host::gru_tc_prepare(w, c.embed, c.hidden, c.math == RNNLM_MATH_TF32,
-                                   c.cell == RNNLM_CELL_GRU_LBR, &h->tc) != 0)
+                                   (int)c.cell, &h->tc) != 0)
       st = RNNLM_E_OOM;
   }
   // ---- pools

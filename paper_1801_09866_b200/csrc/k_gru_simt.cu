@@ -14,9 +14,10 @@
 //            Wh x + bh.
 //   phase 2: [Q, H] x [H, H] for Uh (r . h); epilogue: tanh, the update,
 //            the new fp32 state (and its bf16 shadow when the engine keeps one).
-// Cell variant GRU_LBR: phase 1 stores r instead of r . h,
-// phase 2 contracts the parent state h and applies r after: c = tanh(Wh x +
-// bh + r . (Uh h)).
+// Cell variants: GRU_LBR -- phase 1 stores r instead of
+// r . h, phase 2 contracts the parent state h and applies r after:
+// c = tanh(Wh x + bh + r . (Uh h)); RNN -- phase 2 contracts h, the new state
+// is sigma(Wh x + bh + Uh h) (phase 1's z, r are not used).
 // Register-tiled FFMA (64 x 64 tile, 4 x 4 per thread) with A rows gathered
 // through row_word / row_src; fp32 accumulation.  This is the 1e-5 path; the
 // tensor-core path lives in k_gru_tc.cu.
@@ -152,8 +153,8 @@ __global__ void __launch_bounds__(NT) k_gru2_f32(Params P) {
     const uint32_t lrow = r0 + lr;
     const bool rv = lrow < Q;
     // A operand: r . h (GRU) or the parent state h itself (LBR: Uh h, reset applied after)
-    const bool lbr = P.cell == RNNLM_CELL_GRU_LBR;
-    const float *as = lbr ? P.state + (size_t)(rv ? P.row_src[lrow] : 0) * H : P.g_rh + (size_t)(rv ? lrow : 0) * H;
+    const bool lbr = P.cell == RNNLM_CELL_GRU_LBR, rnn = P.cell == RNNLM_CELL_RNN;
+    const float *as = (lbr || rnn) ? P.state + (size_t)(rv ? P.row_src[lrow] : 0) * H : P.g_rh + (size_t)(rv ? lrow : 0) * H;
     for (uint32_t k0 = 0; k0 < H; k0 += BK) {
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
       if (rv && k0 + lk < H) a = *reinterpret_cast<const float4 *>(as + k0 + lk);
@@ -192,9 +193,14 @@ __global__ void __launch_bounds__(NT) k_gru2_f32(Params P) {
         const uint32_t u = u0 + j;
         if (u >= H) continue;
         const size_t o = (size_t)row * H + u;
-        const float z = P.g_z[o];
-        const float c = tanhf(P.g_wxb[o] + (lbr ? P.g_rh[o] * acc[i][j] : acc[i][j]));
-        const float hn = (1.0f - z) * hp[u] + z * c;
+        float hn;
+        if (rnn) {                                           // vanilla RNN: sigma(Wh x + bh + Uh h)
+          hn = sigmoidf_(P.g_wxb[o] + acc[i][j]);
+        } else {
+          const float z = P.g_z[o];
+          const float c = tanhf(P.g_wxb[o] + (lbr ? P.g_rh[o] * acc[i][j] : acc[i][j]));
+          hn = (1.0f - z) * hp[u] + z * c;
+        }
         P.state[(size_t)dst * H + u] = hn;
       }
     }

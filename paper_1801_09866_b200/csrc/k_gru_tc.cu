@@ -587,6 +587,37 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
   }
   if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
 }
+// Vanilla-RNN epilogue of one thread (cell variant): row
+// `row`, 128 units from n0; accumulator = Wh x + Uh h; h' = sigma(. + bh),
+// the new fp32 state (staged row store) and its compression code.
+__device__ __forceinline__ void epi_rnn(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid, uint32_t n0,
+                                        uint8_t *stg, uint32_t lane) {
+  const uint32_t dst = valid ? a.row_dst[row] : NONE;
+  const bool live = dst != NONE;
+  float *hout = live ? a.state_out + (size_t)dst * a.H + n0 : nullptr;
+  uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && live) ? a.codes + (size_t)dst * a.cstride : nullptr;
+  unsigned long long hs = 0;
+  uint32_t signacc = 0;
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {                  // 4 chunks of 32 units
+    float v[32], b[32];
+    tmem_ld32(tbase + c * 32, v);
+    ld_bias16(a.bh + n0 + c * 32, b);
+    ld_bias16(a.bh + n0 + c * 32 + 16, b + 16);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = sigm(v[j] + b[j]);
+    __syncwarp();
+    put_row_f32(stg, lane, v);
+    coop_store<128>(stg, hout ? hout + c * 32 : nullptr, lane);
+    if (a.cache && live) {
+      hs += encode16(a, v, n0 + c * 32, code, signacc);
+      hs += encode16(a, v + 16, n0 + c * 32 + 16, code, signacc);
+    }
+  }
+  if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
+}
+
 // LBR epilogue of one thread (cell variant): row `row`, the 32
 // units [64 ub + 32 half, +32) of the tile's 64; accumulator columns: Wh x
 // at 0-63, z at 64-127, r at 128-191, Uh h at 192-255 (tacc = the lane
@@ -645,7 +676,7 @@ __device__ __forceinline__ void epi_lbr(const TcArgs &a, uint32_t tacc, uint32_t
 // warp 0: TMA producer (waits on the phase-1 counter before a phase-2 tile);
 // warp 1: TMEM allocation + MMA issue; warps 2-9: epilogue, TMEM lane quarter
 // = warp % 4, column half = (warp - 2) / 4.
-template <typename T, bool LBR>
+template <typename T, int CELL>
 __global__ void __maxnreg__(GRU_MAXREG)
     k_gru_tc(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1,
              const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2,
@@ -653,8 +684,10 @@ __global__ void __maxnreg__(GRU_MAXREG)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Smem m = carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // GRU: per M-tile nub phase-1 + H/256 phase-2 tiles; LBR: H/64 one-phase tiles
-  const uint32_t n1 = LBR ? a.H / 64 : a.nub, n2 = LBR ? 0u : a.H / BN;
+  // GRU: per M-tile nub phase-1 + H/256 phase-2 tiles; LBR: H/64 one-phase
+  // tiles over W3; RNN: H/256 one-phase tiles of A1 x W2 = [Wh | Uh]
+  constexpr bool LBR = CELL == RNNLM_CELL_GRU_LBR, RNN = CELL == RNNLM_CELL_RNN;
+  const uint32_t n1 = LBR ? a.H / 64 : (RNN ? a.H / BN : a.nub), n2 = (LBR || RNN) ? 0u : a.H / BN;
   const uint32_t b_bytes = LBR ? 192 * 128 : B_BYTES;
   constexpr int BKE = Op<T>::BKE;
   const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE;
@@ -749,7 +782,12 @@ __global__ void __maxnreg__(GRU_MAXREG)
         }
         continue;
       }
-      if constexpr (LBR) {
+      if constexpr (RNN) {
+        epi_rnn(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
+        tc_fence_before();
+        mbar_arrive(&m.tempty[acc]);
+        b1 += clock64() - t0;
+      } else if constexpr (LBR) {
         epi_lbr(a, tbase - half * (BN / 2), row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
@@ -1098,6 +1136,7 @@ struct TcState {
   unsigned long long *prof = nullptr;
   float *bzr = nullptr, *bh = nullptr;
   bool lbr = false;                // cell GRU_LBR: one-phase tiles over W3
+  bool rnn = false;                // cell RNN: one-phase tiles over W2 = [Wh | Uh]
   void *w3 = nullptr;
   float *bz = nullptr, *br = nullptr;
   CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h, map_w3;
@@ -1181,11 +1220,13 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
          cudaMemcpy(t->w2, w2.data(), w2.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
 }
 
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int lbr, void **state_out) {
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int cell, void **state_out) {
   *state_out = nullptr;
   TcState *t = new TcState;
-  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0; t->lbr = lbr != 0;
-  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = (t->tf32 || t->lbr) ? 0 : atoi(e);   // pair: bf16 GRU only
+  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0;
+  t->lbr = cell == RNNLM_CELL_GRU_LBR;
+  t->rnn = cell == RNNLM_CELL_RNN;
+  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = (t->tf32 || cell) ? 0 : atoi(e);   // pair: bf16 GRU only
   if (const char *e = getenv("RNNLM_TC_DIAG")) t->diag = (uint32_t)atoi(e);
   const size_t K1 = E + H;
   std::vector<float> bzr((size_t)2 * H), bh(H);
@@ -1212,14 +1253,12 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int
   if (!t->tf32)
     ok = ok && make_map(&t->map_w1h, t->w1, K1, 2 * (uint64_t)H, BN / 2) &&
          make_map(&t->map_w2h, t->w2, K1, H, BN / 2);
-  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)SMEM) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)SMEM) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)SMEM) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PAIR) == cudaSuccess;
   *state_out = t;
   if (!ok) {
@@ -1286,7 +1325,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     a.prof = t->prof;
   }
   const uint32_t mt = (max_rows + BM - 1) / BM;
-  uint32_t g1 = t->lbr ? mt * (P.H / 64) : mt * (t->nub + P.H / BN);
+  uint32_t g1 = t->lbr ? mt * (P.H / 64) : (t->rnn ? mt * (P.H / BN) : mt * (t->nub + P.H / BN));
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
   uint32_t gg = (max_rows + 7) / 8;
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
@@ -1302,11 +1341,14 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
                        t->map_w2h, a);
   } else {
     if (t->lbr) {
-      if (t->tf32) launch_pdl(k_gru_tc<float, true>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
-      else launch_pdl(k_gru_tc<__nv_bfloat16, true>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
+      if (t->tf32) launch_pdl(k_gru_tc<float, 1>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
+      else launch_pdl(k_gru_tc<__nv_bfloat16, 1>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
+    } else if (t->rnn) {
+      if (t->tf32) launch_pdl(k_gru_tc<float, 2>, g1, THREADS, SMEM, s, t->map_a1, t->map_w2, t->map_rh, t->map_w2, a);
+      else launch_pdl(k_gru_tc<__nv_bfloat16, 2>, g1, THREADS, SMEM, s, t->map_a1, t->map_w2, t->map_rh, t->map_w2, a);
     } else {
-      if (t->tf32) launch_pdl(k_gru_tc<float, false>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
-      else launch_pdl(k_gru_tc<__nv_bfloat16, false>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+      if (t->tf32) launch_pdl(k_gru_tc<float, 0>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
+      else launch_pdl(k_gru_tc<__nv_bfloat16, 0>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
     }
   }
   if (ev_phase1) cudaEventRecord(ev_phase1, s);

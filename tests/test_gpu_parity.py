@@ -460,3 +460,23 @@ def test_offline_level_batches_equal_online(math):
         a = on.read_states(s, child_on[msk]).cpu().numpy()
         b = off.read_states(s, child_off[msk]).cpu().numpy()
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("math", [MATH_FP32, MATH_BF16, MATH_TF32])
+def test_rnn_cell_moderate(math):
+    """Vanilla-RNN cell (h' = sigma(Wh x + Uh h + bh)) on every math
+    path: FP32 SIMT (phase 2 contracts h), BF16 / TF32 one-phase tcgen05 tiles
+    of A1 x [Wh | Uh]; lossy sign keys, codes bit-exact."""
+    d, m = model("moderate")
+    wl = generate_workload(1, 30, 256, d.V, seed=31)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=O.CELL_RNN)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
+    assert rep["miss"] > 200
+
+
+def test_rnn_cell_large_full_tiles():
+    d, m = model("large")
+    wl = generate_workload(1, 2, 2048, d.V, seed=5)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16, cache=False, cell=O.CELL_RNN)
+    rep = replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+    assert rep["miss"] == wl.n_total

@@ -359,3 +359,40 @@ def test_gru_cells_hand_case_reset_placement():
         out = O.gru(O.make_config(2, E, H, 1, 1, cell=cell), m, x, h, fp64=True)
         assert out[0] == pytest.approx(0.125 + 0.5 * c0, abs=1e-15)
         assert out[1] == pytest.approx(-0.375, abs=1e-15)
+
+
+def test_rnn_cell_hand_case():
+    """Vanilla RNN cell (Elman, logistic): H = 2, E = 1, Wh = [[a], [0]],
+    Uh = [[0, 1], [0, 0]], bh = (0, b1), every GRU gate weight set to junk
+    (must be ignored): h'_0 = sigma(a x + h_1), h'_1 = sigma(b1)."""
+    E, H = 1, 2
+    rng = np.random.default_rng(3)
+    m = {k: rng.uniform(-5, 5, s).astype(np.float32) for k, s in
+         dict(Wz=(H, E), Uz=(H, H), bz=(H,), Wr=(H, E), Ur=(H, H), br=(H,)).items()}
+    m.update(Wh=np.array([[0.75], [0.0]], np.float32), Uh=np.array([[0.0, 1.0], [0.0, 0.0]], np.float32),
+             bh=np.array([0.0, -0.5], np.float32), emb=np.zeros((2, E), np.float32),
+             nce_w=np.zeros((2, H), np.float32), nce_b=np.zeros(2, np.float32), maxent=np.zeros(2, np.float32))
+    x = np.array([0.5], np.float32)
+    h = np.array([0.1, -0.25], np.float32)
+    out = O.gru(O.make_config(2, E, H, 1, 1, cell=O.CELL_RNN), m, x, h, fp64=True)
+    sig = lambda a: 1.0 / (1.0 + math.exp(-a))
+    assert out[0] == pytest.approx(sig(0.375 - 0.25), abs=1e-15)
+    assert out[1] == pytest.approx(sig(-0.5), abs=1e-15)
+
+
+def test_rnn_cell_matches_torch_functional():
+    """The Elman layer through torch's library linear + sigmoid (E != H)."""
+    E, H = 6, 4
+    rng = np.random.default_rng(12)
+    m = {k: rng.uniform(-1, 1, s).astype(np.float32) for k, s in
+         dict(Wz=(H, E), Uz=(H, H), bz=(H,), Wr=(H, E), Ur=(H, H), br=(H,), Wh=(H, E), Uh=(H, H),
+              bh=(H,)).items()}
+    m.update(emb=np.zeros((2, E), np.float32), nce_w=np.zeros((2, H), np.float32),
+             nce_b=np.zeros(2, np.float32), maxent=np.zeros(2, np.float32))
+    x = rng.uniform(-1, 1, E).astype(np.float32)
+    h = rng.uniform(-1, 1, H).astype(np.float32)
+    ours = O.gru(O.make_config(2, E, H, 1, 1, cell=O.CELL_RNN), m, x, h, fp64=True)
+    t = lambda a: torch.tensor(a, dtype=torch.float64)
+    ref = torch.sigmoid(torch.nn.functional.linear(t(x), t(m["Wh"]), t(m["bh"])) +
+                        torch.nn.functional.linear(t(h), t(m["Uh"]))).numpy()
+    np.testing.assert_allclose(ours, ref, atol=1e-13, rtol=0)
