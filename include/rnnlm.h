@@ -83,7 +83,7 @@ typedef enum {
   RNNLM_MATH_FP32 = 0,      /* FP32 FFMA (SIMT) */
   RNNLM_MATH_TF32 = 1,      /* fp32 operands read as TF32, fp32 accumulation on tcgen05 tensor cores */
   RNNLM_MATH_BF16 = 2       /* bf16 operands, fp32 accumulation on tcgen05 tensor cores */
-  /* The two tensor-core modes need E % 64 == 0 and H % 256 == 0 (else
+  /* The two tensor-core modes need E % 64 == 0 and H % 128 == 0 (else
    * rnnlm_create returns RNNLM_E_DIMENSION).  BF16 stores bf16 copies of E
    * and the gate weights (and of nce_w when every entry is bf16-exact); TF32
    * keeps every parameter fp32. */

@@ -126,6 +126,7 @@ struct TcArgs {
   // cell variant GRU_LBR: one phase, tiles of 64 units x
   // (z | r | Wh x | Uh h), B = W3 [(H/64) x 192 rows][E+H]
   const float *bz, *br;            // [H] (LBR epilogue)
+  uint32_t bn2;                    // units per phase-2 (and RNN) tile: 256, or 128 when H % 256 != 0
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
   float round_scale;
@@ -286,16 +287,20 @@ __device__ __forceinline__ uint32_t next_tile(const Smem &m, uint32_t it, bool r
 // every K-chunk is ONE N = 192 MMA: x chunks into columns 0-191, h chunks
 // into columns 64-255 (no product of a zero block).  The first h K-step
 // splits into N = 128 (accumulate into z | r) + N = 64 (initialise Uh h).
+// Phase-2 (and RNN) tiles are 128 units wide (N = 128) when H % 256 != 0.
 template <typename T, bool LBR>
 __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, uint32_t kx, int lane,
-                                         uint32_t diag, unsigned long long *prof) {
+                                         uint32_t diag, unsigned long long *prof, bool narrow, bool rnn,
+                                         uint32_t mt, uint32_t n1, uint32_t n2, uint32_t L) {
   uint32_t stage = 0, phase = 0;
-  const uint32_t id = idesc_of(Op<T>::FMT, BM, BN);
+  const uint32_t id256 = idesc_of(Op<T>::FMT, BM, BN);
   const uint32_t id192 = idesc_of(Op<T>::FMT, BM, 192), id128 = idesc_of(Op<T>::FMT, BM, 128),
                  id64 = idesc_of(Op<T>::FMT, BM, 64);
   unsigned long long w_full = 0, w_tempty = 0, t0;
   for (uint32_t it = 0;; ++it) {
-    if (next_tile(m, it, lane == 0) == NO_TILE) break;
+    const uint32_t tid = next_tile(m, it, lane == 0);
+    if (tid == NO_TILE) break;
+    const uint32_t id = (narrow && (rnn || tile_of(tid, mt, n1, n2, L).kind == 1)) ? id128 : id256;
     const uint32_t acc = it & 1;
     t0 = clock64();
     mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
@@ -550,7 +555,7 @@ __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint
 
 // Phase-2 epilogue of one thread: row `row`, 128 units starting at n0.
 __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid,
-                                           uint32_t n0, uint8_t *stg, uint32_t lane) {
+                                           uint32_t n0, uint32_t units, uint8_t *stg, uint32_t lane) {
   const uint32_t dst = valid ? a.row_dst[row] : NONE;
   const bool live = dst != NONE;
   const float *hp = live ? a.state + (size_t)a.row_src[row] * a.H + n0 : nullptr;
@@ -560,7 +565,7 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
   unsigned long long hs = 0;
   uint32_t signacc = 0;
 #pragma unroll 1
-  for (int c = 0; c < BN / 64; ++c) {                  // 4 chunks of 32 units
+  for (uint32_t c = 0; c < units / 32; ++c) {           // chunks of 32 units
     float v[32], b[32], z[32], h[32];
     tmem_ld32(tbase + c * 32, v);
     if (live) {
@@ -591,7 +596,7 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
 // `row`, 128 units from n0; accumulator = Wh x + Uh h; h' = sigma(. + bh),
 // the new fp32 state (staged row store) and its compression code.
 __device__ __forceinline__ void epi_rnn(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid, uint32_t n0,
-                                        uint8_t *stg, uint32_t lane) {
+                                        uint32_t units, uint8_t *stg, uint32_t lane) {
   const uint32_t dst = valid ? a.row_dst[row] : NONE;
   const bool live = dst != NONE;
   float *hout = live ? a.state_out + (size_t)dst * a.H + n0 : nullptr;
@@ -599,7 +604,7 @@ __device__ __forceinline__ void epi_rnn(const TcArgs &a, uint32_t tbase, uint32_
   unsigned long long hs = 0;
   uint32_t signacc = 0;
 #pragma unroll 1
-  for (int c = 0; c < BN / 64; ++c) {                  // 4 chunks of 32 units
+  for (uint32_t c = 0; c < units / 32; ++c) {           // chunks of 32 units
     float v[32], b[32];
     tmem_ld32(tbase + c * 32, v);
     ld_bias16(a.bh + n0 + c * 32, b);
@@ -687,8 +692,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   // GRU: per M-tile nub phase-1 + H/256 phase-2 tiles; LBR: H/64 one-phase
   // tiles over W3; RNN: H/256 one-phase tiles of A1 x W2 = [Wh | Uh]
   constexpr bool LBR = CELL == RNNLM_CELL_GRU_LBR, RNN = CELL == RNNLM_CELL_RNN;
-  const uint32_t n1 = LBR ? a.H / 64 : (RNN ? a.H / BN : a.nub), n2 = (LBR || RNN) ? 0u : a.H / BN;
-  const uint32_t b_bytes = LBR ? 192 * 128 : B_BYTES;
+  const uint32_t n1 = LBR ? a.H / 64 : (RNN ? a.H / a.bn2 : a.nub), n2 = (LBR || RNN) ? 0u : a.H / a.bn2;
   constexpr int BKE = Op<T>::BKE;
   const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE;
   const uint32_t target = n1 * EPI_WARPS;               // phase-1 arrivals per M-tile
@@ -735,15 +739,17 @@ __global__ void __maxnreg__(GRU_MAXREG)
             if (++stage == ST) { stage = 0; phase ^= 1; }
             continue;
           }
-          mbar_expect_tx(&m.full[stage], A_BYTES + b_bytes);
+          // B rows this tile loads: 192 (LBR), bn2 (phase 2, RNN), 256 (phase 1)
+          const uint32_t b_rows = LBR ? 192u : ((x.kind == 1 || RNN) ? a.bn2 : (uint32_t)BN);
+          mbar_expect_tx(&m.full[stage], A_BYTES + b_rows * 128);
           const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * B_BYTES);
           if (x.kind == 0) {
             tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BKE), (int)m0);
-            tma_load_2d(dB, &map_w1, &m.full[stage], (int)(kc * BKE), (int)(x.j * (LBR ? 192u : BN)));
+            tma_load_2d(dB, &map_w1, &m.full[stage], (int)(kc * BKE), (int)(x.j * b_rows));
           } else {
             if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BKE), (int)m0);
             else tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BKE), (int)m0);
-            tma_load_2d(dB, &map_w2, &m.full[stage], (int)(kc * BKE), (int)(x.j * BN));
+            tma_load_2d(dB, &map_w2, &m.full[stage], (int)(kc * BKE), (int)(x.j * b_rows));
           }
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
@@ -751,7 +757,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
       if (prof) { prof[0] = w_empty; prof[1] = w_dep; }
     }
   } else if (warp == 1) {
-    mma_loop<T, LBR>(m, tmem_base, KC, kx, lane, a.diag, prof);
+    mma_loop<T, LBR>(m, tmem_base, KC, kx, lane, a.diag, prof, a.bn2 != BN, RNN, mt, n1, n2, L);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -769,7 +775,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
       tc_fence_after();
       const uint32_t row = x.m * BM + r_in;
       const bool valid = row < Q;
-      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2);
+      // column half of the tile: 128 of 256 (phase 1 / LBR / wide tiles) or 64 of 128
+      const uint32_t hw = (x.kind == 1 || RNN) ? a.bn2 / 2 : (uint32_t)(BN / 2);
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16) + half * hw;
       if (a.diag == 3 || a.diag == 4) {                   // timing only: no epilogue work
         float v[16];
         tmem_ld16(tbase, v);
@@ -783,7 +791,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
         continue;
       }
       if constexpr (RNN) {
-        epi_rnn(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
+        epi_rnn(a, tbase, row, valid, x.j * a.bn2 + half * hw, hw, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
         b1 += clock64() - t0;
@@ -806,7 +814,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
         b1 += clock64() - t0;
       } else {
         wait_phase1(a.done1 + x.m, target);               // acquire z of this M-tile
-        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), m.stg + (warp - 2) * STG_BYTES, lane);
+        epi_phase2(a, tbase, row, valid, x.j * a.bn2 + half * hw, hw, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
         b2 += clock64() - t0;
@@ -1089,7 +1097,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
         epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j, stg, lane);
       } else {
         wait_phase1(a.done1 + x.m, target);
-        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), stg, lane);
+        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), BN / 2, stg, lane);
       }
       tc_fence_before();
       __syncwarp();
@@ -1149,7 +1157,7 @@ namespace rnnlm_host {
 using namespace rnnlm_tc;
 
 int gru_tc_supported(uint32_t E, uint32_t H) {
-  return E % BK == 0 && H % BN == 0 && E >= BK && H >= BN;
+  return E % BK == 0 && H % UB == 0 && E >= BK && H >= UB;      // phase-2 tiles narrow to 128 units
 }
 
 template <typename T>
@@ -1249,7 +1257,8 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int
   ok = ok && cudaMemcpy(t->bzr, bzr.data(), bzr.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bh, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && make_map(&t->map_w1, t->w1, K1, 2 * (uint64_t)H, BN, t->tf32) &&
-       make_map(&t->map_w2, t->w2, K1, H, BN, t->tf32);
+       make_map(&t->map_w2, t->w2, K1, H, H % BN ? UB : BN, t->tf32);
+  if (H % BN) t->pair = 0;        // the CTA pair keeps 256-unit phase-2 tiles
   if (!t->tf32)
     ok = ok && make_map(&t->map_w1h, t->w1, K1, 2 * (uint64_t)H, BN / 2) &&
          make_map(&t->map_w2h, t->w2, K1, H, BN / 2);
@@ -1318,6 +1327,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.lag = 48;
   a.diag = t->diag;
   a.bz = t->bz; a.br = t->br;
+  a.bn2 = P.H % BN ? UB : BN;
   a.prof = nullptr;
   if (t->diag == 5) {
     if (!t->prof) cudaMalloc(&t->prof, 1024 * 16 * sizeof(unsigned long long));
@@ -1325,7 +1335,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     a.prof = t->prof;
   }
   const uint32_t mt = (max_rows + BM - 1) / BM;
-  uint32_t g1 = t->lbr ? mt * (P.H / 64) : (t->rnn ? mt * (P.H / BN) : mt * (t->nub + P.H / BN));
+  uint32_t g1 = t->lbr ? mt * (P.H / 64) : (t->rnn ? mt * (P.H / a.bn2) : mt * (t->nub + P.H / a.bn2));
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
   uint32_t gg = (max_rows + 7) / 8;
   if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;

@@ -480,3 +480,18 @@ def test_rnn_cell_large_full_tiles():
     eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16, cache=False, cell=O.CELL_RNN)
     rep = replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
     assert rep["miss"] == wl.n_total
+
+
+# ---------------------------------------------------------------- the hidden sizes of the paper's Fig. 4
+@pytest.mark.parametrize("H", [128, 512])
+@pytest.mark.parametrize("cell", [0, O.CELL_GRU_LBR, O.CELL_RNN])
+@pytest.mark.parametrize("math", [MATH_BF16, MATH_TF32])
+def test_fig4_hidden_sizes_tensor_core(H, cell, math):
+    """H = 128 (phase-2 / RNN tiles narrow to 128 units, N = 128) and H = 512 on
+    the tensor-core paths, every cell, E = H, lossy sign keys."""
+    d = ModelDims(V=5000, E=H, H=H, maxent_log2=18, N=4)
+    m = generate_model(d, seed=77)
+    wl = generate_workload(1, 12, 300, d.V, seed=13)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=cell)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
+    assert rep["miss"] > 100
