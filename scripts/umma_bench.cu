@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(192, 1)
   fence_after();
   if constexpr (PAIR == 2) cluster_sync();
   const uint32_t tb = *tbase_s;
+  const long long clk0 = clock64();
   const int mt = M / (BM * PAIR), nt = N / BN, KC = K / BK;
   const int ntiles = mt * nt;
   const int unit = blockIdx.x / PAIR, nunits = gridDim.x / PAIR;
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   fence_before();
   __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[(size_t)M * (N / BN)] = (float)(clock64() - clk0);
   if constexpr (PAIR == 2) cluster_sync();
   if (warp == 1) {
     fence_after();
@@ -293,7 +295,7 @@ static void run(const char *name, int M, int N, int K, __nv_bfloat16 *dA, __nv_b
   cfg.dynamicSmemBytes = smem;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaMemset(dout, 0, (size_t)M * (N / BN) * 4));
+  CK(cudaMemset(dout, 0, ((size_t)M * (N / BN) + 1) * 4));
   for (int i = 0; i < 3; ++i) CK(cudaLaunchKernelEx(&cfg, kbench<PAIR, ST, G>, mA, mB, M, N, K, dout, gidx));
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
@@ -307,8 +309,11 @@ static void run(const char *name, int M, int N, int K, __nv_bfloat16 *dA, __nv_b
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   ms /= R;
-  std::vector<float> out((size_t)M * (N / BN));
+  std::vector<float> out((size_t)M * (N / BN) + 1);
   CK(cudaMemcpy(out.data(), dout, out.size() * 4, cudaMemcpyDeviceToHost));
+  const double cycles = out[(size_t)M * (N / BN)];
+  // per-cycle efficiency: ideal cycles = MACs per SM / 4096 (8192 flop/clk/SM dense bf16)
+  const double ideal = 2.0 * M * N * K / 8192.0 / nsm;
   double maxerr = 0;
   for (int s = 0; s < 64; ++s) {
     const int row = (int)(((long long)s * 7919) % M), j = s % (N / BN);
@@ -321,8 +326,9 @@ static void run(const char *name, int M, int N, int K, __nv_bfloat16 *dA, __nv_b
     maxerr = fmax(maxerr, fabs(ref - out[(size_t)row * (N / BN) + j]));
   }
   const double tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12;
-  printf("{\"variant\": \"%s\", \"M\": %d, \"N\": %d, \"K\": %d, \"us\": %.2f, \"tflops\": %.1f, \"maxerr\": %.3g}\n",
-         name, M, N, K, ms * 1e3, tf, maxerr);
+  printf("{\"variant\": \"%s\", \"M\": %d, \"N\": %d, \"K\": %d, \"us\": %.2f, \"tflops\": %.1f, \"maxerr\": %.3g, "
+         "\"cycles_cta0\": %.0f, \"clock_ghz\": %.3f, \"per_cycle_eff\": %.3f}\n",
+         name, M, N, K, ms * 1e3, tf, maxerr, cycles, cycles / (ms * 1e-3) / 1e9, ideal / cycles);
 }
 
 int main(int argc, char **argv) {
@@ -343,7 +349,7 @@ int main(int argc, char **argv) {
   float *dout;
   CK(cudaMalloc(&dA, bA.size() * 2));
   CK(cudaMalloc(&dB, bB.size() * 2));
-  CK(cudaMalloc(&dout, (size_t)M * (N / BN) * 4));
+  CK(cudaMalloc(&dout, ((size_t)M * (N / BN) + 1) * 4));
   CK(cudaMemcpy(dA, bA.data(), bA.size() * 2, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, bB.data(), bB.size() * 2, cudaMemcpyHostToDevice));
   run<1, 4>("one-cta st4", M, N, K, dA, dB, dout, hA, hB, nsm);
