@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
       }
       if (lane == 0) atomicExch(&P.tile_status[tile], to_status(excl + agg, ST_INC));
     }
+    __syncwarp();                      // every lane of warp 0 has read s_warp (line above the look-back)
     if (lane == 0) {
       unsigned long long run = 0;
       for (int i = 0; i < SCAN_THREADS / 32; ++i) {
