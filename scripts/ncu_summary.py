@@ -21,6 +21,7 @@ METRICS = {
     "dram_write_bytes": "dram__bytes_write.sum",
     "dram_pct_peak": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "tensor_pipe_pct": "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "tensor_mem_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "tensor_bf16_ops_pct": "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
     "l2_pct_peak": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm_pct_peak": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -108,13 +109,13 @@ def main():
         R = full_report(a.report)
         summary["full"] = R
         md += ["## ncu --set full", "",
-               "| kernel | us | DRAM bytes | DRAM % | L2 % | tensor pipe % | bf16 MMA ops % | SM % | regs | grid |",
+               "| kernel | us | DRAM bytes | DRAM % | L2 % | tensor pipe % | tensor mem (TMEM) active % | SM % | regs | grid |",
                "|---|---|---|---|---|---|---|---|---|---|"]
         for k, lst in R.items():
             for d in lst:
                 md.append(f"| {k} | {d.get('duration_us', 0):.1f} | {d.get('dram_bytes', 0) / 1e6:.1f} MB"
                           f" | {d.get('dram_pct_peak', 0):.1f} | {d.get('l2_pct_peak', 0):.1f}"
-                          f" | {d.get('tensor_pipe_pct', 0):.1f} | {d.get('tensor_bf16_ops_pct', 0):.1f}"
+                          f" | {d.get('tensor_pipe_pct', 0):.1f} | {d.get('tensor_mem_pct', 0):.1f}"
                           f" | {d.get('sm_pct_peak', 0):.1f}"
                           f" | {d.get('registers', 0):.0f} | {d.get('grid', 0):.0f} |")
     json.dump(summary, open(os.path.join(a.out, f"ncu_{a.tag}.json"), "w"), indent=1)
