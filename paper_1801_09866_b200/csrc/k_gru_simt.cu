@@ -18,17 +18,21 @@
 // r . h, phase 2 contracts the parent state h and applies r after:
 // c = tanh(Wh x + bh + r . (Uh h)); RNN -- phase 2 contracts h, the new state
 // is sigma(Wh x + bh + Uh h) (phase 1's z, r are not used).
-// Register-tiled FFMA (64 x 64 tile, 4 x 4 per thread) with A rows gathered
-// through row_word / row_src; fp32 accumulation.  This is the 1e-5 path; the
+// A rows gathered through row_word / row_src; fp32 accumulation.  This is the 1e-5 path; the
 // tensor-core path lives in k_gru_tc.cu.
 #include "rnnlm_impl.cuh"
 
 namespace rnnlm_dev {
 
-constexpr int BM = 64, BU = 64, BK = 16, NT = 256, AST = BM + 4;
+constexpr int BM = 128, BU = 64, BK = 16, NT = 256, AST = BM + 4;
+constexpr int BU2 = 128;                  // phase-2 units per tile
 
 __device__ __forceinline__ float sigmoidf_(float a) { return 1.0f / (1.0f + expf(-a)); }
 
+// Register-tiled FFMA: 128-row tiles, 256 threads as 16 x 16; a thread owns 8
+// rows x (3 gates x 4 units) in phase 1 and 8 rows x 8 units in phase 2, so
+// one K step costs 5 (4) shared loads for 96 (64) FMAs.  The next K slice is
+// fetched from global into registers while the current one is multiplied.
 __global__ void __launch_bounds__(NT) k_gru1_f32(Params P) {
   pdl_entry();
   __shared__ __align__(16) float As[BK][AST];
@@ -37,85 +41,79 @@ __global__ void __launch_bounds__(NT) k_gru1_f32(Params P) {
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const uint32_t ub = blockIdx.x, nub = P.Hp / 64;
   const uint32_t E = P.E, H = P.H;
-  const int lr = tid >> 2, lk = (tid & 3) * 4;
+  const int lr = tid >> 2, lk = (tid & 3) * 4;          // A loader: rows lr, lr + 64; k lk..lk+3
   for (uint32_t rt = blockIdx.y; rt * BM < Q; rt += gridDim.y) {
     const uint32_t r0 = rt * BM;
-    float acc[3][4][4];
+    float acc[3][8][4];
 #pragma unroll
     for (int g = 0; g < 3; ++g)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[g][i][j] = 0.0f;
-    const uint32_t lrow = r0 + lr;
-    const bool rv = lrow < Q;
-    const float *xs = rv ? P.emb + (size_t)P.row_word[lrow] * E : P.emb;
-    const float *hs = rv ? P.state + (size_t)P.row_src[lrow] * H : P.state;
-    // ---- x part: z, r, h gates
-    for (uint32_t k0 = 0; k0 < E; k0 += BK) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rv && k0 + lk < E) a = *reinterpret_cast<const float4 *>(xs + k0 + lk);
-      As[lk + 0][lr] = a.x; As[lk + 1][lr] = a.y; As[lk + 2][lr] = a.z; As[lk + 3][lr] = a.w;
+    const bool rv0 = r0 + lr < Q, rv1 = r0 + lr + 64 < Q;
+    const float *xs0 = rv0 ? P.emb + (size_t)P.row_word[r0 + lr] * E : P.emb;
+    const float *xs1 = rv1 ? P.emb + (size_t)P.row_word[r0 + lr + 64] * E : P.emb;
+    const float *hs0 = rv0 ? P.state + (size_t)P.row_src[r0 + lr] * H : P.state;
+    const float *hs1 = rv1 ? P.state + (size_t)P.row_src[r0 + lr + 64] * H : P.state;
+    // two K ranges: x part (3 gates, w1x) then h part (z, r gates, w1h)
+    for (int part = 0; part < 2; ++part) {
+      const uint32_t K = part == 0 ? E : H;
+      const int ng = part == 0 ? 3 : 2;
+      const float *a0p = part == 0 ? xs0 : hs0, *a1p = part == 0 ? xs1 : hs1;
+      const float *wp = part == 0 ? P.w1x : P.w1h;
+      float4 ra0, ra1, rb[3];
+      auto fetch = [&](uint32_t k0) {
+        ra0 = (rv0 && k0 + lk < K) ? *reinterpret_cast<const float4 *>(a0p + k0 + lk) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ra1 = (rv1 && k0 + lk < K) ? *reinterpret_cast<const float4 *>(a1p + k0 + lk) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int f = tid + i * NT, kk = f / 48, c = (f % 48) * 4;
-        float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k0 + kk < E)
-          b = __ldg(reinterpret_cast<const float4 *>(P.w1x + ((size_t)(k0 + kk) * nub + ub) * 192 + c));
-        *reinterpret_cast<float4 *>(&Bs[kk][c]) = b;
-      }
-      __syncthreads();
+        for (int i = 0; i < 3; ++i) {
+          const int f = tid + i * NT, kk = f / (ng * 16), c = (f % (ng * 16)) * 4;
+          rb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (i < ng && k0 + kk < K)
+            rb[i] = __ldg(reinterpret_cast<const float4 *>(wp + ((size_t)(k0 + kk) * nub + ub) * (ng * 64) + c));
+        }
+      };
+      auto store = [&]() {
+        As[lk + 0][lr] = ra0.x; As[lk + 1][lr] = ra0.y; As[lk + 2][lr] = ra0.z; As[lk + 3][lr] = ra0.w;
+        As[lk + 0][lr + 64] = ra1.x; As[lk + 1][lr + 64] = ra1.y; As[lk + 2][lr + 64] = ra1.z; As[lk + 3][lr + 64] = ra1.w;
 #pragma unroll
-      for (int kk = 0; kk < BK; ++kk) {
-        const float4 a4 = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
-        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+        for (int i = 0; i < 3; ++i) {
+          if (i >= ng) break;
+          const int f = tid + i * NT, kk = f / (ng * 16), c = (f % (ng * 16)) * 4;
+          *reinterpret_cast<float4 *>(&Bs[kk][c]) = rb[i];
+        }
+      };
+      fetch(0);
+      for (uint32_t k0 = 0; k0 < K; k0 += BK) {
+        __syncthreads();
+        store();
+        __syncthreads();
+        if (k0 + BK < K) fetch(k0 + BK);                 // in flight during the FMAs below
 #pragma unroll
-        for (int g = 0; g < 3; ++g) {
-          const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[kk][g * 64 + tx * 4]);
-          const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+        for (int kk = 0; kk < BK; ++kk) {
+          const float4 a4 = *reinterpret_cast<const float4 *>(&As[kk][ty * 8]);
+          const float4 a5 = *reinterpret_cast<const float4 *>(&As[kk][ty * 8 + 4]);
+          const float av[8] = {a4.x, a4.y, a4.z, a4.w, a5.x, a5.y, a5.z, a5.w};
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int g = 0; g < 3; ++g) {
+            if (g >= ng) break;
+            const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[kk][g * 64 + tx * 4]);
+            const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[g][i][j] = fmaf(av[i], bv[j], acc[g][i][j]);
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) acc[g][i][j] = fmaf(av[i], bv[j], acc[g][i][j]);
+          }
         }
       }
       __syncthreads();
     }
-    // ---- h part: z, r gates only (the h gate sees r . h in phase 2)
-    for (uint32_t k0 = 0; k0 < H; k0 += BK) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rv && k0 + lk < H) a = *reinterpret_cast<const float4 *>(hs + k0 + lk);
-      As[lk + 0][lr] = a.x; As[lk + 1][lr] = a.y; As[lk + 2][lr] = a.z; As[lk + 3][lr] = a.w;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int f = tid + i * NT, kk = f / 32, c = (f % 32) * 4;
-        float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k0 + kk < H)
-          b = __ldg(reinterpret_cast<const float4 *>(P.w1h + ((size_t)(k0 + kk) * nub + ub) * 128 + c));
-        *reinterpret_cast<float4 *>(&Bs[kk][c]) = b;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < BK; ++kk) {
-        const float4 a4 = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
-        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[kk][g * 64 + tx * 4]);
-          const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[g][i][j] = fmaf(av[i], bv[j], acc[g][i][j]);
-        }
-      }
-      __syncthreads();
-    }
-    // ---- epilogue: z, r . h, Wh x + bh
+    // ---- epilogue: z, r . h (GRU) or r (LBR), Wh x + bh
     const uint32_t u0 = ub * 64 + tx * 4;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t row = r0 + ty * 4 + i;
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t row = r0 + ty * 8 + i;
       if (row >= Q) continue;
       const float *hp = P.state + (size_t)P.row_src[row] * H;
 #pragma unroll
@@ -137,59 +135,76 @@ __global__ void __launch_bounds__(NT) k_gru1_f32(Params P) {
 __global__ void __launch_bounds__(NT) k_gru2_f32(Params P) {
   pdl_entry();
   __shared__ __align__(16) float As[BK][AST];
-  __shared__ __align__(16) float Bs[BK][BU];
+  __shared__ __align__(16) float Bs[BK][BU2];
   const uint32_t Q = P.counts[1];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const uint32_t ub = blockIdx.x;
   const uint32_t H = P.H;
   const int lr = tid >> 2, lk = (tid & 3) * 4;
+  const bool lbr = P.cell == RNNLM_CELL_GRU_LBR, rnn = P.cell == RNNLM_CELL_RNN;
   for (uint32_t rt = blockIdx.y; rt * BM < Q; rt += gridDim.y) {
     const uint32_t r0 = rt * BM;
-    float acc[4][4];
+    float acc[8][8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-    const uint32_t lrow = r0 + lr;
-    const bool rv = lrow < Q;
-    // A operand: r . h (GRU) or the parent state h itself (LBR: Uh h, reset applied after)
-    const bool lbr = P.cell == RNNLM_CELL_GRU_LBR, rnn = P.cell == RNNLM_CELL_RNN;
-    const float *as = (lbr || rnn) ? P.state + (size_t)(rv ? P.row_src[lrow] : 0) * H : P.g_rh + (size_t)(rv ? lrow : 0) * H;
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    const bool rv0 = r0 + lr < Q, rv1 = r0 + lr + 64 < Q;
+    // A operand: r . h (GRU) or the parent state h itself (LBR: Uh h, reset applied after; RNN)
+    auto arow = [&](bool rv, uint32_t lrow) -> const float * {
+      if (!rv) return P.g_rh;
+      return (lbr || rnn) ? P.state + (size_t)P.row_src[lrow] * H : P.g_rh + (size_t)lrow * H;
+    };
+    const float *as0 = arow(rv0, r0 + lr), *as1 = arow(rv1, r0 + lr + 64);
+    float4 ra0, ra1, rb[2];
+    auto fetch = [&](uint32_t k0) {
+      ra0 = (rv0 && k0 + lk < H) ? *reinterpret_cast<const float4 *>(as0 + k0 + lk) : make_float4(0.f, 0.f, 0.f, 0.f);
+      ra1 = (rv1 && k0 + lk < H) ? *reinterpret_cast<const float4 *>(as1 + k0 + lk) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int f = tid + i * NT, kk = f / 32, c = (f % 32) * 4;
+        const uint32_t u = ub * BU2 + c;
+        rb[i] = (k0 + kk < H && u < P.Hp)
+                    ? __ldg(reinterpret_cast<const float4 *>(P.w2 + (size_t)(k0 + kk) * P.Hp + u))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    fetch(0);
     for (uint32_t k0 = 0; k0 < H; k0 += BK) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rv && k0 + lk < H) a = *reinterpret_cast<const float4 *>(as + k0 + lk);
-      As[lk + 0][lr] = a.x; As[lk + 1][lr] = a.y; As[lk + 2][lr] = a.z; As[lk + 3][lr] = a.w;
-      {
-        const int kk = tid / 16, c = (tid % 16) * 4;
-        float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k0 + kk < H)
-          b = __ldg(reinterpret_cast<const float4 *>(P.w2 + (size_t)(k0 + kk) * P.Hp + ub * 64 + c));
-        *reinterpret_cast<float4 *>(&Bs[kk][c]) = b;
+      __syncthreads();
+      As[lk + 0][lr] = ra0.x; As[lk + 1][lr] = ra0.y; As[lk + 2][lr] = ra0.z; As[lk + 3][lr] = ra0.w;
+      As[lk + 0][lr + 64] = ra1.x; As[lk + 1][lr + 64] = ra1.y; As[lk + 2][lr + 64] = ra1.z; As[lk + 3][lr + 64] = ra1.w;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int f = tid + i * NT, kk = f / 32, c = (f % 32) * 4;
+        *reinterpret_cast<float4 *>(&Bs[kk][c]) = rb[i];
       }
       __syncthreads();
+      if (k0 + BK < H) fetch(k0 + BK);
 #pragma unroll
       for (int kk = 0; kk < BK; ++kk) {
-        const float4 a4 = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
-        const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 4]);
-        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-        const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+        const float4 a4 = *reinterpret_cast<const float4 *>(&As[kk][ty * 8]);
+        const float4 a5 = *reinterpret_cast<const float4 *>(&As[kk][ty * 8 + 4]);
+        const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 8]);
+        const float4 b5 = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 8 + 4]);
+        const float av[8] = {a4.x, a4.y, a4.z, a4.w, a5.x, a5.y, a5.z, a5.w};
+        const float bv[8] = {b4.x, b4.y, b4.z, b4.w, b5.x, b5.y, b5.z, b5.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
       }
-      __syncthreads();
     }
-    const uint32_t u0 = ub * 64 + tx * 4;
+    const uint32_t u0 = ub * BU2 + tx * 8;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t row = r0 + ty * 4 + i;
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t row = r0 + ty * 8 + i;
       if (row >= Q) continue;
       const uint32_t dst = P.row_dst[row];
       if (dst == NONE) continue;
       const float *hp = P.state + (size_t)P.row_src[row] * H;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 8; ++j) {
         const uint32_t u = u0 + j;
         if (u >= H) continue;
         const size_t o = (size_t)row * H + u;
@@ -204,6 +219,7 @@ __global__ void __launch_bounds__(NT) k_gru2_f32(Params P) {
         P.state[(size_t)dst * H + u] = hn;
       }
     }
+    __syncthreads();
   }
 }
 
@@ -220,7 +236,11 @@ int launch_gru_simt(const Params &P, uint32_t max_rows, int num_sms, cudaStream_
   if (gy > tiles) gy = tiles;
   if (gy < 1) gy = 1;
   launch_pdl(k_gru1_f32, dim3(nub, gy), NT, 0, s, P);
-  launch_pdl(k_gru2_f32, dim3(nub, gy), NT, 0, s, P);
+  const uint32_t nub2 = (P.Hp + BU2 - 1) / BU2;
+  uint32_t gy2 = ((uint32_t)num_sms * 2 + nub2 - 1) / nub2;
+  if (gy2 > tiles) gy2 = tiles;
+  if (gy2 < 1) gy2 = 1;
+  launch_pdl(k_gru2_f32, dim3(nub2, gy2), NT, 0, s, P);
   return 2;
 }
 }  // namespace rnnlm_host
