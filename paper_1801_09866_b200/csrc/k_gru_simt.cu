@@ -39,11 +39,12 @@ __global__ void __launch_bounds__(NT) k_gru1_f32(Params P) {
   __shared__ __align__(16) float Bs[BK][3 * BU];
   const uint32_t Q = P.counts[1];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const uint32_t ub = blockIdx.x, nub = P.Hp / 64;
+  const uint32_t nub = P.Hp / 64, ntile = (Q + BM - 1) / BM;
   const uint32_t E = P.E, H = P.H;
   const int lr = tid >> 2, lk = (tid & 3) * 4;          // A loader: rows lr, lr + 64; k lk..lk+3
-  for (uint32_t rt = blockIdx.y; rt * BM < Q; rt += gridDim.y) {
-    const uint32_t r0 = rt * BM;
+  // persistent: (unit block, row tile) work items, unit block fastest (weights stay in L2)
+  for (uint32_t w = blockIdx.x; w < nub * ntile; w += gridDim.x) {
+    const uint32_t ub = w % nub, r0 = (w / nub) * BM;
     float acc[3][8][4];
 #pragma unroll
     for (int g = 0; g < 3; ++g)
@@ -132,18 +133,17 @@ __global__ void __launch_bounds__(NT) k_gru1_f32(Params P) {
   }
 }
 
-__global__ void __launch_bounds__(NT) k_gru2_f32(Params P) {
+__global__ void __launch_bounds__(NT, 2) k_gru2_f32(Params P) {
   pdl_entry();
   __shared__ __align__(16) float As[BK][AST];
   __shared__ __align__(16) float Bs[BK][BU2];
   const uint32_t Q = P.counts[1];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const uint32_t ub = blockIdx.x;
-  const uint32_t H = P.H;
+  const uint32_t H = P.H, nub2 = (P.Hp + BU2 - 1) / BU2, ntile = (Q + BM - 1) / BM;
   const int lr = tid >> 2, lk = (tid & 3) * 4;
   const bool lbr = P.cell == RNNLM_CELL_GRU_LBR, rnn = P.cell == RNNLM_CELL_RNN;
-  for (uint32_t rt = blockIdx.y; rt * BM < Q; rt += gridDim.y) {
-    const uint32_t r0 = rt * BM;
+  for (uint32_t w = blockIdx.x; w < nub2 * ntile; w += gridDim.x) {
+    const uint32_t ub = w % nub2, r0 = (w / nub2) * BM;
     float acc[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -230,17 +230,15 @@ using namespace rnnlm_dev;
 
 int launch_gru_simt(const Params &P, uint32_t max_rows, int num_sms, cudaStream_t s) {
   if (!max_rows) return 0;
-  const uint32_t nub = P.Hp / 64;
+  // persistent grids sized to the resident CTAs (1 per SM for phase 1, 2 for phase 2);
+  // the row count is read on the device, so the grid is capped by the maximum
   const uint32_t tiles = (max_rows + BM - 1) / BM;
-  uint32_t gy = ((uint32_t)num_sms * 2 + nub - 1) / nub;
-  if (gy > tiles) gy = tiles;
-  if (gy < 1) gy = 1;
-  launch_pdl(k_gru1_f32, dim3(nub, gy), NT, 0, s, P);
-  const uint32_t nub2 = (P.Hp + BU2 - 1) / BU2;
-  uint32_t gy2 = ((uint32_t)num_sms * 2 + nub2 - 1) / nub2;
-  if (gy2 > tiles) gy2 = tiles;
-  if (gy2 < 1) gy2 = 1;
-  launch_pdl(k_gru2_f32, dim3(nub2, gy2), NT, 0, s, P);
+  const uint32_t nub = P.Hp / 64, nub2 = (P.Hp + BU2 - 1) / BU2;
+  uint32_t g1 = nub * tiles, g2 = nub2 * tiles;
+  if (g1 > (uint32_t)num_sms) g1 = num_sms;
+  if (g2 > (uint32_t)num_sms * 2) g2 = num_sms * 2;
+  launch_pdl(k_gru1_f32, g1, NT, 0, s, P);
+  launch_pdl(k_gru2_f32, g2, NT, 0, s, P);
   return 2;
 }
 }  // namespace rnnlm_host
