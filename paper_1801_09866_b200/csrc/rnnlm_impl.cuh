@@ -174,7 +174,7 @@ inline cudaError_t launch_pdl_cluster(void (*k)(KArgs...), dim3 grid, dim3 block
 }
 using rnnlm_dev::CallArgs;
 using rnnlm_dev::Params;
-constexpr int SCAN_TILE = 1024;   // queries per look-back tile
+constexpr int SCAN_TILE = 512;    // queries per look-back tile
 int launch_cache_front(const Params &P, const CallArgs &A, cudaStream_t s);   // returns #launches
 int launch_commit(const Params &P, const CallArgs &A, cudaStream_t s);
 int launch_score(const Params &P, const CallArgs &A, int num_sms, cudaStream_t s);
