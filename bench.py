@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--workload", default="multi", choices=list(CONFIGS))
     ap.add_argument("--sessions", type=int, default=None, help="sessions per rank (default: config)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--math", default="bf16", choices=["bf16", "tf32", "fp32"])
+    ap.add_argument("--math", default="bf16", choices=["bf16", "tf32", "fp32", "tf32x3"])
     ap.add_argument("--key", default="sign", help="off | sign | round:K")
     ap.add_argument("--cell", default="gru", choices=["gru", "lbr", "rnn"],
                     help="recurrent cell (SURVEY 8(f)-3): gru = Chung GRU (the paper's), lbr = linear before "
@@ -238,7 +238,7 @@ def run_ours(args):
     wl = generate_workload(S, frames, B_s, V_draw, seed=7 + rank * S,
                            zipf_s=0.0 if args.uniform_words else 1.0)
     mode, k = key_mode(args.key)
-    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32}[args.math]
+    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[args.math]
     n = wl.n_per_frame
     # cache off: every valid query makes a new history (reading 23), so the
     # per-session pool must hold one per query of the run
@@ -359,6 +359,11 @@ def run_ours(args):
     if math == R.MATH_BF16:
         peak = peaks.get("bf16_tflops_sustained", 1400.0)
         bound, peak_src = "tensor", ("measured bf16_tflops_sustained" if peaks else "fallback")
+    elif math == R.MATH_TF32X3:
+        # three TF32 products per useful multiply-add: useful-flop peak = TF32 peak / 3
+        peak = 0.5 * peaks.get("bf16_tflops_sustained", 1400.0) / 3.0
+        bound, peak_src = "tensor", ("measured bf16_tflops_sustained x 0.5 (tf32/bf16 dense ratio) / 3 "
+                                     "(three TF32 products per useful MAC)")
     elif math == R.MATH_TF32:
         # no measured TF32 peak: the measured bf16 peak x the nominal dense ratio (1.125 / 2.25 PF)
         peak = 0.5 * peaks.get("bf16_tflops_sustained", 1400.0)
@@ -379,7 +384,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None,
-        "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32": "f32"}[args.math], "data": "synthetic",
+        "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "tf32x3": "f32 (3xTF32)"}[args.math], "data": "synthetic",
         "config": {"workload": args.workload, "sessions_per_gpu": S, "queries_per_session_frame": B_s,
                    "queries_per_step": total_queries // args.steps, "V": dims.V, "E": dims.E,
                    "H": dims.H, "maxent": f"2^{dims.maxent_log2} {dims.N}-gram", "key": args.key,
@@ -499,7 +504,7 @@ def run_normalizer(args):
     # distinct histories: one utterance, cache off, 2 frames of n/2 queries
     # each -> every query makes a new history (depth 1 and 2)
     wl = generate_workload(1, 2, n // 2, d.V, seed=5)
-    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32}[args.math]
+    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[args.math]
     eng = R.RNNLM.from_dims(d, m, key_mode=R.KEY_SIGN, math=math, cache_enabled=False, num_sessions=1,
                             max_queries_per_call=n, max_histories_per_session=n + 2)
     dev = torch.device("cuda", 0)
@@ -591,7 +596,7 @@ def run_offline(args):
     model = generate_model(dims, seed=1234)
     wl = generate_workload(S, frames, c["B_s"], dims.V, seed=7)
     mode, k = key_mode(args.key)
-    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32}[args.math]
+    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[args.math]
     dev = torch.device("cuda", 0)
     Bmax = 32768
     cap = wl.max_histories_hint()
@@ -640,7 +645,7 @@ def run_offline(args):
         "metric": "RNNLM queries/sec (offline level-batched rescoring of whole utterances)",
         "value": wl.n_total / (ms_off * 1e-3), "unit": "queries/s", "n_gpus": 1, "steps": 1, "warmup": 1,
         "ms_per_step": ms_off, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32": "f32"}[args.math], "data": "synthetic",
+        "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "tf32x3": "f32 (3xTF32)"}[args.math], "data": "synthetic",
         "config": {"workload": args.workload, "sessions": S, "frames": frames, "queries": int(wl.n_total),
                    "key": args.key, "math": args.math, "offline_calls": nb, "online_calls": frames,
                    "mean_queries_per_offline_call": wl.n_total / max(1, nb),

@@ -82,7 +82,10 @@ typedef enum {
 typedef enum {
   RNNLM_MATH_FP32 = 0,      /* FP32 FFMA (SIMT) */
   RNNLM_MATH_TF32 = 1,      /* fp32 operands read as TF32, fp32 accumulation on tcgen05 tensor cores */
-  RNNLM_MATH_BF16 = 2       /* bf16 operands, fp32 accumulation on tcgen05 tensor cores */
+  RNNLM_MATH_BF16 = 2,      /* bf16 operands, fp32 accumulation on tcgen05 tensor cores */
+  RNNLM_MATH_TF32X3 = 3     /* fp32-accurate on tcgen05: a = a_hi + a_lo, w = w_hi + w_lo (TF32 parts),
+                             * a.w ~ a_hi.w_hi + a_hi.w_lo + a_lo.w_hi (three TF32 products, fp32
+                             * accumulation; the 1e-5 path of the FP32 mode at tensor-core rate) */
   /* The two tensor-core modes need E % 64 == 0 and H % 128 == 0 (else
    * rnnlm_create returns RNNLM_E_DIMENSION).  BF16 stores bf16 copies of E
    * and the gate weights (and of nce_w when every entry is bf16-exact); TF32

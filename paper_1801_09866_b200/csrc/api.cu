@@ -15,7 +15,7 @@ namespace rnnlm_host {
 // Tensor-core path (k_gru_tc.cu).  Returns kernels launched, or -1 if the
 // configuration is not supported by it.
 int gru_tc_supported(uint32_t E, uint32_t H);
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int cell, void **state_out);
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int x3, int cell, void **state_out);
 void gru_tc_release(void *state);
 int gru_tc_bind(void *state, void *rh, uint32_t bmax);
 int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s,
@@ -181,7 +181,8 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   if (c.key_mode > RNNLM_KEY_SIGN) return RNNLM_E_INVALID_ARG;
   if (c.key_mode == RNNLM_KEY_ROUND && (c.round_digits < 1 || c.round_digits > 4))
     return RNNLM_E_INVALID_ARG;
-  if (c.math > RNNLM_MATH_BF16) return RNNLM_E_INVALID_ARG;
+  if (c.math > RNNLM_MATH_TF32X3) return RNNLM_E_INVALID_ARG;
+  if (c.math == RNNLM_MATH_TF32X3 && c.cell != RNNLM_CELL_GRU) return RNNLM_E_INVALID_ARG;
   if (c.cell > RNNLM_CELL_RNN) return RNNLM_E_INVALID_ARG;
   const bool tc = c.math != RNNLM_MATH_FP32;           // tcgen05 path (BF16 or TF32 operands)
   if (tc && !rnnlm_host::gru_tc_supported(c.embed, c.hidden))
@@ -259,7 +260,8 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
     if (c.math == RNNLM_MATH_BF16)
       chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.emb16), w->emb, V * E));
     if (st == RNNLM_OK &&
-        rnnlm_host::gru_tc_prepare(w, c.embed, c.hidden, c.math == RNNLM_MATH_TF32,
+        rnnlm_host::gru_tc_prepare(w, c.embed, c.hidden, c.math == RNNLM_MATH_TF32 || c.math == RNNLM_MATH_TF32X3,
+                                   c.math == RNNLM_MATH_TF32X3,
                                    (int)c.cell, &h->tc) != 0)
       st = RNNLM_E_OOM;
   }
@@ -290,7 +292,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   chk(dalloc(h, &P.g_z, (B + 127) / 128 * 128 * H));
   if (c.math == RNNLM_MATH_FP32) chk(dalloc(h, &P.g_wxb, B * H));
   if (c.math == RNNLM_MATH_BF16) chk(dalloc(h, &P.g_rh16, B * H));
-  else chk(dalloc(h, &P.g_rh, B * H));
+  else chk(dalloc(h, &P.g_rh, (c.math == RNNLM_MATH_TF32X3 ? 2 : 1) * B * H));   // 3xTF32: [hi | lo]
   if (st == RNNLM_OK && tc &&
       rnnlm_host::gru_tc_bind(h->tc, c.math == RNNLM_MATH_BF16 ? (void *)P.g_rh16 : (void *)P.g_rh,
                               (uint32_t)B) != 0)

@@ -127,6 +127,8 @@ struct TcArgs {
   // (z | r | Wh x | Uh h), B = W3 [(H/64) x 192 rows][E+H]
   const float *bz, *br;            // [H] (LBR epilogue)
   uint32_t bn2;                    // units per phase-2 (and RNN) tile: 256, or 128 when H % 256 != 0
+  uint32_t x3;                     // RNNLM_MATH_TF32X3 (TF32 instance only): operands as [hi | lo] TF32 parts,
+                                   // three K segments hi.hi, hi.lo, lo.hi (A1 2(E+H), r.h 2H, W 2(E+H) wide)
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
   float round_scale;
@@ -167,10 +169,21 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
       // TF32 operands are the fp32 values themselves (the MMA reads their TF32 part)
       const float4 *x = reinterpret_cast<const float4 *>(a.emb + (size_t)a.row_word[r] * a.E);
       const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
-      float4 *dst = reinterpret_cast<float4 *>(a.a1f + (size_t)r * K1);
       const uint32_t nx = a.E / 4, nh = a.H / 4;
-      for (uint32_t i = lane; i < nx; i += 32) dst[i] = to_tf32(__ldg(x + i));
-      for (uint32_t i = lane; i < nh; i += 32) dst[nx + i] = to_tf32(h[i]);
+      if (!a.x3) {
+        float4 *dst = reinterpret_cast<float4 *>(a.a1f + (size_t)r * K1);
+        for (uint32_t i = lane; i < nx; i += 32) dst[i] = to_tf32(__ldg(x + i));
+        for (uint32_t i = lane; i < nh; i += 32) dst[nx + i] = to_tf32(h[i]);
+      } else {  // [hi(x) | hi(h) | lo(x) | lo(h)], lo = tf32(v - hi)
+        float4 *dst = reinterpret_cast<float4 *>(a.a1f + (size_t)r * 2 * K1);
+        const uint32_t nk = nx + nh;
+        for (uint32_t i = lane; i < nk; i += 32) {
+          const float4 v = i < nx ? __ldg(x + i) : h[i - nx];
+          const float4 hi = to_tf32(v);
+          dst[i] = hi;
+          dst[nk + i] = to_tf32(make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w));
+        }
+      }
     }
   }
 }
@@ -543,11 +556,23 @@ __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint
       if constexpr (sizeof(T) == 2) {
         put_row_bf16(stg, lane, hv);
         coop_store<64>(stg, valid ? a.g_rh16 + (size_t)row * a.H + u0 + c * 32 : nullptr, lane);
-      } else {
+      } else if (!a.x3) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) hv[j] = to_tf32(hv[j]);
         put_row_f32(stg, lane, hv);
         coop_store<128>(stg, valid ? a.g_rhf + (size_t)row * a.H + u0 + c * 32 : nullptr, lane);
+      } else {  // 3xTF32: r.h as [hi | lo] rows of 2H
+        float lo[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float hi = to_tf32(hv[j]);
+          lo[j] = to_tf32(hv[j] - hi);
+          hv[j] = hi;
+        }
+        put_row_f32(stg, lane, hv);
+        coop_store<128>(stg, valid ? a.g_rhf + (size_t)row * 2 * a.H + u0 + c * 32 : nullptr, lane);
+        put_row_f32(stg, lane, lo);
+        coop_store<128>(stg, valid ? a.g_rhf + (size_t)row * 2 * a.H + a.H + u0 + c * 32 : nullptr, lane);
       }
     }
   }
@@ -694,7 +719,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   constexpr bool LBR = CELL == RNNLM_CELL_GRU_LBR, RNN = CELL == RNNLM_CELL_RNN;
   const uint32_t n1 = LBR ? a.H / 64 : (RNN ? a.H / a.bn2 : a.nub), n2 = (LBR || RNN) ? 0u : a.H / a.bn2;
   constexpr int BKE = Op<T>::BKE;
-  const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE;
+  const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE, KCt = a.x3 ? 3 * KC : KC;
   const uint32_t target = n1 * EPI_WARPS;               // phase-1 arrivals per M-tile
   if (threadIdx.x == 0) {
     prefetch_map(&map_a1); prefetch_map(&map_w1); prefetch_map(&map_rh); prefetch_map(&map_w2);
@@ -730,7 +755,11 @@ __global__ void __maxnreg__(GRU_MAXREG)
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         if (prof) prof[9 + x.kind] += 1;
-        for (uint32_t kc = 0; kc < KC; ++kc) {
+        for (uint32_t kc3 = 0; kc3 < KCt; ++kc3) {
+          // 3xTF32: segment 0 = A_hi.W_hi, 1 = A_hi.W_lo, 2 = A_lo.W_hi (column offsets of the lo parts)
+          const uint32_t seg = a.x3 ? kc3 / KC : 0u, kc = a.x3 ? kc3 % KC : kc3;
+          const int a_off = seg == 2 ? (int)(a.E + a.H) : 0, b_off = seg == 1 ? (int)(a.E + a.H) : 0;
+          const int rh_off = seg == 2 ? (int)a.H : 0;
           t0 = clock64();
           mbar_wait(&m.empty[stage], phase ^ 1);
           w_empty += clock64() - t0;
@@ -744,12 +773,12 @@ __global__ void __maxnreg__(GRU_MAXREG)
           mbar_expect_tx(&m.full[stage], A_BYTES + b_rows * 128);
           const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * B_BYTES);
           if (x.kind == 0) {
-            tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BKE), (int)m0);
-            tma_load_2d(dB, &map_w1, &m.full[stage], (int)(kc * BKE), (int)(x.j * b_rows));
+            tma_load_2d(dA, &map_a1, &m.full[stage], a_off + (int)(kc * BKE), (int)m0);
+            tma_load_2d(dB, &map_w1, &m.full[stage], b_off + (int)(kc * BKE), (int)(x.j * b_rows));
           } else {
-            if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], (int)(kc * BKE), (int)m0);
-            else tma_load_2d(dA, &map_rh, &m.full[stage], (int)((kc - kx) * BKE), (int)m0);
-            tma_load_2d(dB, &map_w2, &m.full[stage], (int)(kc * BKE), (int)(x.j * b_rows));
+            if (kc < kx) tma_load_2d(dA, &map_a1, &m.full[stage], a_off + (int)(kc * BKE), (int)m0);
+            else tma_load_2d(dA, &map_rh, &m.full[stage], rh_off + (int)((kc - kx) * BKE), (int)m0);
+            tma_load_2d(dB, &map_w2, &m.full[stage], b_off + (int)(kc * BKE), (int)(x.j * b_rows));
           }
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
@@ -757,7 +786,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
       if (prof) { prof[0] = w_empty; prof[1] = w_dep; }
     }
   } else if (warp == 1) {
-    mma_loop<T, LBR>(m, tmem_base, KC, kx, lane, a.diag, prof, a.bn2 != BN, RNN, mt, n1, n2, L);
+    mma_loop<T, LBR>(m, tmem_base, KCt, kx, lane, a.diag, prof, a.bn2 != BN, RNN, mt, n1, n2, L);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -1143,6 +1172,7 @@ struct TcState {
   uint32_t diag = 0;               // RNNLM_TC_DIAG: timing diagnostics (see TcArgs::diag)
   unsigned long long *prof = nullptr;
   float *bzr = nullptr, *bh = nullptr;
+  bool x3 = false;                 // RNNLM_MATH_TF32X3: [hi | lo] operand rows, three K segments
   bool lbr = false;                // cell GRU_LBR: one-phase tiles over W3
   bool rnn = false;                // cell RNN: one-phase tiles over W2 = [Wh | Uh]
   void *w3 = nullptr;
@@ -1195,8 +1225,9 @@ static bool upload_w3(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H
 
 template <typename T>
 static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H) {
-  const size_t K1 = E + H;
-  std::vector<T> w1((size_t)2 * H * K1), w2((size_t)H * K1);
+  // rows of K1 = E + H operands; with 3xTF32 each row is [hi | lo] (2 K1)
+  const size_t K1 = E + H, RW = t->x3 ? 2 * K1 : K1;
+  std::vector<T> w1((size_t)2 * H * RW), w2((size_t)H * RW);
   auto cv = [](float v) -> T {
     if constexpr (sizeof(T) == 2) {
       return __float2bfloat16_rn(v);
@@ -1211,16 +1242,23 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
   };
   const float *Wg[2] = {w->Wz, w->Wr};
   const float *Ug[2] = {w->Uz, w->Ur};
+  // one weight into (row, k): its (TF32 / bf16) value, and with 3xTF32 the
+  // TF32 part of the remainder at k + K1
+  auto put = [&](T *row, size_t k, float v) {
+    row[k] = cv(v);
+    if constexpr (sizeof(T) == 4)
+      if (t->x3) row[K1 + k] = cv(v - (float)row[k]);
+  };
   for (size_t u = 0; u < H; ++u) {
     const size_t ub = u / UB, uu = u % UB;
     for (int g = 0; g < 2; ++g) {
-      T *row = w1.data() + (ub * BN + g * UB + uu) * K1;
-      for (size_t k = 0; k < E; ++k) row[k] = cv(Wg[g][u * E + k]);
-      for (size_t k = 0; k < H; ++k) row[E + k] = cv(Ug[g][u * H + k]);
+      T *row = w1.data() + (ub * BN + g * UB + uu) * RW;
+      for (size_t k = 0; k < E; ++k) put(row, k, Wg[g][u * E + k]);
+      for (size_t k = 0; k < H; ++k) put(row, E + k, Ug[g][u * H + k]);
     }
-    T *row2 = w2.data() + u * K1;
-    for (size_t k = 0; k < E; ++k) row2[k] = cv(w->Wh[u * E + k]);
-    for (size_t k = 0; k < H; ++k) row2[E + k] = cv(w->Uh[u * H + k]);
+    T *row2 = w2.data() + u * RW;
+    for (size_t k = 0; k < E; ++k) put(row2, k, w->Wh[u * E + k]);
+    for (size_t k = 0; k < H; ++k) put(row2, E + k, w->Uh[u * H + k]);
   }
   return cudaMalloc(&t->w1, w1.size() * sizeof(T)) == cudaSuccess &&
          cudaMalloc(&t->w2, w2.size() * sizeof(T)) == cudaSuccess &&
@@ -1228,10 +1266,10 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
          cudaMemcpy(t->w2, w2.data(), w2.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
 }
 
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int cell, void **state_out) {
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int x3, int cell, void **state_out) {
   *state_out = nullptr;
   TcState *t = new TcState;
-  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0;
+  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0; t->x3 = x3 != 0 && t->tf32;
   t->lbr = cell == RNNLM_CELL_GRU_LBR;
   t->rnn = cell == RNNLM_CELL_RNN;
   if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = (t->tf32 || cell) ? 0 : atoi(e);   // pair: bf16 GRU only
@@ -1256,8 +1294,10 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int
        cudaMalloc(&t->bh, bh.size() * 4) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bzr, bzr.data(), bzr.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bh, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
-  ok = ok && make_map(&t->map_w1, t->w1, K1, 2 * (uint64_t)H, BN, t->tf32) &&
-       make_map(&t->map_w2, t->w2, K1, H, H % BN ? UB : BN, t->tf32);
+  const size_t RW = t->x3 ? 2 * K1 : K1;
+  ok = ok && make_map(&t->map_w1, t->w1, RW, 2 * (uint64_t)H, BN, t->tf32) &&
+       make_map(&t->map_w2, t->w2, RW, H, H % BN ? UB : BN, t->tf32);
+  if (t->x3) t->pair = 0;
   if (H % BN) t->pair = 0;        // the CTA pair keeps 256-unit phase-2 tiles
   if (!t->tf32)
     ok = ok && make_map(&t->map_w1h, t->w1, K1, 2 * (uint64_t)H, BN / 2) &&
@@ -1283,13 +1323,14 @@ int gru_tc_bind(void *state, void *rh, uint32_t bmax) {
   t->rh = rh;
   t->bmax = bmax;
   const size_t es = t->tf32 ? 4 : 2;
-  if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * es) != cudaSuccess ||
+  const size_t xw = t->x3 ? 2 : 1;                     // 3xTF32: [hi | lo] rows
+  if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * es * xw) != cudaSuccess ||
       cudaMalloc(&t->done1, ((size_t)bmax / BM + 4) * sizeof(uint32_t)) != cudaSuccess) {
     (void)cudaGetLastError();
     return -1;
   }
-  t->bound = make_map(&t->map_rh, rh, t->H, bmax, BM, t->tf32) &&
-             make_map(&t->map_a1, t->a1, t->E + t->H, bmax, BM, t->tf32);
+  t->bound = make_map(&t->map_rh, rh, t->H * xw, bmax, BM, t->tf32) &&
+             make_map(&t->map_a1, t->a1, (t->E + t->H) * xw, bmax, BM, t->tf32);
   return t->bound ? 0 : -1;
 }
 
@@ -1328,6 +1369,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.diag = t->diag;
   a.bz = t->bz; a.br = t->br;
   a.bn2 = P.H % BN ? UB : BN;
+  a.x3 = t->x3 ? 1u : 0u;
   a.prof = nullptr;
   if (t->diag == 5) {
     if (!t->prof) cudaMalloc(&t->prof, 1024 * 16 * sizeof(unsigned long long));

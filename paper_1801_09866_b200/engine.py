@@ -14,7 +14,7 @@ from . import _lib
 from ._lib import Config, Stats, Timing, Weights, check
 
 KEY_OFF, KEY_ROUND, KEY_SIGN = 0, 1, 2
-MATH_FP32, MATH_TF32, MATH_BF16 = 0, 1, 2
+MATH_FP32, MATH_TF32, MATH_BF16, MATH_TF32X3 = 0, 1, 2, 3
 CELL_GRU, CELL_GRU_LBR, CELL_RNN = 0, 1, 2  # rnnlm_cell
 QHIT, SHIT, MISS, INVALID = 0, 1, 2, 255
 ALL = 0xFFFFFFFF

@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import oracle as O
-from paper_1801_09866_b200 import (KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32, RNNLM,
+from paper_1801_09866_b200 import (KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32, MATH_TF32X3, RNNLM,
                                    INVALID, MISS, QHIT, SHIT)
 from synth import generate_model, generate_workload, model_dims
 from synth.model import ModelDims
@@ -18,7 +18,8 @@ from tests.parity_util import _dev, replay_compare
 
 pytestmark = pytest.mark.gpu
 
-TOL = {MATH_FP32: 1e-5, MATH_BF16: 1e-3, MATH_TF32: 1e-3}   # 1e-3 for bf16/tf32
+TOL = {MATH_FP32: 1e-5, MATH_BF16: 1e-3, MATH_TF32: 1e-3,    # 1e-3 for bf16/tf32
+       MATH_TF32X3: 1e-5}                                      # fp32-accurate tensor-core mode: the FP32 bar
 _models = {}
 
 
@@ -495,3 +496,40 @@ def test_fig4_hidden_sizes_tensor_core(H, cell, math):
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=cell)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
     assert rep["miss"] > 100
+
+
+# ---------------------------------------------------------------- 3xTF32: fp32-accurate tensor-core GRU
+def test_tf32x3_moderate_fp32_tolerance():
+    """RNNLM_MATH_TF32X3 holds the FP32 path's 1e-5 bar on scores and states
+    (operands split into TF32 hi + lo parts, three products), sign keys with
+    lossy hits, codes bit-exact."""
+    d, m = model("moderate")
+    wl = generate_workload(1, 30, 256, d.V, seed=17)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_TF32X3)
+    rep = replay_compare(eng, orc, wl, tol_score=1e-5, tol_state=1e-5)
+    assert rep["miss"] > 200
+
+
+def test_tf32x3_large_full_tiles_and_ragged():
+    d, m = model("large")
+    wl = generate_workload(1, 2, 2048, d.V, seed=5)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_TF32X3, cache=False)
+    rep = replay_compare(eng, orc, wl, tol_score=1e-5, tol_state=1e-5)
+    assert rep["miss"] == wl.n_total
+    wl = generate_workload(3, 3, 300, d.V, seed=6)
+    eng, orc = pair(d, m, wl, KEY_ROUND, k=2, math=MATH_TF32X3)
+    replay_compare(eng, orc, wl, tol_score=1e-5, tol_state=1e-5)
+
+
+def test_tf32x3_off_grid_weights_accuracy():
+    """Weights NOT on the bf16 grid: the 3xTF32 states sit at FP32-path error
+    (< 1e-5 from the fp64 oracle), far below single TF32."""
+    d = ModelDims(V=1000, E=256, H=256, maxent_log2=16, N=3)
+    m = generate_model(d, seed=3, scale=0.1, bf16_grid=False)
+    wl = generate_workload(1, 6, 256, d.V, seed=8)
+    errs = {}
+    for math in (MATH_TF32, MATH_TF32X3):
+        eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cache=False)
+        errs[math] = replay_compare(eng, orc, wl, tol_score=1e-2, tol_state=1e-2)["max_state_err"]
+    assert errs[MATH_TF32X3] < 1e-5, errs
+    assert errs[MATH_TF32X3] < 0.1 * errs[MATH_TF32], errs
