@@ -221,10 +221,18 @@ def run_ours(args):
     rank, world, local = dist_env()
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    # One rank per GPU.  RNNLM_BENCH_SHARED_GPU=1 (code-path check on a one-GPU
+    # box only: ranks share device 0 and the collectives go through gloo) --
+    # numbers of such a run are not bench values.
+    shared = os.environ.get("RNNLM_BENCH_SHARED_GPU") == "1"
+    local = local % torch.cuda.device_count() if shared else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     c = CONFIGS[args.workload]
     dims = model_dims(args.workload)
     S = sessions_for(args, world)
