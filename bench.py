@@ -446,27 +446,32 @@ def run_e2e(args, eng, wl, dev, world):
     n = wl.n_per_frame
     eng.reset_session()
     import paper_1801_09866_b200 as R
-    h_sess_all = torch.from_numpy(wl.session.view(np.int32).copy()).pin_memory()
-    h_word_all = torch.from_numpy(wl.word.view(np.int32).copy()).pin_memory()
-    h_ref_all = torch.from_numpy(np.ascontiguousarray(wl.parent_ref, dtype=np.int64)).pin_memory()
-    h_score = torch.empty(n, dtype=torch.float32).pin_memory()
-    h_child = torch.empty(n, dtype=torch.int32).pin_memory()
-    d_sess = torch.empty(n, dtype=torch.int32, device=dev)
-    d_word = torch.empty(n, dtype=torch.int32, device=dev)
-    d_ref = torch.empty(n, dtype=torch.int64, device=dev)
+    # per frame one contiguous pinned record block [ref i64 | session u32 | word u32] x n
+    # (16 B per query), so each step's inputs are ONE host->device copy
+    F = wl.frames
+    blk = np.empty((F, 4 * n), dtype=np.int32)
+    for t in range(F):
+        sl = wl.frame_slice(t)
+        blk[t, :2 * n] = np.ascontiguousarray(wl.parent_ref[sl], dtype=np.int64).view(np.int32)
+        blk[t, 2 * n:3 * n] = wl.session[sl].view(np.int32)
+        blk[t, 3 * n:] = wl.word[sl].view(np.int32)
+    h_in_all = torch.from_numpy(blk).pin_memory()
+    h_out = torch.empty(2 * n, dtype=torch.int32).pin_memory()      # [score bits | child]
+    d_in = torch.empty(4 * n, dtype=torch.int32, device=dev)
+    d_ref = d_in[:2 * n].view(torch.int64)
+    d_sess, d_word = d_in[2 * n:3 * n], d_in[3 * n:]
     d_par = torch.empty(n, dtype=torch.int32, device=dev)
-    d_score = torch.empty(n, dtype=torch.float32, device=dev)
+    d_out = torch.empty(2 * n, dtype=torch.int32, device=dev)
+    d_score = d_out[:n].view(torch.float32)
     d_child_log = torch.zeros(wl.n_total, dtype=torch.int32, device=dev)
 
     def host_step(t):
         sl = wl.frame_slice(t)
-        d_sess.copy_(h_sess_all[sl], non_blocking=True)
-        d_ref.copy_(h_ref_all[sl], non_blocking=True)
-        d_word.copy_(h_word_all[sl], non_blocking=True)
+        d_in.copy_(h_in_all[t], non_blocking=True)
         R.resolve_parents(d_ref, d_child_log, d_par)
         eng.query_batch(d_sess, d_par, d_word, score=d_score, child=d_child_log[sl], want_outcome=False)
-        h_score.copy_(d_score, non_blocking=True)
-        h_child.copy_(d_child_log[sl], non_blocking=True)
+        d_out[n:].copy_(d_child_log[sl])
+        h_out.copy_(d_out, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
     F0 = args.prefill
