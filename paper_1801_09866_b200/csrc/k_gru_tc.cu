@@ -1,4 +1,6 @@
-// k_gru_tc.cu -- step (a5), BF16 tensor-core path on sm_100a (tcgen05 + TMEM + TMA).
+// k_gru_tc.cu -- step (a5), tensor-core paths on sm_100a (tcgen05 + TMEM + TMA):
+// BF16 operands (kind::f16), TF32 operands (kind::tf32), and 3xTF32 (kind::tf32
+// over [hi | lo] operand parts in three K segments: the FP32 path's accuracy).
 //
 // The GRU gate contraction of the frame's MISS rows (the
 // frame's (h || x) rows form one block) is a real dense contraction:
@@ -32,6 +34,14 @@
 // accumulator; two 256-column accumulators, so the epilogue of tile i
 // overlaps the MMAs of tile i+1).  Rows >= Q read stale A rows and are
 // discarded.
+//
+// Variants of the same kernel template (k_gru_tc<T, CELL>): CELL 1 = the
+// linear-before-reset GRU (one phase, tiles of 64 units x [Wh x | z | r | Uh h]
+// over W3, see mma_loop), CELL 2 = the vanilla RNN (one phase, A1 x [Wh | Uh]);
+// phase-2 / RNN tiles narrow to 128 units when H % 256 != 0 (a.bn2); the CTA
+// pair k_gru_tc2 (cta_group::2, M = 256) is an opt-in experiment
+// (RNNLM_TC_PAIR=1), and RNNLM_TC_DIAG selects the timing diagnostics of
+// DESIGN.md section 5.
 #include <cuda.h>
 
 #include <cstdio>
