@@ -1375,7 +1375,10 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.cstride = P.cstride; a.round_scale = P.round_scale; a.codes = P.codes; a.codehash = P.codehash;
   a.done1 = t->done1;
   a.tile_ctr = t->done1 + (t->bmax / BM + 2);
-  a.lag = 48;
+  // phase-2 tiles trail their phase-1 tiles by this many M-tiles (RNNLM_TC_LAG); measured:
+  // 24: 504, 48: 521, 96-1000: 530-535 M q/s on the bench workload -- keeping the two
+  // phases apart (each phase's weights hot in L2) beats interleaving them tightly
+  a.lag = getenv("RNNLM_TC_LAG") ? (uint32_t)atoi(getenv("RNNLM_TC_LAG")) : 128u;
   a.diag = t->diag;
   a.bz = t->bz; a.br = t->br;
   a.bn2 = P.H % BN ? UB : BN;
