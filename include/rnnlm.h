@@ -171,6 +171,14 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
                                const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
                                uint32_t *d_child, uint8_t *d_outcome, rnnlm_stream_t stream);
 
+/* Makes `stream` wait until the per-query results of the most recent
+ * rnnlm_query_batch (d_score, d_child, d_outcome) are written.  They are final
+ * before that call's GRU (a5) finishes -- the GRU only produces the new
+ * states later calls read -- so a caller can copy the results out and
+ * prepare the next frame while the state update still runs; the next
+ * rnnlm_query_batch on the same stream is ordered after it as usual. */
+rnnlm_status rnnlm_results_ready(rnnlm_t *h, rnnlm_stream_t stream);
+
 /* Counters of one session (UINT32_MAX = sum over all).  Synchronises the
  * device.  Returns the sticky error (also stored in out->sticky_error). */
 rnnlm_status rnnlm_cache_stats(rnnlm_t *h, uint32_t session, rnnlm_stats *out);

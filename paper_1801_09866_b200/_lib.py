@@ -60,6 +60,7 @@ SIGNATURES = {
     "rnnlm_read_codes": (ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp, _vp]),
     "rnnlm_encode_states": (ctypes.c_int, [_vp, ctypes.c_uint32, _vp, _vp, _vp]),
     "rnnlm_log_normalizer": (ctypes.c_int, [_vp, ctypes.c_uint32, _vp, _vp, _vp, _vp]),
+    "rnnlm_results_ready": (ctypes.c_int, [_vp, _vp]),
     "rnnlm_maxent_indices": (ctypes.c_int, [_vp, ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp]),
     "rnnlm_code_bytes": (ctypes.c_uint32, [_vp]),
     "rnnlm_resolve_parents": (ctypes.c_int, [ctypes.c_uint32, _vp, _vp, _vp, _vp]),

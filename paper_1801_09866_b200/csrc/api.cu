@@ -485,6 +485,13 @@ rnnlm_status rnnlm_maxent_indices(rnnlm_t *h, uint32_t n, const uint32_t *d_sess
   return cuda_status(cudaGetLastError());
 }
 
+rnnlm_status rnnlm_results_ready(rnnlm_t *h, rnnlm_stream_t stream) {
+  if (!h) return RNNLM_E_INVALID_ARG;
+  // every result write (k_commit on the caller's stream before the fork;
+  // k_final, k_score, k_dup_scores on the side stream) precedes ev_join
+  return cuda_status(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), h->ev_join, 0));
+}
+
 rnnlm_status rnnlm_log_normalizer(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
                                   const uint32_t *d_history, float *d_log_z, rnnlm_stream_t stream) {
   if (!h) return RNNLM_E_INVALID_ARG;

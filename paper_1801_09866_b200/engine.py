@@ -98,6 +98,11 @@ class RNNLM:
                                                _stream(stream)), "rnnlm_log_normalizer")
         return out
 
+    def results_ready(self, stream=None):
+        """`stream` waits for the last query_batch's scores / handles / outcomes
+        (not for its GRU state update)."""
+        check(_lib.load().rnnlm_results_ready(self._h, _stream(stream)), "rnnlm_results_ready")
+
     def reset_session(self, session: int = ALL, stream=None):
         check(_lib.load().rnnlm_reset_session(self._h, session, _stream(stream)), "reset_session")
 

@@ -533,3 +533,29 @@ def test_tf32x3_off_grid_weights_accuracy():
         errs[math] = replay_compare(eng, orc, wl, tol_score=1e-2, tol_state=1e-2)["max_state_err"]
     assert errs[MATH_TF32X3] < 1e-5, errs
     assert errs[MATH_TF32X3] < 0.1 * errs[MATH_TF32], errs
+
+
+def test_results_ready_before_state_update():
+    """rnnlm_results_ready: a second stream that waits only for it and copies
+    the scores / handles out sees the final values (the large model's GRU may
+    still be running), identical to the values after a full synchronize."""
+    d, m = model("large")
+    wl = generate_workload(4, 3, 1024, d.V, seed=9)
+    eng, _ = pair(d, m, wl, KEY_SIGN, math=MATH_BF16)
+    child = np.zeros(wl.n_total, np.uint32)
+    side = torch.cuda.Stream()
+    for t in range(wl.frames):
+        sl = wl.frame_slice(t)
+        par = O.resolve_parents(wl.parent_ref[sl], child)
+        sc = torch.empty(wl.n_per_frame, dtype=torch.float32, device="cuda")
+        ch = torch.empty(wl.n_per_frame, dtype=torch.int32, device="cuda")
+        eng.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]), score=sc, child=ch)
+        eng.results_ready(stream=side)
+        with torch.cuda.stream(side):
+            early_sc = sc.to("cpu", non_blocking=True)
+            early_ch = ch.to("cpu", non_blocking=True)
+        side.synchronize()
+        torch.cuda.synchronize()
+        assert np.array_equal(early_sc.numpy().view(np.uint32), sc.cpu().numpy().view(np.uint32))
+        assert np.array_equal(early_ch.numpy(), ch.cpu().numpy())
+        child[sl] = ch.cpu().numpy().view(np.uint32)
