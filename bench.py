@@ -381,11 +381,16 @@ def run_ours(args):
         peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # FP32 FFMA lanes x 2 flop x clock
         bound, peak_src = "alu", "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz"
     achieved = flops / gru_s / 1e12 if gru_s > 0 else 0.0
+    # the library runs the CTA-pair kernel for the bf16 GRU when H % 256 == 0
+    # (gru_tc_prepare; RNNLM_TC_PAIR=0 selects one CTA per tile)
+    pair = (math == R.MATH_BF16 and args.cell == "gru" and dims.H % 256 == 0
+            and os.environ.get("RNNLM_TC_PAIR", "1") != "0")
+    gru_kernel = "k_gru_tc2" if pair else "k_gru_tc"
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         ent = prof.get(args.workload, {}).get(args.math, {})
-        traffic = ent.get("kernels", {}).get("k_gru_tc", ent.get("gru_dram_bytes_per_step"))
+        traffic = ent.get("kernels", {}).get(gru_kernel, ent.get("gru_dram_bytes_per_step"))
     except Exception:
         pass
     line = {
@@ -400,7 +405,8 @@ def run_ours(args):
                    "l2": "flushed between timed steps (256 MiB write outside the event pair)",
                    "timed_frames": f"value: frames {tA}..{tB - 1}; roofline pass (library kernel events on): frames {tB}..{frames - 1} ({F0} prefill + {args.warmup} warm-up frames untimed)",
                    "parallelism": f"dp{world} (sessions sharded, weights replicated, NCCL all-gather of (score, child))"},
-        "roofline": {"kernel": ("k_gru_tc (fused tcgen05 GRU, both phases)" if math != R.MATH_FP32
+        "roofline": {"kernel": ((f"{gru_kernel} (fused tcgen05 GRU, both phases"
+                                 + (", CTA pair)" if pair else ")")) if math != R.MATH_FP32
                                 else "k_gru1_f32 + k_gru2_f32 (+ gather, FP32 SIMT)"), "bound": bound,
                      "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak if peak else None,

@@ -39,8 +39,8 @@
 // linear-before-reset GRU (one phase, tiles of 64 units x [Wh x | z | r | Uh h]
 // over W3, see mma_loop), CELL 2 = the vanilla RNN (one phase, A1 x [Wh | Uh]);
 // phase-2 / RNN tiles narrow to 128 units when H % 256 != 0 (a.bn2); the CTA
-// pair k_gru_tc2 (cta_group::2, M = 256) is an opt-in experiment
-// (RNNLM_TC_PAIR=1), and RNNLM_TC_DIAG selects the timing diagnostics of
+// pair k_gru_tc2 (cta_group::2, M = 256) runs the bf16 GRU cell when
+// H % 256 == 0 (RNNLM_TC_PAIR=0 selects one CTA per tile), and RNNLM_TC_DIAG selects the timing diagnostics of
 // DESIGN.md section 5.
 #include <cuda.h>
 
@@ -1178,7 +1178,7 @@ struct TcState {
   bool tf32 = false;               // operands fp32 read as TF32 (else bf16)
   void *w1 = nullptr, *w2 = nullptr, *rh = nullptr, *a1 = nullptr;
   uint32_t *done1 = nullptr;
-  int pair = 0;                    // 0: one-CTA kernel; 1: cta_group::2 pair (RNNLM_TC_PAIR)
+  int pair = 0;                    // 0: one-CTA kernel; 1: cta_group::2 pair (bf16 GRU default; RNNLM_TC_PAIR)
   uint32_t diag = 0;               // RNNLM_TC_DIAG: timing diagnostics (see TcArgs::diag)
   unsigned long long *prof = nullptr;
   float *bzr = nullptr, *bh = nullptr;
@@ -1282,7 +1282,12 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int
   t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0; t->x3 = x3 != 0 && t->tf32;
   t->lbr = cell == RNNLM_CELL_GRU_LBR;
   t->rnn = cell == RNNLM_CELL_RNN;
-  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = (t->tf32 || cell) ? 0 : atoi(e);   // pair: bf16 GRU only
+  // the CTA pair (cta_group::2) is the default for the bf16 GRU: ~1.3 % faster kernel
+  // than one CTA per tile at the bench size (198.5 vs 201.1 us, three runs each);
+  // RNNLM_TC_PAIR=0 selects the one-CTA kernel, which runs every other mode
+  t->pair = 1;
+  if (const char *e = getenv("RNNLM_TC_PAIR")) t->pair = atoi(e);
+  if (t->tf32 || cell) t->pair = 0;
   if (const char *e = getenv("RNNLM_TC_DIAG")) t->diag = (uint32_t)atoi(e);
   const size_t K1 = E + H;
   std::vector<float> bzr((size_t)2 * H), bh(H);

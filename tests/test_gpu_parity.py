@@ -268,11 +268,13 @@ def test_moderate_bf16_round_codes(k):
     assert rep["miss"] > 300
 
 
+@pytest.mark.parametrize("pair_kernel", ["1", "0"])
 @pytest.mark.parametrize("shape", ["full", "ragged_multisession"])
-def test_bf16_cta_pair_kernel(shape, monkeypatch):
-    """The CTA-pair variant (cta_group::2, M = 256; RNNLM_TC_PAIR=1) against the
-    oracle: full 256-row pair tiles and a ragged multi-session batch."""
-    monkeypatch.setenv("RNNLM_TC_PAIR", "1")
+def test_bf16_cta_pair_kernel(shape, pair_kernel, monkeypatch):
+    """Both bf16 GRU kernels against the oracle: the CTA pair (cta_group::2,
+    M = 256; the default, RNNLM_TC_PAIR=1) and one CTA per tile
+    (RNNLM_TC_PAIR=0): full 256-row pair tiles and a ragged multi-session batch."""
+    monkeypatch.setenv("RNNLM_TC_PAIR", pair_kernel)
     d, m = model("large")
     if shape == "full":
         wl = generate_workload(1, 2, 2048, d.V, seed=5)
