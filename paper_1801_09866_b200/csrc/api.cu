@@ -275,6 +275,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
     chk(dalloc(h, &P.qowner, S * tcap));
     chk(dalloc(h, &P.htab, S * tcap));
     chk(dalloc(h, &P.howner, S * tcap));
+    chk(dalloc(h, &P.phash, B));
   }
   chk(dalloc(h, &P.ctr, S));
   chk(dalloc(h, &P.sticky, 1));

@@ -37,6 +37,8 @@ __device__ __forceinline__ uint32_t hhome(unsigned long long codehash, uint32_t 
 }
 
 // Full code equality of the states in global rows a and b (never a hash).
+// Loads are issued four 16-byte words at a time before any compare, so a
+// 128-byte sign code costs two dependent round trips instead of eight.
 __device__ bool code_equal(const Params &P, size_t a, size_t b) {
   if (a == b) return true;
   const uint4 *pa, *pb;
@@ -50,19 +52,29 @@ __device__ bool code_equal(const Params &P, size_t a, size_t b) {
     pb = reinterpret_cast<const uint4 *>(P.codes + b * P.cstride);
     n16 = P.cstride / 16;
   }
-  for (uint32_t i = 0; i < n16; ++i) {
-    const uint4 x = pa[i], y = pb[i];
-    if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w) return false;
+  for (uint32_t i = 0; i < n16; i += 4) {
+    uint4 x[4], y[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x[j] = y[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (i + j < n16) { x[j] = pa[i + j]; y[j] = pb[i + j]; }
+    }
+    uint32_t d = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d |= (x[j].x ^ y[j].x) | (x[j].y ^ y[j].y) | (x[j].z ^ y[j].z) | (x[j].w ^ y[j].w);
+    if (d) return false;
   }
   return true;
 }
 
-// Hidden-cache key match: same word and equal code of the reference state.
+// Hidden-cache key match: same word and equal code of the reference state
+// (an entry whose reference IS the probing row matches without reading it).
 __device__ __forceinline__ bool hkey_match(const Params &P, unsigned long long tag, uint32_t s,
                                            uint32_t w, uint32_t ps, unsigned long long hh) {
   if ((uint32_t)tag != w) return false;
-  const size_t base = (size_t)s * P.cap;
   const uint32_t ref = (uint32_t)(tag >> 32);
+  if (ref == ps) return true;
+  const size_t base = (size_t)s * P.cap;
   if (P.codehash[base + ref] != hh) return false;
   return code_equal(P, base + ref, base + ps);
 }
@@ -75,42 +87,55 @@ __device__ __forceinline__ bool hkey_match(const Params &P, unsigned long long t
 constexpr unsigned long long NEW_BIT = 1ull << 31;
 
 // ---- (a2) LM-query cache: probe + claim ---------------------------------------
+// The loads of the session counters, the parent's record, the first probe and
+// the parent's code hash are issued before the validation that decides whether
+// they are needed (indices clamped in bounds), so the chain is inputs ->
+// {counters, record, probe} -> {code hash, CAS}.  The parent's state slot and
+// code hash are handed to k_hcache (pslot, phash).
 __global__ void k_qcache(Params P, CallArgs A, uint32_t ntiles) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < ntiles) P.tile_status[q] = 0ull;
   if (q == 0) { *P.tile_ticket = 0u; P.counts[3] = 0u; }
   if (q >= A.n) return;
-  P.claimed[q] = 0;
   const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
+  const uint32_t sprev = q > 0 ? A.session[q - 1] : 0u;
+  const uint32_t sc = s < P.S ? s : 0u, pc = p < P.cap ? p : 0u;
+  const size_t cb = (size_t)sc * P.cap;
+  const uint32_t poisoned = P.ctr[sc].poisoned, nh = P.ctr[sc].next_handle;
+  const uint32_t ps = P.rec[cb + pc].slot;
+  const unsigned long long key = ((unsigned long long)p << 32) | w, nkey = key | NEW_BIT;
+  const size_t base = (size_t)sc * (P.qmask + 1);
+  uint32_t idx = (uint32_t)(mix64(key) & P.qmask);
+  unsigned long long t = P.cache ? vload64(&P.qtab[base + idx].tag) : 0ull;
+  P.claimed[q] = 0;
   int err = 0;
   if (s >= P.S) err = RNNLM_E_INVALID_ARG;
-  else if (q > 0 && A.session[q - 1] > s) err = RNNLM_E_INVALID_ARG;
+  else if (q > 0 && sprev > s) err = RNNLM_E_INVALID_ARG;
   else if (w >= P.V) err = RNNLM_E_VOCAB;
-  else if (P.ctr[s].poisoned) err = RNNLM_E_CAPACITY;
-  else if (p >= P.ctr[s].next_handle) err = RNNLM_E_HISTORY;
-  if (q > 0 && A.session[q - 1] > s) P.counts[2] = A.epoch;   // batch not sorted by session
+  else if (poisoned) err = RNNLM_E_CAPACITY;
+  else if (p >= nh) err = RNNLM_E_HISTORY;
+  if (q > 0 && sprev > s) P.counts[2] = A.epoch;       // batch not sorted by session
   if (err) {
     P.st[q] = ST_INVALID;
     latch(P.sticky, err);
     return;
   }
+  P.pslot[q] = ps;
   if (!P.cache) {
     P.st[q] = ST_MISS_NC;
-    P.pslot[q] = P.rec[(size_t)s * P.cap + p].slot;
     return;
   }
-  const unsigned long long key = ((unsigned long long)p << 32) | w, nkey = key | NEW_BIT;
-  const size_t base = (size_t)s * (P.qmask + 1);
-  uint32_t idx = (uint32_t)(mix64(key) & P.qmask);
+  const unsigned long long hh = P.codehash[cb + (ps < P.cap ? ps : 0u)];
   for (uint32_t probes = 0; probes <= P.qmask; ++probes) {
-    unsigned long long t = vload64(&P.qtab[base + idx].tag);
+    if (probes) t = vload64(&P.qtab[base + idx].tag);
     if (t == key) { P.st[q] = ST_QHIT_OLD; P.qent[q] = idx; return; }
     if (t == TAG_EMPTY) t = atomicCAS(&P.qtab[base + idx].tag, TAG_EMPTY, nkey);
     if (t == TAG_EMPTY || t == nkey) {                  // claimed (or joined) in this call
       atomicMin(&P.qowner[base + idx], q);
       P.st[q] = ST_QNEED;
       P.qent[q] = idx;
+      P.phash[q] = hh;
       P.claimed[q] = 1;
       return;
     }
@@ -122,22 +147,24 @@ __global__ void k_qcache(Params P, CallArgs A, uint32_t ntiles) {
 }
 
 // ---- (a3) hidden-state cache: owner resolution + probe + claim -----------------
+// Chain: per-query scratch -> {query-cache owner, first probe} -> CAS.
 __global__ void k_hcache(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= A.n || P.st[q] != ST_QNEED || P.counts[2] == A.epoch) return;
-  const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
-  const uint32_t o = P.qowner[(size_t)s * (P.qmask + 1) + P.qent[q]];
-  if (o != q) { P.st[q] = ST_QHIT_NEW; P.aux[q] = o; return; }
-  const size_t cb = (size_t)s * P.cap;
-  const uint32_t ps = P.rec[cb + p].slot;
-  P.pslot[q] = ps;
-  const unsigned long long hh = P.codehash[cb + ps];
-  const unsigned long long mine = (((unsigned long long)ps << 32) | w) | NEW_BIT;
+  if (q >= A.n) return;
+  const uint32_t st = P.st[q];
+  const bool bad = P.counts[2] == A.epoch;
+  const uint32_t s = A.session[q], w = A.word[q], qe = P.qent[q], ps = P.pslot[q];
+  const unsigned long long hh = P.phash[q];
+  if (st != ST_QNEED || bad) return;
+  const uint32_t o = P.qowner[(size_t)s * (P.qmask + 1) + qe];
   const size_t base = (size_t)s * (P.hmask + 1);
   uint32_t idx = hhome(hh, w, P.hmask);
+  unsigned long long t = vload64(&P.htab[base + idx].tag);
+  if (o != q) { P.st[q] = ST_QHIT_NEW; P.aux[q] = o; return; }
+  const unsigned long long mine = (((unsigned long long)ps << 32) | w) | NEW_BIT;
   for (uint32_t probes = 0; probes <= P.hmask; ++probes) {
-    unsigned long long t = vload64(&P.htab[base + idx].tag);
+    if (probes) t = vload64(&P.htab[base + idx].tag);
     if (t == TAG_EMPTY) {
       t = atomicCAS(&P.htab[base + idx].tag, TAG_EMPTY, mine);
       if (t == TAG_EMPTY) t = mine;                     // inserted: falls into the claim below
@@ -192,11 +219,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
     uint32_t nonq = 0, miss = 0;
     if (q < A.n) {
       uint32_t st = P.st[q];
+      const uint32_t sq = A.session[q], he = P.hent[q];
       if (bad) {
         if (st != ST_INVALID) latch(P.sticky, RNNLM_E_INVALID_ARG);
         st = ST_INVALID;
       } else if (st == ST_HNEED) {
-        const uint32_t o = P.howner[(size_t)A.session[q] * (P.hmask + 1) + P.hent[q]];
+        const uint32_t o = P.howner[(size_t)sq * (P.hmask + 1) + he];
         st = (o == q) ? ST_MISS : ST_SHIT_NEW;
         P.aux[q] = o;
       }
@@ -281,71 +309,79 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
 }
 
 // ---- (a4) commit: handles, slots, records, cache values, work lists -------
+// Every load is issued before the first store (the compiler cannot move a load
+// above a store it cannot prove disjoint), so the chain is per-query scratch ->
+// {session segments and cursors, owners, parent record, owner's miss index}.
 __global__ void k_commit(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= A.n) return;
   const uint32_t st = P.st[q];
   const uint32_t s = A.session[q];
+  const uint32_t snext = q + 1 < A.n ? A.session[q + 1] : NONE;
+  const uint32_t w = A.word[q], p = A.parent[q];
+  const uint32_t en = P.excl_nonq[q], r = P.excl_miss[q];
+  const uint32_t qe = P.qent[q], he = P.hent[q], cs = P.cslot[q], ax = P.aux[q], ps = P.pslot[q];
+  const uint8_t cl = P.claimed[q];
   const bool bad = P.counts[2] == A.epoch;
   const bool nonq = (st == ST_SHIT_OLD || st == ST_SHIT_NEW || st == ST_MISS || st == ST_MISS_NC);
   const bool miss = (st == ST_MISS || st == ST_MISS_NC);
-  if (!bad && s < P.S && (q == A.n - 1 || A.session[q + 1] != s)) {   // last of the session
-    P.seg_cnt_nonq[s] = P.excl_nonq[q] + (nonq ? 1u : 0u) - P.seg_excl_nonq[s];
-    P.seg_cnt_miss[s] = P.excl_miss[q] + (miss ? 1u : 0u) - P.seg_excl_miss[s];
+  // second round trip (indices clamped in bounds; unused values are discarded)
+  const uint32_t sc = s < P.S ? s : 0u;
+  const size_t cb = (size_t)sc * P.cap;
+  const size_t qb0 = (size_t)sc * (P.qmask + 1), hb0 = (size_t)sc * (P.hmask + 1);
+  const uint32_t sen = P.seg_excl_nonq[sc], sem = P.seg_excl_miss[sc];
+  const uint32_t nh0 = P.ctr[sc].next_handle, ns0 = P.ctr[sc].next_slot;
+  const uint32_t qo = (cl & 1) ? P.qowner[qb0 + qe] : NONE;
+  const uint32_t ho = (cl & 2) ? P.howner[hb0 + he] : NONE;
+  const Rec pr = nonq ? P.rec[cb + (p < P.cap ? p : 0u)] : Rec{};
+  const uint32_t eo = (nonq && st == ST_SHIT_NEW) ? P.excl_miss[ax] : 0u;
+  if (!bad && s < P.S && snext != s) {                 // last of the session
+    P.seg_cnt_nonq[s] = en + (nonq ? 1u : 0u) - sen;
+    P.seg_cnt_miss[s] = r + (miss ? 1u : 0u) - sem;
   }
   // entries this query claimed AND owns: clear NEW_BIT (good batch) or remove
   // them again (rejected batch: every entry of this call goes, chains return
   // to their state before the call)
-  const uint8_t cl = P.claimed[q];
-  if (cl) {
-    const size_t qb0 = (size_t)s * (P.qmask + 1), hb0 = (size_t)s * (P.hmask + 1);
-    if ((cl & 1) && P.qowner[qb0 + P.qent[q]] == q) {
-      QEntry *e = &P.qtab[qb0 + P.qent[q]];
-      if (bad) { e->tag = TAG_EMPTY; P.qowner[qb0 + P.qent[q]] = NONE; }
-      else e->tag &= ~NEW_BIT;
-    }
-    if ((cl & 2) && P.howner[hb0 + P.hent[q]] == q) {
-      HEntry *e = &P.htab[hb0 + P.hent[q]];
-      if (bad) { e->tag = TAG_EMPTY; P.howner[hb0 + P.hent[q]] = NONE; }
-      else e->tag &= ~NEW_BIT;
-    }
+  if (qo == q) {
+    QEntry *e = &P.qtab[qb0 + qe];
+    if (bad) { e->tag = TAG_EMPTY; P.qowner[qb0 + qe] = NONE; }
+    else e->tag &= ~NEW_BIT;
+  }
+  if (ho == q) {
+    HEntry *e = &P.htab[hb0 + he];
+    if (bad) { e->tag = TAG_EMPTY; P.howner[hb0 + he] = NONE; }
+    else e->tag &= ~NEW_BIT;
   }
   if (!nonq) return;
-  const uint32_t w = A.word[q], p = A.parent[q];
-  const size_t cb = (size_t)s * P.cap;
-  const uint32_t h = P.ctr[s].next_handle + (P.excl_nonq[q] - P.seg_excl_nonq[s]);
-  const size_t qb = (size_t)s * (P.qmask + 1);
-  const uint32_t r = P.excl_miss[q];
-  P.nonq_list[P.excl_nonq[q]] = q;
+  const uint32_t h = nh0 + (en - sen);
+  P.nonq_list[en] = q;
   if (h >= P.cap) {                                    // out of history handles
     P.st[q] = ST_INVALID;
     latch(P.sticky, RNNLM_E_CAPACITY);
     P.ctr[s].poisoned = 1u;                            // read from the next call on
     A.score[q] = __int_as_float(0x7fc00000);
     A.child[q] = NONE;
-    if (P.cache) { P.qtab[qb + P.qent[q]].child = NONE; P.qtab[qb + P.qent[q]].score = __int_as_float(0x7fc00000); }
+    if (P.cache) { P.qtab[qb0 + qe].child = NONE; P.qtab[qb0 + qe].score = __int_as_float(0x7fc00000); }
     if (miss) P.row_dst[r] = NONE;
     return;
   }
   uint32_t sl;
   if (miss) {
-    sl = P.ctr[s].next_slot + (r - P.seg_excl_miss[s]);
-    P.row_src[r] = (uint32_t)(cb + P.pslot[q]);
+    sl = ns0 + (r - sem);
+    P.row_src[r] = (uint32_t)(cb + ps);
     P.row_dst[r] = (uint32_t)(cb + sl);
     P.row_word[r] = w;
     if (P.cache) {
-      P.htab[(size_t)s * (P.hmask + 1) + P.hent[q]].slot = sl;
+      P.htab[hb0 + he].slot = sl;
       P.codehash[cb + sl] = 0ull;                      // accumulated by the GRU epilogue
     }
   } else if (st == ST_SHIT_OLD) {
-    sl = P.cslot[q];
+    sl = cs;
   } else {                                             // SHIT_NEW: the owner's new slot
-    const uint32_t o = P.aux[q];
-    sl = P.ctr[s].next_slot + (P.excl_miss[o] - P.seg_excl_miss[s]);
+    sl = ns0 + (eo - sem);
   }
   P.cslot[q] = sl;
-  const Rec pr = P.rec[cb + p];
   Rec nr;
   nr.slot = sl;
   for (int j = 0; j < MAX_CTX; ++j) nr.ctx[j] = NONE;
@@ -355,7 +391,7 @@ __global__ void k_commit(Params P, CallArgs A) {
   }
   P.rec[cb + h] = nr;
   A.child[q] = h;
-  if (P.cache) P.qtab[qb + P.qent[q]].child = h;
+  if (P.cache) P.qtab[qb0 + qe].child = h;
 }
 
 // ---- (a7) final: QHIT results, outcomes, counters, cursors -----------------
