@@ -161,21 +161,46 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (Q + BM - 1) / BM; i += gridDim.x * blockDim.x)
     a.done1[i] = 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.tile_ctr = 0u;
-  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Q; r += nw) {
-    if constexpr (sizeof(T) == 2) {
-      const uint4 *x = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)a.row_word[r] * a.E);
-      const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
+  if constexpr (sizeof(T) == 2) {
+    // bf16: every load of a row chunk (4 x 16 B of x, 8 x 16 B of h per lane)
+    // is issued before its stores, and the next row's indices are fetched
+    // while the current row is copied, so a warp keeps ~12 loads in flight
+    const uint32_t nx = a.E / 8, nh = a.H / 8, nmax = nx > nh ? nx : nh;
+    uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t wd = r < Q ? a.row_word[r] : 0u, src = r < Q ? a.row_src[r] : 0u;
+    for (; r < Q; r += nw) {
+      const uint4 *x = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)wd * a.E);
+      const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)src * a.H);
       uint4 *dst = reinterpret_cast<uint4 *>(a.a1 + (size_t)r * K1);
-      const uint32_t nx = a.E / 8, nh = a.H / 8;
-      for (uint32_t i = lane; i < nx; i += 32) dst[i] = __ldg(x + i);
-      for (uint32_t i = lane; i < nh; i += 32) {
-        const float4 u = h[2 * i], v = h[2 * i + 1];
-        __nv_bfloat162 b0 = __floats2bfloat162_rn(u.x, u.y), b1 = __floats2bfloat162_rn(u.z, u.w);
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(v.x, v.y), b3 = __floats2bfloat162_rn(v.z, v.w);
-        dst[nx + i] = make_uint4(*reinterpret_cast<uint32_t *>(&b0), *reinterpret_cast<uint32_t *>(&b1),
-                                 *reinterpret_cast<uint32_t *>(&b2), *reinterpret_cast<uint32_t *>(&b3));
+      const uint32_t rn = r + nw;
+      if (rn < Q) { wd = a.row_word[rn]; src = a.row_src[rn]; }
+      for (uint32_t i0 = lane; i0 < nmax; i0 += 128) {
+        uint4 xv[4];
+        float4 hu[4], hv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t i = i0 + 32 * j;
+          if (i < nx) xv[j] = __ldg(x + i);
+          if (i < nh) { hu[j] = __ldg(h + 2 * i); hv[j] = __ldg(h + 2 * i + 1); }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t i = i0 + 32 * j;
+          if (i < nx) dst[i] = xv[j];
+          if (i < nh) {
+            const float4 u = hu[j], v = hv[j];
+            __nv_bfloat162 b0 = __floats2bfloat162_rn(u.x, u.y), b1 = __floats2bfloat162_rn(u.z, u.w);
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v.x, v.y), b3 = __floats2bfloat162_rn(v.z, v.w);
+            dst[nx + i] = make_uint4(*reinterpret_cast<uint32_t *>(&b0), *reinterpret_cast<uint32_t *>(&b1),
+                                     *reinterpret_cast<uint32_t *>(&b2), *reinterpret_cast<uint32_t *>(&b3));
+          }
+        }
       }
-    } else {
+    }
+    return;
+  }
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Q; r += nw) {
+    {
       // TF32 operands are the fp32 values themselves (the MMA reads their TF32 part)
       const float4 *x = reinterpret_cast<const float4 *>(a.emb + (size_t)a.row_word[r] * a.E);
       const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
@@ -1398,7 +1423,11 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   uint32_t g1 = t->lbr ? mt * (P.H / 64) : (t->rnn ? mt * (P.H / a.bn2) : mt * (t->nub + P.H / a.bn2));
   if (g1 > (uint32_t)num_sms) g1 = num_sms;
   uint32_t gg = (max_rows + 7) / 8;
-  if (gg > (uint32_t)num_sms * 4) gg = num_sms * 4;
+  // resident blocks per SM: 4 for the fp32-operand gather (40 registers), 3 for
+  // the bf16 gather (70 registers: a row chunk's 12 loads are held at once)
+  uint32_t bps = t->tf32 ? 4u : 3u;
+  if (const char *e = getenv("RNNLM_TC_GATHER_BPS")) bps = (uint32_t)atoi(e);
+  if (gg > (uint32_t)num_sms * bps) gg = num_sms * bps;
   if (t->tf32) launch_pdl(k_gather_a1<float>, gg, 256, 0, s, a);
   else launch_pdl(k_gather_a1<__nv_bfloat16>, gg, 256, 0, s, a);
   if (ev_gathered) cudaEventRecord(ev_gathered, s);
