@@ -500,6 +500,24 @@ def test_fig4_hidden_sizes_tensor_core(H, cell, math):
     assert rep["miss"] > 100
 
 
+@pytest.mark.parametrize("pair_kernel", ["1", "0"])
+@pytest.mark.parametrize("E", [64, 192, 448])
+@pytest.mark.parametrize("math", [MATH_BF16, MATH_TF32])
+def test_tensor_core_embed_neq_hidden(E, math, pair_kernel, monkeypatch):
+    """E != H on the tensor-core paths (H = 256): the A1 gather's x and h row
+    chunks of different lengths (E/8 vs H/8 16-byte words), K = E + H not a
+    multiple of 256, both bf16 kernels."""
+    if math == MATH_TF32 and pair_kernel == "1":
+        pytest.skip("TF32 runs the one-CTA kernel only")
+    monkeypatch.setenv("RNNLM_TC_PAIR", pair_kernel)
+    d = ModelDims(V=3000, E=E, H=256, maxent_log2=16, N=3)
+    m = generate_model(d, seed=41)
+    wl = generate_workload(2, 8, 300, d.V, seed=19)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=math)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
+    assert rep["miss"] > 100
+
+
 # ---------------------------------------------------------------- 3xTF32: fp32-accurate tensor-core GRU
 def test_tf32x3_moderate_fp32_tolerance():
     """RNNLM_MATH_TF32X3 holds the FP32 path's 1e-5 bar on scores and states
