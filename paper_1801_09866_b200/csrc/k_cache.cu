@@ -254,23 +254,33 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
       if (lane == 0) atomicExch(&P.tile_status[0], to_status(agg, ST_INC));
     } else {
       if (lane == 0) atomicExch(&P.tile_status[tile], to_status(agg, ST_AGG));
-      // warp-parallel look-back over 32 predecessors at a time: lane l reads
-      // tile (j - l); the nearest inclusive prefix ends the walk
+      // warp-parallel look-back over 64 predecessors at a time: lane l reads
+      // tiles (j - l) and (j - 32 - l); the nearest inclusive prefix ends the
+      // walk (inclusive prefixes then travel 64 tiles per round trip)
       int j = (int)tile - 1;
       for (;;) {
-        const int idx = j - lane;
-        unsigned long long x = idx >= 0 ? vload64(&P.tile_status[idx]) : to_status(0ull, ST_INC);
-        while (__any_sync(0xffffffffu, (x >> 62) == 0)) {
-          if ((x >> 62) == 0) x = vload64(&P.tile_status[idx]);
+        const int i0 = j - lane, i1 = j - 32 - lane;
+        unsigned long long x0 = i0 >= 0 ? vload64(&P.tile_status[i0]) : to_status(0ull, ST_INC);
+        unsigned long long x1 = i1 >= 0 ? vload64(&P.tile_status[i1]) : to_status(0ull, ST_INC);
+        while (__any_sync(0xffffffffu, (x0 >> 62) == 0 || (x1 >> 62) == 0)) {
+          if ((x0 >> 62) == 0) x0 = vload64(&P.tile_status[i0]);
+          if ((x1 >> 62) == 0) x1 = vload64(&P.tile_status[i1]);
         }
-        const uint32_t incm = __ballot_sync(0xffffffffu, (x >> 62) == 2);
-        const int stop = incm ? __ffs(incm) - 1 : 31;
-        unsigned long long part = lane <= stop ? from_status(x) : 0ull;
+        const uint32_t inc0 = __ballot_sync(0xffffffffu, (x0 >> 62) == 2);
+        const uint32_t inc1 = __ballot_sync(0xffffffffu, (x1 >> 62) == 2);
+        unsigned long long part;
+        if (inc0) {
+          const int stop = __ffs(inc0) - 1;
+          part = lane <= stop ? from_status(x0) : 0ull;
+        } else {
+          const int stop = inc1 ? __ffs(inc1) - 1 : 31;
+          part = from_status(x0) + (lane <= stop ? from_status(x1) : 0ull);
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
         excl += part;
-        if (incm) break;
-        j -= 32;
+        if (inc0 | inc1) break;
+        j -= 64;
       }
       if (lane == 0) atomicExch(&P.tile_status[tile], to_status(excl + agg, ST_INC));
     }
