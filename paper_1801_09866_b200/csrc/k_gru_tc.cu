@@ -901,7 +901,12 @@ __global__ void __maxnreg__(GRU_MAXREG)
 // 32 KB per K-chunk from L2 instead of 48 KB (the one-CTA kernel is
 // L2->SM-bandwidth bound).  The leader CTA claims tiles, issues the MMAs and
 // owns the pipeline barriers that both CTAs' TMA and epilogues signal.
-constexpr int STP = 6;                         // pair-kernel smem stages
+#ifndef RNNLM_TC_STP
+#define RNNLM_TC_STP 5
+#endif
+// pair-kernel smem stages (32 KB each): 5 measured faster than 6 on the bench
+// workload (547-549 vs 537-540 M q/s, kernel 194.8 vs 197.6 us, same box)
+constexpr int STP = RNNLM_TC_STP;
 constexpr int BP_BYTES = (BN / 2) * BK * 2;    // 16 KB: this CTA's half of a B chunk
 
 __device__ __forceinline__ uint32_t cluster_rank() {
