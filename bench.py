@@ -389,7 +389,8 @@ def run_ours(args):
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        ent = prof.get(args.workload, {}).get(args.math, {})
+        # captured for the paper's cell only; other cells report no traffic figure
+        ent = prof.get(args.workload, {}).get(args.math, {}) if args.cell == "gru" else {}
         traffic = ent.get("kernels", {}).get(gru_kernel, ent.get("gru_dram_bytes_per_step"))
     except Exception:
         pass

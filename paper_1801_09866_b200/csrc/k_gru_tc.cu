@@ -62,7 +62,15 @@ constexpr int BN = 256;          // UMMA N of both phases (phase 1: z|r of 128 u
 #ifndef RNNLM_TC_ST
 #define RNNLM_TC_ST 4
 #endif
-constexpr int ST = RNNLM_TC_ST;  // smem pipeline stages
+constexpr int ST = RNNLM_TC_ST;  // smem pipeline stages (one-CTA kernel; GRU, LBR cells)
+#ifndef RNNLM_TC_ST_RNN
+#define RNNLM_TC_ST_RNN 3
+#endif
+// the RNN cell's kernel is short and its step is bound by the side-stream
+// scoring that shares its SMs: 3 stages leave that scoring 48 KB more L1
+// (1,274-1,326 vs 1,068-1,071 M q/s, profiles/ab_st1_r1.txt)
+template <int CELL>
+__host__ __device__ constexpr int st_of() { return CELL == RNNLM_CELL_RNN ? RNNLM_TC_ST_RNN : ST; }
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES = BN * BK * 2;          // 32 KB
 constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 columns
@@ -240,15 +248,15 @@ struct Smem {
   uint32_t *tile_q;
 };
 
-__device__ __forceinline__ Smem carve(uint8_t *raw) {
+__device__ __forceinline__ Smem carve(uint8_t *raw, int nst) {
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   Smem m;
   m.sA = smem;
-  m.sB = smem + ST * A_BYTES;
-  m.stg = m.sB + ST * B_BYTES;
+  m.sB = smem + nst * A_BYTES;
+  m.stg = m.sB + nst * B_BYTES;
   m.full = reinterpret_cast<uint64_t *>(m.stg + EPI_WARPS * STG_BYTES);
-  m.empty = m.full + ST;
-  m.tfull = m.empty + ST;
+  m.empty = m.full + nst;
+  m.tfull = m.empty + nst;
   m.tempty = m.tfull + 2;
   m.qfull = m.tempty + 2;
   m.qempty = m.qfull + TQ;
@@ -257,9 +265,9 @@ __device__ __forceinline__ Smem carve(uint8_t *raw) {
   return m;
 }
 
-__device__ __forceinline__ void setup(const Smem &m, int warp) {
+__device__ __forceinline__ void setup(const Smem &m, int warp, int nst) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) { mbar_init(&m.full[s], 1); mbar_init(&m.empty[s], 1); }
+    for (int s = 0; s < nst; ++s) { mbar_init(&m.full[s], 1); mbar_init(&m.empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&m.tfull[s], 1); mbar_init(&m.tempty[s], EPI_WARPS * 32); }
     // tile ids: the producer publishes, the MMA lane and one lane per epilogue warp release
     for (int s = 0; s < TQ; ++s) { mbar_init(&m.qfull[s], 1); mbar_init(&m.qempty[s], 1 + EPI_WARPS); }
@@ -339,7 +347,7 @@ __device__ __forceinline__ uint32_t next_tile(const Smem &m, uint32_t it, bool r
 template <typename T, bool LBR>
 __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint32_t KC, uint32_t kx, int lane,
                                          uint32_t diag, unsigned long long *prof, bool narrow, bool rnn,
-                                         uint32_t mt, uint32_t n1, uint32_t n2, uint32_t L) {
+                                         uint32_t mt, uint32_t n1, uint32_t n2, uint32_t L, int nst) {
   uint32_t stage = 0, phase = 0;
   const uint32_t id256 = idesc_of(Op<T>::FMT, BM, BN);
   const uint32_t id192 = idesc_of(Op<T>::FMT, BM, 192), id128 = idesc_of(Op<T>::FMT, BM, 128),
@@ -387,7 +395,7 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
         if (kc == KC - 1) umma_commit(&m.tfull[acc]);
       }
       __syncwarp();
-      if (++stage == ST) { stage = 0; phase ^= 1; }
+      if (++stage == nst) { stage = 0; phase ^= 1; }
     }
   }
   if (prof && lane == 0) { prof[2] = w_full; prof[3] = w_tempty; }
@@ -747,7 +755,8 @@ __global__ void __maxnreg__(GRU_MAXREG)
              const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2,
              TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const Smem m = carve(smem_raw);
+  constexpr int NST = st_of<CELL>();
+  const Smem m = carve(smem_raw, NST);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // GRU: per M-tile nub phase-1 + H/256 phase-2 tiles; LBR: H/64 one-phase
   // tiles over W3; RNN: H/256 one-phase tiles of A1 x W2 = [Wh | Uh]
@@ -759,7 +768,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   if (threadIdx.x == 0) {
     prefetch_map(&map_a1); prefetch_map(&map_w1); prefetch_map(&map_rh); prefetch_map(&map_w2);
   }
-  setup(m, warp);
+  setup(m, warp, NST);
   pdl_entry();
   const uint32_t Q = a.counts[1];
   const uint32_t mt = (Q + BM - 1) / BM;
@@ -800,7 +809,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
           w_empty += clock64() - t0;
           if (a.diag == 2 || a.diag == 6) {
             mbar_arrive(&m.full[stage]);
-            if (++stage == ST) { stage = 0; phase ^= 1; }
+            if (++stage == NST) { stage = 0; phase ^= 1; }
             continue;
           }
           // B rows this tile loads: 192 (LBR), bn2 (phase 2, RNN), 256 (phase 1)
@@ -815,13 +824,13 @@ __global__ void __maxnreg__(GRU_MAXREG)
             else tma_load_2d(dA, &map_rh, &m.full[stage], rh_off + (int)((kc - kx) * BKE), (int)m0);
             tma_load_2d(dB, &map_w2, &m.full[stage], b_off + (int)(kc * BKE), (int)(x.j * b_rows));
           }
-          if (++stage == ST) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
       if (prof) { prof[0] = w_empty; prof[1] = w_dep; }
     }
   } else if (warp == 1) {
-    mma_loop<T, LBR>(m, tmem_base, KCt, kx, lane, a.diag, prof, a.bn2 != BN, RNN, mt, n1, n2, L);
+    mma_loop<T, LBR>(m, tmem_base, KCt, kx, lane, a.diag, prof, a.bn2 != BN, RNN, mt, n1, n2, L, NST);
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -1200,7 +1209,8 @@ __global__ void __maxnreg__(GRU_MAXREG)
 }
 constexpr size_t SMEM_PAIR = 1024 + STP * (A_BYTES + BP_BYTES) + EPI_WARPS * STG_BYTES + 256;
 
-constexpr size_t SMEM = 1024 + ST * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 256;
+constexpr size_t smem_of(int nst) { return 1024 + nst * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 256; }
+constexpr size_t SMEM = smem_of(ST), SMEM_RNN = smem_of(st_of<RNNLM_CELL_RNN>());
 
 // ---------------------------------------------------------------- host side
 struct TcState {
@@ -1351,8 +1361,8 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RNN) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RNN) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PAIR) == cudaSuccess;
   *state_out = t;
   if (!ok) {
@@ -1448,8 +1458,8 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
       if (t->tf32) launch_pdl(k_gru_tc<float, 1>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
       else launch_pdl(k_gru_tc<__nv_bfloat16, 1>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
     } else if (t->rnn) {
-      if (t->tf32) launch_pdl(k_gru_tc<float, 2>, g1, THREADS, SMEM, s, t->map_a1, t->map_w2, t->map_rh, t->map_w2, a);
-      else launch_pdl(k_gru_tc<__nv_bfloat16, 2>, g1, THREADS, SMEM, s, t->map_a1, t->map_w2, t->map_rh, t->map_w2, a);
+      if (t->tf32) launch_pdl(k_gru_tc<float, 2>, g1, THREADS, SMEM_RNN, s, t->map_a1, t->map_w2, t->map_rh, t->map_w2, a);
+      else launch_pdl(k_gru_tc<__nv_bfloat16, 2>, g1, THREADS, SMEM_RNN, s, t->map_a1, t->map_w2, t->map_rh, t->map_w2, a);
     } else {
       if (t->tf32) launch_pdl(k_gru_tc<float, 0>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
       else launch_pdl(k_gru_tc<__nv_bfloat16, 0>, g1, THREADS, SMEM, s, t->map_a1, t->map_w1, t->map_rh, t->map_w2, a);
