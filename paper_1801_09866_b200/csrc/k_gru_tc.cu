@@ -1420,10 +1420,13 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.cstride = P.cstride; a.round_scale = P.round_scale; a.codes = P.codes; a.codehash = P.codehash;
   a.done1 = t->done1;
   a.tile_ctr = t->done1 + (t->bmax / BM + 2);
-  // phase-2 tiles trail their phase-1 tiles by this many M-tiles (RNNLM_TC_LAG); measured:
-  // 24: 504, 48: 521, 96-1000: 530-535 M q/s on the bench workload -- keeping the two
+  // phase-2 tiles trail their phase-1 tiles by this many 128-row M-tiles (RNNLM_TC_LAG);
+  // one CTA per tile, measured: 24: 504, 48: 521, 96-1000: 530-535 M q/s on the bench
+  // workload -- keeping the two
   // phases apart (each phase's weights hot in L2) beats interleaving them tightly
-  a.lag = getenv("RNNLM_TC_LAG") ? (uint32_t)atoi(getenv("RNNLM_TC_LAG")) : 128u;
+  // CTA pair (5-stage ring): lag 32: 537-540, 48: 543-545, 64: 548-551, 96: 543-553,
+  // 128: 546-549 M q/s, kernel 199.5 / 196.5 / 193.3 / 193.7 / 195.4 us (profiles/ab_lag_r1.txt)
+  a.lag = getenv("RNNLM_TC_LAG") ? (uint32_t)atoi(getenv("RNNLM_TC_LAG")) : (t->pair ? 64u : 128u);
   a.diag = t->diag;
   a.bz = t->bz; a.br = t->br;
   a.bn2 = P.H % BN ? UB : BN;

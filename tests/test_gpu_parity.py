@@ -268,6 +268,22 @@ def test_moderate_bf16_round_codes(k):
     assert rep["miss"] > 300
 
 
+@pytest.mark.parametrize("lag", ["2", "6"])
+def test_bf16_interleaved_phase_schedule(lag, monkeypatch):
+    """Phase-2 tiles interleaved with the phase-1 tiles of later M-tiles (the
+    middle section of the tile order, RNNLM_TC_LAG smaller than the number of
+    M-tiles): both bf16 kernels, 4,000 rows = 16 pair / 32 single M-tiles."""
+    if lag:
+        monkeypatch.setenv("RNNLM_TC_LAG", lag)
+    d, m = model("large")
+    wl = generate_workload(2, 2, 2000, d.V, seed=23)
+    for pk in ("1", "0"):
+        monkeypatch.setenv("RNNLM_TC_PAIR", pk)
+        eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16, cache=False)
+        rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_BF16], tol_state=TOL[MATH_BF16])
+        assert rep["miss"] == wl.n_total
+
+
 @pytest.mark.parametrize("pair_kernel", ["1", "0"])
 @pytest.mark.parametrize("shape", ["full", "ragged_multisession"])
 def test_bf16_cta_pair_kernel(shape, pair_kernel, monkeypatch):
