@@ -189,7 +189,7 @@ __global__ void k_hcache(Params P, CallArgs A) {
 }
 
 // ---- (a4) decoupled look-back scan over (non-QHIT, MISS) ------------------
-constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 2;
+constexpr int SCAN_THREADS = 256, SCAN_ITEMS = RNNLM_SCAN_ITEMS;
 static_assert(SCAN_THREADS * SCAN_ITEMS == rnnlm_host::SCAN_TILE, "tile");
 constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62;
 

@@ -175,7 +175,10 @@ inline cudaError_t launch_pdl_cluster(void (*k)(KArgs...), dim3 grid, dim3 block
 }
 using rnnlm_dev::CallArgs;
 using rnnlm_dev::Params;
-constexpr int SCAN_TILE = 512;    // queries per look-back tile
+#ifndef RNNLM_SCAN_ITEMS
+#define RNNLM_SCAN_ITEMS 2
+#endif
+constexpr int SCAN_TILE = 256 * RNNLM_SCAN_ITEMS;    // queries per look-back tile (256 threads)
 int launch_cache_front(const Params &P, const CallArgs &A, cudaStream_t s);   // returns #launches
 int launch_commit(const Params &P, const CallArgs &A, cudaStream_t s);
 int launch_score(const Params &P, const CallArgs &A, int num_sms, cudaStream_t s);
