@@ -236,7 +236,9 @@ constexpr int THREADS = (2 + EPI_WARPS) * 32;
 // Register cap of the fused kernels: three of its warps share an SM sub-partition,
 // and 3 x 152 x 32 registers leave room for one warp of k_score (48 registers)
 // per sub-partition, so the side-stream scoring runs beside the GRU.
+#ifndef GRU_MAXREG
 #define GRU_MAXREG 152
+#endif
 
 constexpr int TQ = 4;            // depth of the tile-id ring (producer -> MMA / epilogue)
 constexpr uint32_t NO_TILE = 0xFFFFFFFFu;
