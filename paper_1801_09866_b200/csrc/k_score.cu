@@ -60,6 +60,12 @@ __global__ void __launch_bounds__(128) k_score(Params P, CallArgs A) {
       pr = P.rec[(size_t)s * P.cap + A.parent[q]];
     }
     const float *h = P.state + ((size_t)s * P.cap + pr.slot) * P.H;
+    // the MaxEnt weight and the output bias depend only on the record and the
+    // word: issue them before the dot product so their latency overlaps it
+    const uint32_t K = act ? min(P.N, ctx_len(pr, P.N) + 1) : 0u;
+    float me = 0.0f;
+    if (gl < K) me = __ldg(P.maxent + maxent_index(pr, w, gl + 1, P.M_mask));
+    const float bias = act ? __ldg(P.nce_b + w) : 0.0f;
     float acc = 0.0f;
     if (act) {
       if (P.nce_w16) {
@@ -87,10 +93,7 @@ __global__ void __launch_bounds__(128) k_score(Params P, CallArgs A) {
     }
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    const uint32_t K = act ? min(P.N, ctx_len(pr, P.N) + 1) : 0u;
-    float me = 0.0f;
-    if (gl < K) me = __ldg(P.maxent + maxent_index(pr, w, gl + 1, P.M_mask));
-    float sc = acc + (act ? __ldg(P.nce_b + w) : 0.0f);
+    float sc = acc + bias;
 #pragma unroll
     for (uint32_t k = 0; k < 8; ++k) {
       const float v = __shfl_sync(0xffffffffu, me, (lane & ~7u) + k);
