@@ -284,6 +284,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
                        &P.excl_miss, &P.nonq_list, &P.dup_list, &P.row_src, &P.row_dst, &P.row_word};
   for (uint32_t **p : u32s) chk(dalloc(h, p, B));
   chk(dalloc(h, &P.claimed, B));
+  chk(dalloc(h, &P.score_items, B));
   uint32_t **segs[] = {&P.seg_excl_nonq, &P.seg_excl_miss, &P.seg_cnt_nonq, &P.seg_cnt_miss};
   for (uint32_t **p : segs) chk(dalloc(h, p, S));
   chk(dalloc(h, &P.tile_status, (B + rnnlm_host::SCAN_TILE - 1) / rnnlm_host::SCAN_TILE));

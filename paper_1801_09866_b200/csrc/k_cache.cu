@@ -366,7 +366,12 @@ __global__ void k_commit(Params P, CallArgs A) {
   if (!nonq) return;
   const uint32_t h = nh0 + (en - sen);
   P.nonq_list[en] = q;
+  ScoreItem it;
+  it.pr = pr;
+  it.q = q; it.s = s; it.w = w; it.pad = 0u;
   if (h >= P.cap) {                                    // out of history handles
+    it.pr.slot = NONE;
+    P.score_items[en] = it;
     P.st[q] = ST_INVALID;
     latch(P.sticky, RNNLM_E_CAPACITY);
     P.ctr[s].poisoned = 1u;                            // read from the next call on
@@ -400,6 +405,7 @@ __global__ void k_commit(Params P, CallArgs A) {
     for (uint32_t j = 1; j + 1 < P.N; ++j) nr.ctx[j] = pr.ctx[j - 1];
   }
   P.rec[cb + h] = nr;
+  P.score_items[en] = it;
   A.child[q] = h;
   if (P.cache) P.qtab[qb0 + qe].child = h;
 }

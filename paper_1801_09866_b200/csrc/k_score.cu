@@ -48,17 +48,15 @@ __global__ void __launch_bounds__(128) k_score(Params P, CallArgs A) {
   const uint32_t wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   for (uint32_t base = wg * 4; base < total; base += nw * 4) {
     const uint32_t i = base + gid;
-    uint32_t q = i < total ? P.nonq_list[i] : 0u;
-    const bool act = i < total && P.st[q] != ST_INVALID;
-    uint32_t s = 0, w = 0;
-    Rec pr;
-    pr.slot = 0;
-    for (int j = 0; j < MAX_CTX; ++j) pr.ctx[j] = NONE;
-    if (act) {
-      s = A.session[q];
-      w = A.word[q];
-      pr = P.rec[(size_t)s * P.cap + A.parent[q]];
-    }
+    ScoreItem it;
+    it.pr.slot = NONE;
+    for (int j = 0; j < MAX_CTX; ++j) it.pr.ctx[j] = NONE;
+    it.q = it.s = it.w = 0u;
+    if (i < total) it = P.score_items[i];               // one 48-byte record per query (k_commit)
+    const bool act = i < total && it.pr.slot != NONE;
+    const uint32_t q = it.q, s = act ? it.s : 0u, w = act ? it.w : 0u;
+    Rec pr = it.pr;
+    if (!act) pr.slot = 0;
     const float *h = P.state + ((size_t)s * P.cap + pr.slot) * P.H;
     // the MaxEnt weight and the output bias depend only on the record and the
     // word: issue them before the dot product so their latency overlaps it

@@ -35,6 +35,14 @@ struct __align__(32) Rec {
   uint32_t slot;
   uint32_t ctx[MAX_CTX];
 };
+// Scoring work item of a non-QHIT query, written by k_commit: the parent's
+// record (state slot + word context) and the query's session / word, so the
+// scorer needs no further lookups before its row loads.  pr.slot == NONE: the
+// query failed in k_commit (out of handles) and is not scored.
+struct __align__(16) ScoreItem {
+  Rec pr;
+  uint32_t q, s, w, pad;
+};
 // Per-session counters and allocation cursors.
 struct __align__(64) SessCtr {
   uint32_t next_handle, next_slot;
@@ -94,6 +102,7 @@ struct Params {
   uint32_t *st, *qent, *aux, *hent, *pslot, *cslot, *excl_nonq, *excl_miss;
   unsigned long long *phash;      // code hash of the parent's state (cache on; k_qcache -> k_hcache)
   uint32_t *nonq_list;
+  ScoreItem *score_items;         // [non-QHIT index] (k_commit -> k_score)
   uint32_t *dup_list;             // QHIT_NEW queries of this call (count in counts[3])
   uint8_t *claimed;               // bit 0: claimed a query-cache entry, bit 1: a hidden-cache entry
   uint32_t *row_src, *row_dst, *row_word;   // GRU rows: global state rows + word
