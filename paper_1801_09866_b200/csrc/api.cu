@@ -281,7 +281,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   chk(dalloc(h, &P.sticky, 1));
   // ---- scratch
   uint32_t **u32s[] = {&P.st, &P.qent, &P.aux, &P.hent, &P.pslot, &P.cslot, &P.excl_nonq,
-                       &P.excl_miss, &P.nonq_list, &P.dup_list, &P.row_src, &P.row_dst, &P.row_word};
+                       &P.excl_miss, &P.dup_list, &P.row_src, &P.row_dst, &P.row_word};
   for (uint32_t **p : u32s) chk(dalloc(h, p, B));
   chk(dalloc(h, &P.claimed, B));
   chk(dalloc(h, &P.score_items, B));

@@ -18,7 +18,7 @@
 //             First occurrences probe + claim the hidden cache the same way
 //   k_scan    owner == q -> MISS else SHIT; one decoupled look-back scan
 //             over (non-QHIT, MISS) flags -> dense handles and slots
-//   k_commit  records, cache values (NEW tags cleared), GRU row list, scoring list
+//   k_commit  records, cache values (NEW tags cleared), GRU row list, scoring work items
 //   k_final   QHIT results (handles), outcomes, counters, allocation cursors
 //   k_dup_scores  same-call duplicates copy their owner's score (after k_score)
 //
@@ -365,7 +365,6 @@ __global__ void k_commit(Params P, CallArgs A) {
   }
   if (!nonq) return;
   const uint32_t h = nh0 + (en - sen);
-  P.nonq_list[en] = q;
   ScoreItem it;
   it.pr = pr;
   it.q = q; it.s = s; it.w = w; it.pad = 0u;

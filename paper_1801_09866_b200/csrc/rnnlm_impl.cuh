@@ -101,7 +101,6 @@ struct Params {
   // per-call scratch (B_max)
   uint32_t *st, *qent, *aux, *hent, *pslot, *cslot, *excl_nonq, *excl_miss;
   unsigned long long *phash;      // code hash of the parent's state (cache on; k_qcache -> k_hcache)
-  uint32_t *nonq_list;
   ScoreItem *score_items;         // [non-QHIT index] (k_commit -> k_score)
   uint32_t *dup_list;             // QHIT_NEW queries of this call (count in counts[3])
   uint8_t *claimed;               // bit 0: claimed a query-cache entry, bit 1: a hidden-cache entry
