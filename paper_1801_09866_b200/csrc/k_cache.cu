@@ -396,13 +396,11 @@ __global__ void k_commit(Params P, CallArgs A) {
     sl = ns0 + (eo - sem);
   }
   P.cslot[q] = sl;
-  Rec nr;
+  Rec nr;                                              // last N-1 words of (ctx o w)
   nr.slot = sl;
-  for (int j = 0; j < MAX_CTX; ++j) nr.ctx[j] = NONE;
-  if (P.N > 1) {                                       // last N-1 words of (ctx o w)
-    nr.ctx[0] = w;
-    for (uint32_t j = 1; j + 1 < P.N; ++j) nr.ctx[j] = pr.ctx[j - 1];
-  }
+  nr.ctx[0] = P.N > 1 ? w : NONE;
+#pragma unroll
+  for (int j = 1; j < MAX_CTX; ++j) nr.ctx[j] = (uint32_t)j + 1 < P.N ? pr.ctx[j - 1] : NONE;   // static indices: registers
   P.rec[cb + h] = nr;
   P.score_items[en] = it;
   A.child[q] = h;
