@@ -54,9 +54,10 @@
 extern "C" {
 #endif
 
-#define RNNLM_ABI_VERSION 1
+#define RNNLM_ABI_VERSION 2
 
 typedef struct rnnlm rnnlm_t;          /* opaque; one per CUDA device */
+typedef struct rnnlm_graph rnnlm_graph_t;   /* opaque; a captured rnnlm_query_batch (rnnlm_graph_create) */
 typedef struct CUstream_st *rnnlm_stream_t;   /* == cudaStream_t; NULL = legacy default stream */
 
 typedef enum {
@@ -115,6 +116,10 @@ typedef struct {
   uint32_t max_histories_per_session;   /* handle/state capacity per session (>= 2); no eviction */
   int32_t device;                       /* CUDA device ordinal */
   uint32_t cell;                        /* rnnlm_cell (0 = GRU) */
+  uint32_t max_queries_per_session_call;  /* most queries ONE session has in one call (0 = max_queries_per_call);
+                                         * sizes each session's two hash tables at 2 x (this + max_histories)
+                                         * entries (load <= 0.5).  A call exceeding it stays memory-safe but
+                                         * may fail its queries with RNNLM_E_CAPACITY. */
 } rnnlm_config;
 
 /* Host fp32 row-major weights, copied at create (caller may free on return).
@@ -170,6 +175,23 @@ rnnlm_status rnnlm_reset_session(rnnlm_t *h, uint32_t session, rnnlm_stream_t st
 rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
                                const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
                                uint32_t *d_child, uint8_t *d_outcome, rnnlm_stream_t stream);
+
+/* CUDA-graph form of rnnlm_query_batch for decoder loops (SURVEY 3.2, 7 step
+ * 9): captures ONE call on fixed device buffers into an instantiated graph;
+ * every rnnlm_graph_launch replays it on `stream` (one graph launch instead of
+ * ~10 kernel launches; no host work per frame).  The caller rewrites the
+ * CONTENTS of d_session / d_parent / d_word (and *d_n) before each launch.
+ *   max_n: queries the graph is sized for (<= max_queries_per_call).
+ *   d_n: nullable device u32, the query count of each replay (read on the
+ *     device; values above max_n are clamped); NULL = always max_n.
+ * Same semantics, results and errors as rnnlm_query_batch with those inputs.
+ * rnnlm_results_ready does not apply to graph launches (the stream itself
+ * orders them).  The graph references the engine: destroy it first. */
+rnnlm_status rnnlm_graph_create(rnnlm_t *h, uint32_t max_n, const uint32_t *d_n, const uint32_t *d_session,
+                                const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
+                                uint32_t *d_child, uint8_t *d_outcome, rnnlm_graph_t **out);
+rnnlm_status rnnlm_graph_launch(rnnlm_graph_t *g, rnnlm_stream_t stream);
+void rnnlm_graph_destroy(rnnlm_graph_t *g);
 
 /* Makes `stream` wait until the per-query results of the most recent
  * rnnlm_query_batch (d_score, d_child, d_outcome) are written.  They are final

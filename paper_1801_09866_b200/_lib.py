@@ -21,7 +21,7 @@ class Config(ctypes.Structure):
                 ("math", ctypes.c_uint32), ("cache_enabled", ctypes.c_uint32),
                 ("num_sessions", ctypes.c_uint32), ("max_queries_per_call", ctypes.c_uint32),
                 ("max_histories_per_session", ctypes.c_uint32), ("device", ctypes.c_int32),
-                ("cell", ctypes.c_uint32)]
+                ("cell", ctypes.c_uint32), ("max_queries_per_session_call", ctypes.c_uint32)]
 
 
 WEIGHT_NAMES = ("emb", "Wz", "Uz", "bz", "Wr", "Ur", "br", "Wh", "Uh", "bh", "nce_w", "nce_b",
@@ -69,6 +69,10 @@ SIGNATURES = {
     "rnnlm_launch_count": (ctypes.c_uint64, [_vp]),
     "rnnlm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rnnlm_abi_version": (ctypes.c_int, []),
+    "rnnlm_graph_create": (ctypes.c_int, [_vp, ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                          ctypes.POINTER(_vp)]),
+    "rnnlm_graph_launch": (ctypes.c_int, [_vp, _vp]),
+    "rnnlm_graph_destroy": (None, [_vp]),
 }
 
 _lib = None

@@ -35,7 +35,6 @@ struct rnnlm {
   std::vector<void *> allocs;
   void *tc = nullptr;                 // tensor-core GRU state (descriptors, weights)
   void *norm = nullptr;               // log-normaliser scratch (first rnnlm_log_normalizer call)
-  uint32_t epoch = 0;
   uint64_t launches = 0;
   // scoring + result write run on a side stream, concurrently with the GRU
   cudaStream_t side = nullptr;
@@ -132,6 +131,20 @@ void free_all(rnnlm *h) {
   h->side = nullptr;
 }
 
+// Every call that launches or synchronises runs on the handle's device and
+// restores the caller's current device on return (one handle per device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const rnnlm *h) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != h->cfg.device) cudaSetDevice(h->cfg.device);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 cudaEvent_t take_event(rnnlm *h) {
   if (!h->ev_pool.empty()) {
     cudaEvent_t e = h->ev_pool.back();
@@ -207,10 +220,13 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   Params &P = h->P;
   P.V = c.vocab; P.E = c.embed; P.H = c.hidden; P.N = c.maxent_order; P.S = c.num_sessions;
   P.cap = c.max_histories_per_session;
-  // Tables hold >= cap + B_max keys at load <= 0.5: the keys claimed before a
-  // session's first capacity failure (< cap) plus one call's worth of claims
-  // (<= B_max) always fit, so claiming never depends on thread order.
-  const uint32_t tcap = next_pow2(2ull * ((uint64_t)P.cap + c.max_queries_per_call));
+  // Each session's tables hold >= cap + Bs keys at load <= 0.5, Bs = the most
+  // queries one session has in one call: the keys claimed before a session's
+  // first capacity failure (< cap) plus one call's worth of claims (<= Bs)
+  // always fit, so claiming never depends on thread order.
+  const uint64_t bs = c.max_queries_per_session_call && c.max_queries_per_session_call < c.max_queries_per_call
+                          ? c.max_queries_per_session_call : c.max_queries_per_call;
+  const uint32_t tcap = next_pow2(2ull * ((uint64_t)P.cap + bs));
   P.qmask = tcap - 1;
   P.hmask = tcap - 1;
   P.key_mode = c.key_mode; P.round_digits = c.round_digits; P.cache = c.cache_enabled ? 1 : 0;
@@ -334,6 +350,7 @@ void rnnlm_destroy(rnnlm_t *h) {
 
 rnnlm_status rnnlm_reset_session(rnnlm_t *h, uint32_t session, rnnlm_stream_t stream) {
   if (!h) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   const Params &P = h->P;
   uint32_t lo = session, hi = session + 1;
   if (session == 0xFFFFFFFFu) { lo = 0; hi = P.S; }
@@ -358,68 +375,136 @@ rnnlm_status rnnlm_reset_session(rnnlm_t *h, uint32_t session, rnnlm_stream_t st
   return cuda_status(e);
 }
 
-rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
-                               const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
-                               uint32_t *d_child, uint8_t *d_outcome, rnnlm_stream_t stream) {
-  if (!h) return RNNLM_E_INVALID_ARG;
-  if (n == 0) return RNNLM_OK;
-  if (n > h->cfg.max_queries_per_call) return RNNLM_E_INVALID_ARG;
-  if (!d_session || !d_parent || !d_word || !d_score || !d_child) return RNNLM_E_INVALID_ARG;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  CallArgs A;
-  A.n = n;
-  A.epoch = ++h->epoch;
-  if (A.epoch == 0) A.epoch = ++h->epoch;
-  A.session = d_session; A.parent = d_parent; A.word = d_word;
-  A.score = d_score; A.child = d_child; A.outcome = d_outcome;
+}  // extern "C"
+
+namespace {
+// One call's kernels on stream s (k launches returned): (a1)-(a4) on the
+// caller's stream, then the fork: (a6) scoring and (a7) result write depend
+// only on the commit, the GRU (a5) too.  Scoring + result write go to the
+// side stream and run beside the tensor-core GRU (co-resident CTAs); on the
+// tensor-core path the fork is taken after the A1 gather, so the memory-bound
+// gather has the GPU to itself.  s joins the side stream at the end.
+int enqueue_step(rnnlm *h, const CallArgs &A, cudaStream_t s, bool timed) {
   const Params &P = h->P;
   std::vector<cudaEvent_t> ev;
-  if (h->timing) {
+  if (timed) {
     for (int i = 0; i < NEV; ++i) ev.push_back(take_event(h));
     cudaEventRecord(ev[0], s);
   }
-  // (a1)-(a4) on the caller's stream
   int k = 0;
   k += rnnlm_host::launch_cache_front(P, A, s);
   k += rnnlm_host::launch_commit(P, A, s);
-  // fork: (a6) scoring and (a7) result write depend only on the commit; the
-  // GRU (a5) too.  Scoring + result write go to the side stream and run
-  // beside the tensor-core GRU (co-resident CTAs); on the tensor-core path the
-  // fork is taken after the A1 gather, so the memory-bound gather has the GPU
-  // to itself.  The caller's stream joins the side stream before returning.
   cudaEvent_t fork = h->ev_fork;
-  if (h->timing) cudaEventRecord(ev[1], s);             // ms_cache ends at the commit
+  if (timed) cudaEventRecord(ev[1], s);                 // ms_cache ends at the commit
   if (P.math != RNNLM_MATH_FP32) {
-    k += rnnlm_host::launch_gru_tc(P, h->tc, n, h->num_sms, s, h->timing >= 2 ? ev[4] : nullptr,
+    k += rnnlm_host::launch_gru_tc(P, h->tc, A.n, h->num_sms, s, timed && h->timing >= 2 ? ev[4] : nullptr,
                                    nullptr, fork);
   } else {
     cudaEventRecord(fork, s);
-    k += rnnlm_host::launch_gru_simt(P, n, h->num_sms, s);
+    k += rnnlm_host::launch_gru_simt(P, A.n, h->num_sms, s);
   }
   cudaStreamWaitEvent(h->side, fork, 0);
   k += rnnlm_host::launch_final(P, A, h->side);
-  if (h->timing) cudaEventRecord(ev[2], h->side);
+  if (timed) cudaEventRecord(ev[2], h->side);
   k += rnnlm_host::launch_score(P, A, h->num_sms, h->side);
   k += rnnlm_host::launch_dup_scores(P, A, h->num_sms, h->side);
-  if (h->timing) cudaEventRecord(ev[3], h->side);
+  if (timed) cudaEventRecord(ev[3], h->side);
   cudaEventRecord(h->ev_join, h->side);
-  if (h->timing) cudaEventRecord(ev[5], s);
+  if (timed) cudaEventRecord(ev[5], s);
   if (P.math == RNNLM_MATH_FP32)                      // the tcgen05 epilogue encodes in place
-    k += rnnlm_host::launch_encode_rows(P, n, h->num_sms, s);
-  if (h->timing) cudaEventRecord(ev[6], s);
+    k += rnnlm_host::launch_encode_rows(P, A.n, h->num_sms, s);
+  if (timed) cudaEventRecord(ev[6], s);
   cudaStreamWaitEvent(s, h->ev_join, 0);
-  if (h->timing) {
+  if (timed) {
     if (h->timing < 2) { h->ev_pool.push_back(ev[4]); ev[4] = nullptr; }
     h->ev_pending.push_back(ev);
     h->acc.calls += 1;
     h->acc.launches += (uint64_t)k;
   }
-  h->launches += (uint64_t)k;
+  return k;
+}
+}  // namespace
+
+struct rnnlm_graph {
+  rnnlm *h = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int kernels = 0;
+};
+
+extern "C" {
+
+rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
+                               const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
+                               uint32_t *d_child, uint8_t *d_outcome, rnnlm_stream_t stream) {
+  if (!h) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
+  if (n == 0) return RNNLM_OK;
+  if (n > h->cfg.max_queries_per_call) return RNNLM_E_INVALID_ARG;
+  if (!d_session || !d_parent || !d_word || !d_score || !d_child) return RNNLM_E_INVALID_ARG;
+  CallArgs A;
+  A.n = n;
+  A.d_n = nullptr;
+  A.session = d_session; A.parent = d_parent; A.word = d_word;
+  A.score = d_score; A.child = d_child; A.outcome = d_outcome;
+  h->launches += (uint64_t)enqueue_step(h, A, reinterpret_cast<cudaStream_t>(stream), h->timing != 0);
   return cuda_status(cudaGetLastError());
+}
+
+rnnlm_status rnnlm_graph_create(rnnlm_t *h, uint32_t max_n, const uint32_t *d_n, const uint32_t *d_session,
+                                const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
+                                uint32_t *d_child, uint8_t *d_outcome, rnnlm_graph_t **out) {
+  if (!out) return RNNLM_E_INVALID_ARG;
+  *out = nullptr;
+  if (!h || max_n == 0 || max_n > h->cfg.max_queries_per_call) return RNNLM_E_INVALID_ARG;
+  if (!d_session || !d_parent || !d_word || !d_score || !d_child) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
+  CallArgs A;
+  A.n = max_n;
+  A.d_n = d_n;
+  A.session = d_session; A.parent = d_parent; A.word = d_word;
+  A.score = d_score; A.child = d_child; A.outcome = d_outcome;
+  rnnlm_graph *g = new (std::nothrow) rnnlm_graph;
+  if (!g) return RNNLM_E_OOM;
+  g->h = h;
+  cudaStream_t cs = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (!e) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (!e) {
+    g->kernels = enqueue_step(h, A, cs, false);
+    e = cudaStreamEndCapture(cs, &g->graph);
+  }
+  if (!e) e = cudaGraphInstantiateWithFlags(&g->exec, g->graph, 0);
+  if (cs) cudaStreamDestroy(cs);
+  if (e) {
+    (void)cudaGetLastError();
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return cuda_status(e);
+  }
+  *out = g;
+  return RNNLM_OK;
+}
+
+rnnlm_status rnnlm_graph_launch(rnnlm_graph_t *g, rnnlm_stream_t stream) {
+  if (!g) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(g->h);
+  g->h->launches += (uint64_t)g->kernels;
+  return cuda_status(cudaGraphLaunch(g->exec, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+void rnnlm_graph_destroy(rnnlm_graph_t *g) {
+  if (!g) return;
+  DeviceGuard dg(g->h);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
 }
 
 rnnlm_status rnnlm_cache_stats(rnnlm_t *h, uint32_t session, rnnlm_stats *out) {
   if (!h || !out) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   const Params &P = h->P;
   if (session != 0xFFFFFFFFu && session >= P.S) return RNNLM_E_INVALID_ARG;
   cudaError_t e = cudaDeviceSynchronize();
@@ -445,6 +530,7 @@ rnnlm_status rnnlm_cache_stats(rnnlm_t *h, uint32_t session, rnnlm_stats *out) {
 rnnlm_status rnnlm_read_states(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
                                float *d_states, rnnlm_stream_t stream) {
   if (!h || (n && (!d_handles || !d_states))) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   h->launches += rnnlm_host::launch_read_states(h->P, session, n, d_handles, d_states,
                                                 reinterpret_cast<cudaStream_t>(stream));
   return cuda_status(cudaGetLastError());
@@ -453,6 +539,7 @@ rnnlm_status rnnlm_read_states(rnnlm_t *h, uint32_t session, uint32_t n, const u
 rnnlm_status rnnlm_read_slots(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
                               uint32_t *d_slots, rnnlm_stream_t stream) {
   if (!h || (n && (!d_handles || !d_slots))) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   h->launches += rnnlm_host::launch_read_slots(h->P, session, n, d_handles, d_slots,
                                                reinterpret_cast<cudaStream_t>(stream));
   return cuda_status(cudaGetLastError());
@@ -461,6 +548,7 @@ rnnlm_status rnnlm_read_slots(rnnlm_t *h, uint32_t session, uint32_t n, const ui
 rnnlm_status rnnlm_read_codes(rnnlm_t *h, uint32_t session, uint32_t n, const uint32_t *d_handles,
                               uint8_t *d_codes, rnnlm_stream_t stream) {
   if (!h || (n && (!d_handles || !d_codes))) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   if (!h->P.cache && h->P.key_mode != RNNLM_KEY_OFF) return RNNLM_E_INVALID_ARG;  // no arena
   h->launches += rnnlm_host::launch_read_codes(h->P, session, n, d_handles, d_codes,
                                                reinterpret_cast<cudaStream_t>(stream));
@@ -470,6 +558,7 @@ rnnlm_status rnnlm_read_codes(rnnlm_t *h, uint32_t session, uint32_t n, const ui
 rnnlm_status rnnlm_encode_states(rnnlm_t *h, uint32_t n, const float *d_states, uint8_t *d_codes,
                                  rnnlm_stream_t stream) {
   if (!h || (n && (!d_states || !d_codes))) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   Params P = h->P;
   if (P.key_mode != RNNLM_KEY_OFF && P.cstride == 0) return RNNLM_E_INVALID_ARG;
   h->launches += rnnlm_host::launch_encode_states(P, n, d_states, d_codes,
@@ -481,6 +570,7 @@ rnnlm_status rnnlm_maxent_indices(rnnlm_t *h, uint32_t n, const uint32_t *d_sess
                                   const uint32_t *d_parent, const uint32_t *d_word, uint64_t *d_idx,
                                   rnnlm_stream_t stream) {
   if (!h || (n && (!d_session || !d_parent || !d_word || !d_idx))) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   h->launches += rnnlm_host::launch_maxent_indices(
       h->P, n, d_session, d_parent, d_word, reinterpret_cast<unsigned long long *>(d_idx),
       reinterpret_cast<cudaStream_t>(stream));
@@ -489,6 +579,7 @@ rnnlm_status rnnlm_maxent_indices(rnnlm_t *h, uint32_t n, const uint32_t *d_sess
 
 rnnlm_status rnnlm_results_ready(rnnlm_t *h, rnnlm_stream_t stream) {
   if (!h) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   // every result write (k_commit on the caller's stream before the fork;
   // k_final, k_score, k_dup_scores on the side stream) precedes ev_join
   return cuda_status(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), h->ev_join, 0));
@@ -497,6 +588,7 @@ rnnlm_status rnnlm_results_ready(rnnlm_t *h, rnnlm_stream_t stream) {
 rnnlm_status rnnlm_log_normalizer(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
                                   const uint32_t *d_history, float *d_log_z, rnnlm_stream_t stream) {
   if (!h) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   if (n == 0) return RNNLM_OK;
   if (n > h->cfg.max_queries_per_call || !d_session || !d_history || !d_log_z) return RNNLM_E_INVALID_ARG;
   if (!rnnlm_host::norm_supported(h->P.H, h->P.N)) return RNNLM_E_DIMENSION;
@@ -527,6 +619,7 @@ rnnlm_status rnnlm_set_timing(rnnlm_t *h, int level) {
 
 rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset) {
   if (!h || !out) return RNNLM_E_INVALID_ARG;
+  DeviceGuard dg(h);
   for (auto &ev : h->ev_pending) {
     cudaError_t e = cudaEventSynchronize(ev[6]);
     if (!e) e = cudaEventSynchronize(ev[3]);

@@ -97,7 +97,8 @@ __global__ void k_qcache(Params P, CallArgs A, uint32_t ntiles) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < ntiles) P.tile_status[q] = 0ull;
   if (q == 0) { *P.tile_ticket = 0u; P.counts[3] = 0u; }
-  if (q >= A.n) return;
+  const uint32_t n = call_n(A);
+  if (q >= n) return;
   const uint32_t s = A.session[q], w = A.word[q], p = A.parent[q];
   const uint32_t sprev = q > 0 ? A.session[q - 1] : 0u;
   const uint32_t sc = s < P.S ? s : 0u, pc = p < P.cap ? p : 0u;
@@ -115,7 +116,7 @@ __global__ void k_qcache(Params P, CallArgs A, uint32_t ntiles) {
   else if (w >= P.V) err = RNNLM_E_VOCAB;
   else if (poisoned) err = RNNLM_E_CAPACITY;
   else if (p >= nh) err = RNNLM_E_HISTORY;
-  if (q > 0 && sprev > s) P.counts[2] = A.epoch;       // batch not sorted by session
+  if (q > 0 && sprev > s) P.counts[2] = 1u;            // batch not sorted by session
   if (err) {
     P.st[q] = ST_INVALID;
     latch(P.sticky, err);
@@ -151,9 +152,9 @@ __global__ void k_qcache(Params P, CallArgs A, uint32_t ntiles) {
 __global__ void k_hcache(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= A.n) return;
+  if (q >= call_n(A)) return;
   const uint32_t st = P.st[q];
-  const bool bad = P.counts[2] == A.epoch;
+  const bool bad = P.counts[2] != 0u;
   const uint32_t s = A.session[q], w = A.word[q], qe = P.qent[q], ps = P.pslot[q];
   const unsigned long long hh = P.phash[q];
   if (st != ST_QNEED || bad) return;
@@ -209,7 +210,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
   if (threadIdx.x == 0) s_tile = atomicAdd(P.tile_ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const bool bad = P.counts[2] == A.epoch;
+  const bool bad = P.counts[2] != 0u;
+  const uint32_t n = call_n(A);
   const uint32_t q0 = tile * rnnlm_host::SCAN_TILE + threadIdx.x * SCAN_ITEMS;
   unsigned long long v[SCAN_ITEMS];
   unsigned long long tsum = 0;
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
   for (int i = 0; i < SCAN_ITEMS; ++i) {
     const uint32_t q = q0 + i;
     uint32_t nonq = 0, miss = 0;
-    if (q < A.n) {
+    if (q < n) {
       uint32_t st = P.st[q];
       const uint32_t sq = A.session[q], he = P.hent[q];
       if (bad) {
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; ++i) {
     const uint32_t q = q0 + i;
-    if (q < A.n) {
+    if (q < n) {
       P.excl_nonq[q] = (uint32_t)(run >> 32);
       P.excl_miss[q] = (uint32_t)run;
       const uint32_t s = A.session[q];
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
         P.seg_excl_nonq[s] = (uint32_t)(run >> 32);
         P.seg_excl_miss[s] = (uint32_t)run;
       }
-      if (q == A.n - 1) {
+      if (q == n - 1) {
         const unsigned long long tot = run + v[i];
         P.counts[0] = (uint32_t)(tot >> 32);
         P.counts[1] = (uint32_t)tot;
@@ -325,15 +327,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Params P, CallArgs A) {
 __global__ void k_commit(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= A.n) return;
+  const uint32_t n = call_n(A);
+  if (q >= n) return;
   const uint32_t st = P.st[q];
   const uint32_t s = A.session[q];
-  const uint32_t snext = q + 1 < A.n ? A.session[q + 1] : NONE;
+  const uint32_t snext = q + 1 < n ? A.session[q + 1] : NONE;
   const uint32_t w = A.word[q], p = A.parent[q];
   const uint32_t en = P.excl_nonq[q], r = P.excl_miss[q];
   const uint32_t qe = P.qent[q], he = P.hent[q], cs = P.cslot[q], ax = P.aux[q], ps = P.pslot[q];
   const uint8_t cl = P.claimed[q];
-  const bool bad = P.counts[2] == A.epoch;
+  const bool bad = P.counts[2] != 0u;
   const bool nonq = (st == ST_SHIT_OLD || st == ST_SHIT_NEW || st == ST_MISS || st == ST_MISS_NC);
   const bool miss = (st == ST_MISS || st == ST_MISS_NC);
   // second round trip (indices clamped in bounds; unused values are discarded)
@@ -377,7 +380,11 @@ __global__ void k_commit(Params P, CallArgs A) {
     A.score[q] = __int_as_float(0x7fc00000);
     A.child[q] = NONE;
     if (P.cache) { P.qtab[qb0 + qe].child = NONE; P.qtab[qb0 + qe].score = __int_as_float(0x7fc00000); }
-    if (miss) P.row_dst[r] = NONE;
+    if (miss) {                                        // a GRU row that is computed and discarded:
+      P.row_src[r] = (uint32_t)cb;                     // in-range gather indices (the session's root)
+      P.row_word[r] = 0u;
+      P.row_dst[r] = NONE;
+    }
     return;
   }
   uint32_t sl;
@@ -411,7 +418,8 @@ __global__ void k_commit(Params P, CallArgs A) {
 __global__ void k_final(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = q < A.n;
+  const uint32_t n = call_n(A);
+  const bool active = q < n;
   uint32_t st = active ? P.st[q] : ST_INVALID;
   const uint32_t s = active ? A.session[q] : NONE;
   uint8_t oc = RNNLM_INVALID;
@@ -463,7 +471,7 @@ __global__ void k_final(Params P, CallArgs A) {
     if (t_hh) atomicAdd(&c->hhits, (unsigned long long)t_hh);
     if (t_gru) atomicAdd(&c->gru, (unsigned long long)t_gru);
   }
-  if (active && P.counts[2] != A.epoch && s < P.S && (q == A.n - 1 || A.session[q + 1] != s)) {
+  if (active && P.counts[2] == 0u && s < P.S && (q == n - 1 || A.session[q + 1] != s)) {
     SessCtr *c = &P.ctr[s];
     const uint32_t nh = c->next_handle + P.seg_cnt_nonq[s];
     const uint32_t ns = c->next_slot + P.seg_cnt_miss[s];
@@ -473,9 +481,13 @@ __global__ void k_final(Params P, CallArgs A) {
 }
 
 // Duplicates of this call's new queries (QHIT_NEW) take their owner's score.
+// It is the call's last kernel: it also clears the bad-batch flag (every
+// reader -- k_hcache, k_scan, k_commit, k_final -- has completed), so the
+// host passes no per-call state and a call can be replayed as a CUDA graph.
 __global__ void k_dup_scores(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t nd = P.counts[3];
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.counts[2] = 0u;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
     const uint32_t q = P.dup_list[i];
     A.score[q] = A.score[P.aux[q]];

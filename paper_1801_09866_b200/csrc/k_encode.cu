@@ -1,80 +1,13 @@
 // k_encode.cu -- step (a1): compression key of a history vector.
 //
-// "we propose to quantize the history vectors by controlling the precision of
-// history vector itself by rounding up to a specified decimal point.  We also
-// consider an extreme case, in which we store only the signs of each element"
-// (Table 1).  Readings 3-6:
-//   sign     bit_i = (h_i >= 0.0f)                  (IEEE compare: -0 -> 1)
-//   round:k  q_i = roundf(__fmul_rn(h_i, 10^k))     (fp32 product, half away)
-//            int8 for k <= 2, little-endian int16 for k = 3, 4
-//   off      the fp32 bit pattern (the state row itself is the code)
-// The code is a pure function of the stored fp32 state, so it is computed
-// ONCE when a state is created (after the GRU) and stored with its slot,
-// together with a 64-bit hash of the code words used as the probe position of
-// the hidden-state cache.  Cache decisions always compare the full code, so
-// the hash never decides a hit.
-#include "rnnlm_impl.cuh"
+// The code (readings 3-6) is a pure function of the stored fp32 state, so it
+// is computed ONCE when a state is created and stored with its slot, together
+// with a 64-bit hash of the code words used as the probe position of the
+// hidden-state cache; cache decisions always compare the full code.  The
+// encoder itself is encode.cuh's encode32, shared with the tcgen05 epilogues.
+#include "encode.cuh"
 
 namespace rnnlm_dev {
-
-// One warp encodes one row.  Returns the code hash in every lane.
-__device__ unsigned long long encode_row_warp(const Params &P, const float *__restrict__ h,
-                                              uint8_t *__restrict__ code) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t H = P.H;
-  unsigned long long hs = 0;
-  uint32_t *cw = reinterpret_cast<uint32_t *>(code);
-  if (P.key_mode == RNNLM_KEY_SIGN) {
-    const uint32_t nwords = (H + 31) / 32;
-    for (uint32_t wi = 0; wi < nwords; ++wi) {
-      const uint32_t i = wi * 32 + lane;
-      const bool b = (i < H) && (h[i] >= 0.0f);
-      const uint32_t bits = __ballot_sync(0xffffffffu, b);
-      if (lane == 0) {
-        if (cw) cw[wi] = bits;
-        hs += mix64(((unsigned long long)wi << 32) | bits);
-      }
-    }
-    for (uint32_t wi = nwords + lane; cw && wi < P.cstride / 4; wi += 32) cw[wi] = 0u;
-  } else if (P.key_mode == RNNLM_KEY_ROUND) {
-    const float scale = P.round_scale;
-    if (P.round_digits <= 2) {                       // 4 int8 codes per word
-      const uint32_t nwords = (H + 3) / 4;
-      for (uint32_t wi = lane; wi < nwords; wi += 32) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t e = wi * 4 + j;
-          const int q = e < H ? (int)roundf(__fmul_rn(h[e], scale)) : 0;
-          word |= ((uint32_t)(uint8_t)(int8_t)q) << (8 * j);
-        }
-        if (cw) cw[wi] = word;
-        hs += mix64(((unsigned long long)wi << 32) | word);
-      }
-      for (uint32_t wi = nwords + lane; cw && wi < P.cstride / 4; wi += 32) cw[wi] = 0u;
-    } else {                                         // 2 int16 codes per word
-      const uint32_t nwords = (H + 1) / 2;
-      for (uint32_t wi = lane; wi < nwords; wi += 32) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint32_t e = wi * 2 + j;
-          const int q = e < H ? (int)roundf(__fmul_rn(h[e], scale)) : 0;
-          word |= ((uint32_t)(uint16_t)(int16_t)q) << (16 * j);
-        }
-        if (cw) cw[wi] = word;
-        hs += mix64(((unsigned long long)wi << 32) | word);
-      }
-      for (uint32_t wi = nwords + lane; cw && wi < P.cstride / 4; wi += 32) cw[wi] = 0u;
-    }
-  } else {                                           // off: the bit pattern itself
-    for (uint32_t wi = lane; wi < H; wi += 32)
-      hs += mix64(((unsigned long long)wi << 32) | __float_as_uint(h[wi]));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
-  return hs;
-}
 
 // New states of this call: rows r < counts[1] (GRU rows), code + hash per row.
 __global__ void k_encode_rows(Params P) {
@@ -85,7 +18,7 @@ __global__ void k_encode_rows(Params P) {
     const uint32_t dst = P.row_dst[r];
     if (dst == NONE) continue;
     uint8_t *code = P.key_mode == RNNLM_KEY_OFF ? nullptr : P.codes + (size_t)dst * P.cstride;
-    const unsigned long long hs = encode_row_warp(P, P.state + (size_t)dst * P.H, code);
+    const unsigned long long hs = encode_row_warp(key_spec(P), P.cstride, P.state + (size_t)dst * P.H, code);
     if ((threadIdx.x & 31) == 0) P.codehash[dst] = hs;
   }
 }
@@ -107,7 +40,7 @@ __global__ void k_reset_root(Params P, uint32_t lo) {
   __syncthreads();
   if (threadIdx.x < 32 && P.cache) {
     uint8_t *code = P.key_mode == RNNLM_KEY_OFF ? nullptr : P.codes + row * P.cstride;
-    const unsigned long long hs = encode_row_warp(P, P.state + row * P.H, code);
+    const unsigned long long hs = encode_row_warp(key_spec(P), P.cstride, P.state + row * P.H, code);
     if (threadIdx.x == 0) P.codehash[row] = hs;
   }
 }
@@ -127,7 +60,7 @@ __global__ void k_encode_states(Params P, uint32_t n, const float *__restrict__ 
     return;
   }
   uint8_t *code = sm_code + (size_t)wib * P.cstride;
-  encode_row_warp(P, h, code);
+  encode_row_warp(key_spec(P), P.cstride, h, code);
   __syncwarp();
   for (uint32_t b = threadIdx.x & 31; b < P.code_bytes; b += 32) dst[b] = code[b];
 }

@@ -51,6 +51,7 @@
 
 #include "rnnlm_impl.cuh"
 #include "tc_common.cuh"
+#include "encode.cuh"
 
 namespace rnnlm_tc {
 using namespace rnnlm_dev;
@@ -403,58 +404,10 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
   if (prof && lane == 0) { prof[2] = w_full; prof[3] = w_tempty; }
 }
 
-// Compression code words of 16 consecutive new-state elements starting at
-// unit u0 (same packing and hash terms as k_encode.cu's encode_row_warp):
-// sign: bits of a 32-bit word (two calls fill one word), round: int8 / int16
-// codes, off: the fp32 bit patterns.  Returns the hash contribution.
-__device__ __forceinline__ unsigned long long encode16(const TcArgs &a, const float *hn, uint32_t u0,
-                                                       uint8_t *code, uint32_t &signacc) {
-  unsigned long long hs = 0;
-  if (a.key_mode == RNNLM_KEY_SIGN) {
-    uint32_t b = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) b |= (hn[j] >= 0.0f ? 1u : 0u) << j;
-    if ((u0 & 31) == 0) {
-      signacc = b;
-    } else {
-      const uint32_t word = signacc | (b << 16);
-      const uint32_t wi = u0 >> 5;
-      reinterpret_cast<uint32_t *>(code)[wi] = word;
-      hs += mix64(((unsigned long long)wi << 32) | word);
-    }
-  } else if (a.key_mode == RNNLM_KEY_ROUND) {
-    if (a.round_digits <= 2) {
-      uint32_t w[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          word |= ((uint32_t)(uint8_t)(int8_t)(int)roundf(__fmul_rn(hn[4 * i + j], a.round_scale))) << (8 * j);
-        w[i] = word;
-        hs += mix64(((unsigned long long)(u0 / 4 + i) << 32) | word);
-      }
-      *reinterpret_cast<uint4 *>(code + u0) = make_uint4(w[0], w[1], w[2], w[3]);
-    } else {
-      uint32_t w[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          word |= ((uint32_t)(uint16_t)(int16_t)(int)roundf(__fmul_rn(hn[2 * i + j], a.round_scale))) << (16 * j);
-        w[i] = word;
-        hs += mix64(((unsigned long long)(u0 / 2 + i) << 32) | word);
-      }
-      *reinterpret_cast<uint4 *>(code + 2 * u0) = make_uint4(w[0], w[1], w[2], w[3]);
-      *reinterpret_cast<uint4 *>(code + 2 * u0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      hs += mix64(((unsigned long long)(u0 + j) << 32) | __float_as_uint(hn[j]));
-  }
-  return hs;
+// (a1) compression code of the new state: encode.cuh's encode32 (the same
+// device code as k_encode_rows and rnnlm_encode_states).
+__device__ __forceinline__ KeySpec key_spec(const TcArgs &a) {
+  return KeySpec{a.key_mode, a.round_digits, a.H, a.round_scale};
 }
 
 
@@ -633,7 +586,6 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
   uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && live) ? a.codes + (size_t)dst * a.cstride : nullptr;
   const float4 *zq = reinterpret_cast<const float4 *>(a.g_z) + zq4(live ? row : 0, n0, a.H);
   unsigned long long hs = 0;
-  uint32_t signacc = 0;
 #pragma unroll 1
   for (uint32_t c = 0; c < units / 32; ++c) {           // chunks of 32 units
     float v[32], b[32], z[32], h[32];
@@ -655,10 +607,7 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
     __syncwarp();
     put_row_f32(stg, lane, h);
     coop_store<128>(stg, hout ? hout + c * 32 : nullptr, lane);
-    if (a.cache && live) {
-      hs += encode16(a, h, n0 + c * 32, code, signacc);
-      hs += encode16(a, h + 16, n0 + c * 32 + 16, code, signacc);
-    }
+    if (a.cache && live) hs += encode32(key_spec(a), h, n0 + c * 32, code);
   }
   if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
 }
@@ -672,7 +621,6 @@ __device__ __forceinline__ void epi_rnn(const TcArgs &a, uint32_t tbase, uint32_
   float *hout = live ? a.state_out + (size_t)dst * a.H + n0 : nullptr;
   uint8_t *code = (a.cache && a.key_mode != RNNLM_KEY_OFF && live) ? a.codes + (size_t)dst * a.cstride : nullptr;
   unsigned long long hs = 0;
-  uint32_t signacc = 0;
 #pragma unroll 1
   for (uint32_t c = 0; c < units / 32; ++c) {           // chunks of 32 units
     float v[32], b[32];
@@ -685,10 +633,7 @@ __device__ __forceinline__ void epi_rnn(const TcArgs &a, uint32_t tbase, uint32_
     __syncwarp();
     put_row_f32(stg, lane, v);
     coop_store<128>(stg, hout ? hout + c * 32 : nullptr, lane);
-    if (a.cache && live) {
-      hs += encode16(a, v, n0 + c * 32, code, signacc);
-      hs += encode16(a, v + 16, n0 + c * 32 + 16, code, signacc);
-    }
+    if (a.cache && live) hs += encode32(key_spec(a), v, n0 + c * 32, code);
   }
   if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
 }
@@ -741,7 +686,7 @@ __device__ __forceinline__ void epi_lbr(const TcArgs &a, uint32_t tacc, uint32_t
     for (int c = 0; c < 4; ++c)
       *reinterpret_cast<float4 *>(stg + stg_off<128>(lane, 4 * g + c)) =
           make_float4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
-    if (a.cache && live) hs += encode16(a, h, u0 + g * 16, code, signacc);
+    if (a.cache && live) hs += encode16(key_spec(a), h, u0 + g * 16, code, signacc);
   }
   coop_store<128>(stg, live ? a.state_out + (size_t)dst * a.H + u0 : nullptr, lane);
   if (a.cache && live) atomicAdd(&a.codehash[dst], hs);

@@ -39,7 +39,7 @@ struct __align__(32) Rec {
 // record (state slot + word context) and the query's session / word, so the
 // scorer needs no further lookups before its row loads.  pr.slot == NONE: the
 // query failed in k_commit (out of handles) and is not scored.
-struct __align__(16) ScoreItem {
+struct __align__(32) ScoreItem {
   Rec pr;
   uint32_t q, s, w, pad;
 };
@@ -108,15 +108,15 @@ struct Params {
   uint32_t *seg_excl_nonq, *seg_excl_miss, *seg_cnt_nonq, *seg_cnt_miss;  // per session
   unsigned long long *tile_status;
   uint32_t *tile_ticket;
-  uint32_t *counts;               // [0] non-QHIT total, [1] GRU rows, [2] bad-batch epoch, [3] duplicates
+  uint32_t *counts;               // [0] non-QHIT total, [1] GRU rows, [2] bad-batch flag (cleared by the call's last kernel), [3] duplicates
   // GRU intermediates (rows x H)
   float *g_z, *g_rh, *g_wxb;
   __nv_bfloat16 *g_rh16;
 };
 
 struct CallArgs {
-  uint32_t n;
-  uint32_t epoch;                 // host call counter (bad-batch flag tag)
+  uint32_t n;                     // queries of the call (the grids' size); with d_n: the maximum
+  const uint32_t *d_n;            // nullable: the call's query count, read on the device (graph replay, <= n)
   const uint32_t *session, *parent, *word;
   float *score;
   uint32_t *child;
@@ -133,6 +133,14 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 }
 
 __device__ __forceinline__ void latch(int *sticky, int err) { atomicCAS(sticky, 0, err); }
+
+// The call's query count: host-given, or read from device memory (a replayed
+// CUDA graph sized for A.n queries serves any count up to A.n).
+__device__ __forceinline__ uint32_t call_n(const CallArgs &A) {
+  if (!A.d_n) return A.n;
+  const uint32_t n = *A.d_n;
+  return n < A.n ? n : A.n;
+}
 
 // Programmatic dependent launch (PDL): every kernel of the step is launched
 // with programmatic stream serialisation, so its launch and CTA rasterisation

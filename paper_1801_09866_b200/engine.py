@@ -40,11 +40,11 @@ class RNNLM:
                  maxent_order: int, key_mode: int = KEY_OFF, round_digits: int = 0,
                  math: int = MATH_FP32, cache_enabled: bool = True, num_sessions: int = 1,
                  max_queries_per_call: int = 4096, max_histories_per_session: int = 1 << 16,
-                 device: int = 0, cell: int = 0):
+                 device: int = 0, cell: int = 0, max_queries_per_session_call: int = 0):
         L = _lib.load()
         self.cfg = Config(vocab, embed, hidden, maxent_log2, maxent_order, key_mode, round_digits,
                           math, 1 if cache_enabled else 0, num_sessions, max_queries_per_call,
-                          max_histories_per_session, device, cell)
+                          max_histories_per_session, device, cell, max_queries_per_session_call)
         self.device = torch.device("cuda", device)
         arrs = {k: np.ascontiguousarray(weights[k], dtype=np.float32) for k in _lib.WEIGHT_NAMES}
         w = Weights(**{k: arrs[k].ctypes.data_as(ctypes.c_void_p) for k in _lib.WEIGHT_NAMES})
@@ -87,6 +87,18 @@ class RNNLM:
                                             _ptr(score), _ptr(child), _ptr(outcome),
                                             _stream(stream)), "rnnlm_query_batch")
         return score, child, outcome
+
+    def graph(self, max_n: int, session: torch.Tensor, parent: torch.Tensor, word: torch.Tensor,
+              score: torch.Tensor, child: torch.Tensor, outcome: torch.Tensor | None = None,
+              n: torch.Tensor | None = None) -> "StepGraph":
+        """rnnlm_graph_create: one query_batch captured on these buffers; replay
+        with ``.launch()`` after rewriting their contents (and ``n``, a 1-element
+        int32 device tensor holding the query count)."""
+        g = ctypes.c_void_p()
+        check(_lib.load().rnnlm_graph_create(self._h, int(max_n), _ptr(n), _ptr(session), _ptr(parent),
+                                             _ptr(word), _ptr(score), _ptr(child), _ptr(outcome),
+                                             ctypes.byref(g)), "rnnlm_graph_create")
+        return StepGraph(self, g, (session, parent, word, score, child, outcome, n))
 
     def log_normalizer(self, session: torch.Tensor, history: torch.Tensor, out: torch.Tensor | None = None,
                        stream=None) -> torch.Tensor:
@@ -163,6 +175,27 @@ class RNNLM:
 
     def launch_count(self) -> int:
         return int(_lib.load().rnnlm_launch_count(self._h))
+
+
+class StepGraph:
+    """A captured rnnlm_query_batch (rnnlm_graph_t); keeps its buffers alive."""
+
+    def __init__(self, eng: RNNLM, g: ctypes.c_void_p, keep):
+        self.eng, self._g, self._keep = eng, g, keep
+
+    def launch(self, stream=None):
+        check(_lib.load().rnnlm_graph_launch(self._g, _stream(stream)), "rnnlm_graph_launch")
+
+    def close(self):
+        if getattr(self, "_g", None):
+            _lib.load().rnnlm_graph_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def resolve_parents(ref: torch.Tensor, log: torch.Tensor, out: torch.Tensor, stream=None):

@@ -27,21 +27,22 @@ import torch
 from . import engine as _engine
 
 
-def levels(parent_ref: np.ndarray, n_per_frame: int) -> np.ndarray:
-    """Dependency level of every query (int32); parents reference earlier frames."""
+def levels(parent_ref: np.ndarray, frame_ptr: np.ndarray) -> np.ndarray:
+    """Dependency level of every query (int32); parents reference earlier frames
+    (frame t = queries [frame_ptr[t], frame_ptr[t+1]))."""
     n = parent_ref.shape[0]
     lv = np.zeros(n, dtype=np.int32)
-    for lo in range(0, n, n_per_frame):
-        ref = parent_ref[lo:lo + n_per_frame]
-        lv[lo:lo + n_per_frame] = np.where(ref < 0, 0, lv[np.maximum(ref, 0)] + 1)
+    for lo, hi in zip(frame_ptr[:-1], frame_ptr[1:]):
+        ref = parent_ref[lo:hi]
+        lv[lo:hi] = np.where(ref < 0, 0, lv[np.maximum(ref, 0)] + 1)
     return lv
 
 
-def level_schedule(session: np.ndarray, parent_ref: np.ndarray, n_per_frame: int,
+def level_schedule(session: np.ndarray, parent_ref: np.ndarray, frame_ptr: np.ndarray,
                    max_batch: int) -> list:
     """Batches (int64 index arrays) in execution order: by level, then session,
     then stream order; a level larger than ``max_batch`` is split."""
-    lv = levels(parent_ref, n_per_frame)
+    lv = levels(parent_ref, frame_ptr)
     idx = np.arange(lv.shape[0], dtype=np.int64)
     order = np.lexsort((idx, session.astype(np.int64), lv.astype(np.int64)))
     lvs = lv[order]
@@ -60,7 +61,7 @@ class OfflineRunner:
     def __init__(self, eng: "_engine.RNNLM", wl, max_batch: int, device=None):
         self.eng = eng
         self.device = device or eng.device
-        self.batches = level_schedule(wl.session, wl.parent_ref, wl.n_per_frame, max_batch)
+        self.batches = level_schedule(wl.session, wl.parent_ref, wl.frame_ptr, max_batch)
         dev = self.device
         self.d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
         self.d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)

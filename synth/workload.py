@@ -38,47 +38,74 @@ import numpy as np
 @dataclasses.dataclass
 class Workload:
     S: int                 # sessions (utterance streams)
-    B_s: int               # queries per session per frame
+    B_s: int               # queries per session per frame (at most)
     frames: int
     V: int
-    session: np.ndarray    # uint32 [frames*S*B_s], session-major inside a frame
+    session: np.ndarray    # uint32, session-major inside a frame
     parent_ref: np.ndarray  # int64, -1 = root history
     word: np.ndarray       # uint32
     new_per_session: np.ndarray  # int64 [S]: number of first emissions (>= distinct pairs)
+    frame_ptr: np.ndarray = None  # int64 [frames+1]: frame t = queries [ptr[t], ptr[t+1]); None = S*B_s each
+
+    def __post_init__(self):
+        if self.frame_ptr is None:
+            self.frame_ptr = np.arange(self.frames + 1, dtype=np.int64) * (self.S * self.B_s)
 
     @property
     def n_per_frame(self) -> int:
-        return self.S * self.B_s
+        """The largest frame (sizes the engine's max_queries_per_call)."""
+        return int(np.max(np.diff(self.frame_ptr))) if self.frames else 0
 
     @property
     def n_total(self) -> int:
-        return self.frames * self.n_per_frame
+        return int(self.frame_ptr[-1])
 
     def frame_slice(self, t: int) -> slice:
-        n = self.n_per_frame
-        return slice(t * n, (t + 1) * n)
+        return slice(int(self.frame_ptr[t]), int(self.frame_ptr[t + 1]))
 
     def max_histories_hint(self) -> int:
         """Upper bound on history handles any session can need (+root)."""
         return int(self.new_per_session.max()) + 2
 
+    def _select(self, keep: np.ndarray, frame_of: np.ndarray, frames: int, session: np.ndarray,
+                S: int, new_per_session: np.ndarray) -> "Workload":
+        """Queries with keep[i], placed in frame frame_of[i] (stable order inside a
+        frame), references re-based; a kept query's parent must be kept."""
+        idx = np.nonzero(keep)[0]
+        order = idx[np.argsort(frame_of[idx], kind="stable")]
+        remap = np.full(self.n_total, -1, dtype=np.int64)
+        remap[order] = np.arange(len(order))
+        pr = self.parent_ref[order]
+        pr2 = np.where(pr >= 0, remap[np.maximum(pr, 0)], -1)
+        assert not np.any((pr >= 0) & (pr2 < 0)), "a kept query's parent was dropped"
+        ptr = np.searchsorted(frame_of[order], np.arange(frames + 1), side="left").astype(np.int64)
+        return Workload(S=S, B_s=self.B_s, frames=frames, V=self.V,
+                        session=session[order].astype(np.uint32), parent_ref=pr2.astype(np.int64),
+                        word=self.word[order].copy(), new_per_session=new_per_session, frame_ptr=ptr)
+
+    def frame_index(self) -> np.ndarray:
+        """Frame of every query."""
+        return np.repeat(np.arange(self.frames, dtype=np.int64), np.diff(self.frame_ptr))
+
     def select_sessions(self, lo: int, hi: int) -> "Workload":
         """Sessions [lo, hi) as their own workload (references re-based)."""
-        S2 = hi - lo
-        sel = []
-        remap = np.full(self.n_total, -1, dtype=np.int64)
-        for t in range(self.frames):
-            base = t * self.n_per_frame
-            idx = np.arange(base + lo * self.B_s, base + hi * self.B_s)
-            remap[idx] = t * S2 * self.B_s + np.arange(S2 * self.B_s)
-            sel.append(idx)
-        sel = np.concatenate(sel) if sel else np.zeros(0, dtype=np.int64)
-        pr = self.parent_ref[sel]
-        pr2 = np.where(pr >= 0, remap[np.maximum(pr, 0)], -1)
-        return Workload(S=S2, B_s=self.B_s, frames=self.frames, V=self.V,
-                        session=(self.session[sel] - lo).astype(np.uint32),
-                        parent_ref=pr2.astype(np.int64), word=self.word[sel].copy(),
-                        new_per_session=self.new_per_session[lo:hi].copy())
+        keep = (self.session >= lo) & (self.session < hi)
+        return self._select(keep, self.frame_index(), self.frames,
+                            (self.session.astype(np.int64) - lo), hi - lo,
+                            self.new_per_session[lo:hi].copy())
+
+    def staggered(self, starts) -> "Workload":
+        """Concurrent streams that are not in step (BASELINE configs[4]): session s
+        joins at global frame starts[s] with its utterance's frame 0, so at global
+        frame t it is at utterance frame t - starts[s]; every frame of the result
+        keeps the S*B_s layout once all sessions have joined.  Same number of
+        global frames; session s keeps its first frames - starts[s] frames."""
+        starts = np.asarray(starts, dtype=np.int64)
+        assert len(starts) == self.S and np.all(starts >= 0) and np.all(starts < max(1, self.frames))
+        f = self.frame_index()
+        g = f + starts[self.session.astype(np.int64)]
+        keep = g < self.frames
+        return self._select(keep, g, self.frames, self.session, self.S, self.new_per_session.copy())
 
 
 def _zipf_cdf(V: int, s: float) -> np.ndarray:
@@ -89,34 +116,52 @@ def _zipf_cdf(V: int, s: float) -> np.ndarray:
 
 
 def generate_workload(S: int, frames: int, B_s: int, V: int, seed: int = 7,
-                      K: int = 8, dur: tuple = (10, 40), eps: float = 0.3,
+                      K: int = 8, dur: tuple = (10, 40), eps: float = 0.28,
                       window: int = 12, zipf_s: float = 1.0,
-                      qhit_target: float = 0.87, private: int = 2) -> Workload:
-    """Session s draws from its own generator seeded ``seed + s``."""
+                      qhit_target: float = 0.88, n_alt: int = 2,
+                      beam_scale: float = 1.8) -> Workload:
+    """Session s draws from its own generator seeded ``seed + s``.
+
+    Lattice-shaped beam: per session a transcript of
+    Zipf words; transcript position j has ``n_alt`` confusable alternatives
+    and a candidate set C_j of K words (the transcript word, its
+    alternatives, K-1-n_alt other Zipf words) that is the SAME for every path
+    reaching position j -- the acoustic evidence proposes the words, not the
+    LM history.  P beam paths walk the positions at their own word-boundary
+    times (``dur`` frames per word); at a boundary a path emits (history, w)
+    for every w in C_j and then takes the transcript word with probability
+    1 - eps, else one of the alternatives.  Paths therefore differ in a few
+    confusion positions and agree elsewhere: histories that differ only in
+    an older word share their recent words, which is what lossy history keys
+    merge (Table 1).  ``beam_scale`` sets P relative to the
+    number of first emissions a ``qhit_target`` query-cache hit ratio needs
+    (paths with identical histories emit identical queries, so the measured
+    ratio is higher; eps = 0.28, beam_scale = 1.8 give ~0.88 and ~15 % sign
+    redundancy at H = 256).
+    """
     assert V >= 2 and B_s >= 1 and S >= 1 and frames >= 0
+    assert K >= 1 + n_alt
     cdf = _zipf_cdf(V, zipf_s)
     mean_dur = 0.5 * (dur[0] + dur[1])
-    P = max(1, int(round(B_s * (1.0 - qhit_target) * mean_dur / K)))
+    P = max(1, int(round(beam_scale * B_s * (1.0 - qhit_target) * mean_dur / K)))
     n_frame = S * B_s
     session = np.repeat(np.arange(S, dtype=np.uint32), B_s)
     session = np.tile(session, frames)
     parent_ref = np.empty(frames * n_frame, dtype=np.int64)
     word = np.empty(frames * n_frame, dtype=np.uint32)
     new_count = np.zeros(S, dtype=np.int64)
+    L = frames // max(1, dur[0]) + 8                     # transcript positions a path can reach
 
     def zipf(rng, n):
         return (np.searchsorted(cdf, rng.random(n), side="right") + 1).astype(np.int64).clip(1, V - 1)
 
     for s in range(S):
         rng = np.random.default_rng(seed + s)
-        transcript = zipf(rng, frames // max(1, dur[0]) + 8)
-        # each path first emits `private` words of its own (hypotheses that
-        # differ in their earlier context), then follows the shared transcript
-        own = zipf(rng, P * private).reshape(P, private) if private else None
-        path_ref = np.full(P, -1, dtype=np.int64)
-        path_pos = np.full(P, -private, dtype=np.int64)
+        cands = zipf(rng, L * K).reshape(L, K)           # column 0: transcript, 1..n_alt: confusions
+        path_ref = np.full(P, -1, dtype=np.int64)        # -1 = the utterance root
+        path_pos = np.zeros(P, dtype=np.int64)
         next_b = rng.integers(0, dur[1], size=P)
-        recent = []  # list of (parent_refs, words) of first emissions, last `window` frames
+        recent = []  # (parent_refs, words) of first emissions, last `window` frames
         for t in range(frames):
             base = t * n_frame + s * B_s
             bpaths = np.nonzero(next_b == t)[0]
@@ -125,22 +170,11 @@ def generate_workload(S: int, frames: int, B_s: int, V: int, seed: int = 7,
                 next_b[bpaths[max_paths:]] = t + 1
                 bpaths = bpaths[:max_paths]
             nb = len(bpaths)
-            if nb:
-                cand = zipf(rng, nb * K).reshape(nb, K)
-                pos = path_pos[bpaths]
-                cand[:, 0] = np.where(
-                    pos < 0, own[bpaths, np.clip(pos + private, 0, private - 1)] if private else 0,
-                    transcript[np.clip(pos, 0, len(transcript) - 1)])
-                new_par = np.repeat(path_ref[bpaths], K)
-                new_w = cand.reshape(-1)
-            else:
-                new_par = np.zeros(0, dtype=np.int64)
-                new_w = np.zeros(0, dtype=np.int64)
+            new_par = np.repeat(path_ref[bpaths], K)
+            new_w = cands[np.minimum(path_pos[bpaths], L - 1)].reshape(-1)
             m = len(new_w)
-            pool_p = [r[0] for r in recent] + [new_par]
-            pool_w = [r[1] for r in recent] + [new_w]
-            pool_p = np.concatenate(pool_p)
-            pool_w = np.concatenate(pool_w)
+            pool_p = np.concatenate([r[0] for r in recent] + [new_par])
+            pool_w = np.concatenate([r[1] for r in recent] + [new_w])
             n_rep = B_s - m
             if len(pool_p) == 0:             # nothing emitted yet: root queries
                 pool_p = np.full(1, -1, dtype=np.int64)
@@ -154,9 +188,8 @@ def generate_workload(S: int, frames: int, B_s: int, V: int, seed: int = 7,
             if nb:
                 pos_of = np.empty(B_s, dtype=np.int64)
                 pos_of[perm] = np.arange(B_s)
-                choice = np.where(rng.random(nb) < eps, rng.integers(1, K, size=nb), 0)
-                chosen_new_idx = np.arange(nb) * K + choice
-                path_ref[bpaths] = base + pos_of[chosen_new_idx]
+                choice = np.where(rng.random(nb) < eps, rng.integers(1, 1 + n_alt, size=nb), 0)
+                path_ref[bpaths] = base + pos_of[np.arange(nb) * K + choice]
                 path_pos[bpaths] += 1
                 next_b[bpaths] = t + rng.integers(dur[0], dur[1] + 1, size=nb)
             new_count[s] += m
@@ -165,4 +198,3 @@ def generate_workload(S: int, frames: int, B_s: int, V: int, seed: int = 7,
                 recent.pop(0)
     return Workload(S=S, B_s=B_s, frames=frames, V=V, session=session,
                     parent_ref=parent_ref, word=word, new_per_session=new_count + 1)
-

@@ -25,14 +25,20 @@ def _dev(a, device="cuda"):
     return torch.as_tensor(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32), device=device)
 
 
-def replay_compare(eng, orc, wl, frames=None, tol_score=1e-5, tol_state=1e-5, check_codes=True):
-    F = wl.frames if frames is None else frames
+def replay_compare(eng, orc, wl, frames=None, tol_score=1e-5, tol_state=1e-5, check_codes=True,
+                   batches=None):
+    """``batches``: the calls to make, as index arrays into the workload's
+    query stream (default: one call per frame, the first ``frames`` frames);
+    e.g. one call per query or the offline level schedule
+    (8(f)-4).  Both sides get the same calls."""
+    if batches is None:
+        F = wl.frames if frames is None else frames
+        batches = [np.arange(wl.frame_slice(t).start, wl.frame_slice(t).stop) for t in range(F)]
     child_g = np.zeros(wl.n_total, np.uint32)
     child_o = np.zeros(wl.n_total, np.uint32)
-    rep = dict(max_score_err=0.0, max_state_err=0.0, frames=F, queries=0, miss=0, shit=0, qhit=0,
-               invalid=0)
-    for t in range(F):
-        sl = wl.frame_slice(t)
+    rep = dict(max_score_err=0.0, max_state_err=0.0, frames=len(batches), queries=0, miss=0, shit=0,
+               qhit=0, invalid=0)
+    for t, sl in enumerate(batches):
         pg = O.resolve_parents(wl.parent_ref[sl], child_g)
         po = O.resolve_parents(wl.parent_ref[sl], child_o)
         assert np.array_equal(pg, po), f"frame {t}: parent handles diverged"

@@ -1,0 +1,63 @@
+"""GPU parity of the lossy history-vector cache (Table 1) on every
+math path, with the hidden cache actually merging histories.
+
+The paper's contribution is that histories whose quantised vectors are equal
+share one GRU evaluation (SHIT outcome).  These tests run the replay protocol
+(tests/parity_util.py: outcomes, handles, slots, codes, stats bit-exact;
+states and scores within the path's tolerance) on lattice-shaped streams whose
+beam paths differ in an older word and then follow the same words
+(synth/workload.py), and ASSERT that many queries take the SHIT outcome, so a
+broken code, code hash or equal-code probe in the tcgen05 epilogue cannot pass.
+
+Workloads: eps (substitution rate) 0.1 / 0.08 and 2-6 frames per word, so the
+200 / 160 frames hold 40-60 words per path -- enough shared recent words for
+sign, round:1..3 keys to merge under the survey's model init at H = 256 and
+H = 1024 (sign keys of two histories agree after ~12
+shared words at H = 256 and ~16-20 at H = 1024).  The minimum SHIT counts
+are about half of what the CPU oracle produces on the same stream
+(round:3 at H = 256: 149; sign / round:1 at H = 1024: 507 / 425).
+"""
+import pytest
+
+from paper_1801_09866_b200 import KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32, MATH_TF32X3
+from synth import generate_workload
+from tests.parity_util import replay_compare
+from tests.test_gpu_parity import TOL, model, pair
+
+pytestmark = pytest.mark.gpu
+
+# oracle SHIT counts on these streams (free-running, CPU): H=256: sign 3388, round:1 2472,
+# round:2 720, round:3 149; H=1024: sign 507, round:1 425
+MIN_SHIT_256 = {(KEY_SIGN, 0): 1500, (KEY_ROUND, 1): 1000, (KEY_ROUND, 2): 300, (KEY_ROUND, 3): 50}
+MIN_SHIT_1024 = {(KEY_SIGN, 0): 200, (KEY_ROUND, 1): 150}
+
+# (math, RNNLM_TC_PAIR): bf16 CTA pair (default), bf16 one CTA per tile, TF32, 3xTF32, FP32 SIMT
+PATHS = [(MATH_BF16, "1"), (MATH_BF16, "0"), (MATH_TF32, "0"), (MATH_TF32X3, "0"), (MATH_FP32, "0")]
+
+
+def _wl256(V):
+    return generate_workload(1, 200, 256, V, seed=7, dur=(2, 6), eps=0.1)
+
+
+@pytest.mark.parametrize("mode,k", list(MIN_SHIT_256))
+@pytest.mark.parametrize("math,pk", PATHS)
+def test_lossy_merges_h256(math, pk, mode, k, monkeypatch):
+    """H = E = 256 (BASELINE configs[1] model): sign and round:1/2/3 keys."""
+    monkeypatch.setenv("RNNLM_TC_PAIR", pk)
+    d, m = model("moderate")
+    wl = _wl256(d.V)
+    eng, orc = pair(d, m, wl, mode, k=k, math=math)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
+    assert rep["shit"] >= MIN_SHIT_256[(mode, k)], rep
+
+
+@pytest.mark.parametrize("mode,k", list(MIN_SHIT_1024))
+@pytest.mark.parametrize("math,pk", [p for p in PATHS if p[0] != MATH_FP32])
+def test_lossy_merges_h1024(math, pk, mode, k, monkeypatch):
+    """H = E = 1024 (BASELINE configs[2-4] model, V = 200k, 2^27 4-gram)."""
+    monkeypatch.setenv("RNNLM_TC_PAIR", pk)
+    d, m = model("large")
+    wl = generate_workload(1, 160, 128, d.V, seed=7, dur=(2, 5), eps=0.08)
+    eng, orc = pair(d, m, wl, mode, k=k, math=math)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
+    assert rep["shit"] >= MIN_SHIT_1024[(mode, k)], rep

@@ -1,0 +1,103 @@
+"""GPU vs ORACLE under the two alternative call schedules of SURVEY 8(f):
+
+* (f1) one call per query -- the paper's per-query transfer mode (P:181-184,
+  Table 2): the same queries, each its own rnnlm_query_batch call;
+* (f4) offline level batching (paper_1801_09866_b200.offline): the
+  whole stream grouped by dependency level, several frames per call.
+
+Both sides make the same calls (tests/parity_util.replay_compare with
+``batches``), so every decision -- including which query is a lossy key's
+first occupant, which depends on the schedule -- must be bit-identical to the
+oracle, at every key mode; states / scores within the path's tolerance.
+"""
+import numpy as np
+import pytest
+
+from paper_1801_09866_b200 import KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32
+from paper_1801_09866_b200.offline import level_schedule
+from synth import generate_workload
+from tests.parity_util import replay_compare
+from tests.test_gpu_parity import TOL, forgetful_model, model, pair
+
+pytestmark = pytest.mark.gpu
+
+MODES = [(KEY_OFF, 0), (KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 2), (KEY_ROUND, 3)]
+
+
+@pytest.mark.parametrize("mode,k", MODES)
+@pytest.mark.parametrize("math", [MATH_FP32, MATH_BF16])
+def test_per_query_calls_vs_oracle(math, mode, k):
+    """(f1): one call per query; the forgetful model makes lossy keys merge."""
+    if math == MATH_FP32:
+        d, m = forgetful_model()
+    else:                                     # tensor-core tiles need E % 64, H % 128
+        d, m = model("moderate")
+    wl = generate_workload(2, 20, 32, d.V, seed=31, dur=(2, 6), eps=0.3, beam_scale=4)
+    eng, orc = pair(d, m, wl, mode, k=k, math=math, B=64)
+    batches = [np.array([i]) for i in range(wl.n_total)]
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math], batches=batches)
+    assert rep["frames"] == wl.n_total and rep["miss"] > 100
+    if math == MATH_FP32 and mode != KEY_OFF and k < 3:   # oracle: sign 97, round:1 43, round:2 26
+        assert rep["shit"] > 15, rep
+
+
+@pytest.mark.parametrize("mode,k", MODES)
+@pytest.mark.parametrize("math", [MATH_FP32, MATH_BF16, MATH_TF32])
+def test_offline_level_batches_vs_oracle(math, mode, k):
+    """(f4): level-batched calls (several frames' queries per call, sessions
+    mixed), lossy keys merging (H = 256 model, lattice stream)."""
+    d, m = model("moderate")
+    wl = generate_workload(2, 120, 128, d.V, seed=13, dur=(2, 6), eps=0.1)
+    batches = level_schedule(wl.session, wl.parent_ref, wl.frame_ptr, max_batch=2048)
+    assert len(batches) < wl.frames
+    eng, orc = pair(d, m, wl, mode, k=k, math=math, B=2048)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math], batches=batches)
+    assert rep["miss"] > 500
+    if (mode, k) in ((KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 2)):   # oracle: 1250, 772, 221
+        assert rep["shit"] > 100, rep
+
+
+@pytest.mark.parametrize("math", [MATH_FP32, MATH_BF16])
+def test_graph_replay_equals_direct_calls(math):
+    """rnnlm_graph_create / rnnlm_graph_launch: one captured call replayed per
+    frame on fixed buffers, with the frame's query count read on the device
+    (staggered sessions make the frame sizes vary), returns bitwise what
+    rnnlm_query_batch returns; stats equal."""
+    import torch
+    import oracle as O
+    from tests.parity_util import _dev
+    d, m = model("moderate")
+    wl = generate_workload(3, 60, 64, d.V, seed=11, dur=(2, 6), eps=0.1).staggered([0, 7, 19])
+    B = wl.n_per_frame
+    outs = []
+    for use_graph in (False, True):
+        eng, _ = pair(d, m, wl, KEY_SIGN, math=math, B=B)
+        child = np.zeros(wl.n_total, np.uint32)
+        score = np.zeros(wl.n_total, np.float32)
+        outc = np.zeros(wl.n_total, np.uint8)
+        if use_graph:
+            bs, bp, bw = (torch.zeros(B, dtype=torch.int32, device="cuda") for _ in range(3))
+            sc = torch.zeros(B, dtype=torch.float32, device="cuda")
+            ch = torch.zeros(B, dtype=torch.int32, device="cuda")
+            oc = torch.zeros(B, dtype=torch.uint8, device="cuda")
+            nn = torch.zeros(1, dtype=torch.int32, device="cuda")
+            g = eng.graph(B, bs, bp, bw, sc, ch, oc, n=nn)
+        for t in range(wl.frames):
+            sl = wl.frame_slice(t)
+            k = sl.stop - sl.start
+            par = O.resolve_parents(wl.parent_ref[sl], child)
+            if use_graph:
+                bs[:k] = _dev(wl.session[sl]); bp[:k] = _dev(par); bw[:k] = _dev(wl.word[sl])
+                nn.fill_(k)
+                g.launch()
+                s_, c_, o_ = sc[:k], ch[:k], oc[:k]
+            else:
+                s_, c_, o_ = eng.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]))
+            score[sl] = s_.cpu().numpy()
+            child[sl] = c_.cpu().numpy().view(np.uint32)
+            outc[sl] = o_.cpu().numpy()
+        outs.append((score, child, outc, eng.cache_stats()))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+    assert outs[0][3] == outs[1][3]
+    assert outs[0][3]["hidden_hits"] > 0

@@ -15,12 +15,12 @@ def _wl():
 
 def test_schedule_invariants():
     wl = _wl()
-    lv = levels(wl.parent_ref, wl.n_per_frame)
+    lv = levels(wl.parent_ref, wl.frame_ptr)
     ref = wl.parent_ref
     has = ref >= 0
     assert np.all(lv[~has] == 0)
     assert np.all(lv[has] == lv[ref[has]] + 1)
-    batches = level_schedule(wl.session, wl.parent_ref, wl.n_per_frame, max_batch=40)
+    batches = level_schedule(wl.session, wl.parent_ref, wl.frame_ptr, max_batch=40)
     seen = np.full(wl.n_total, -1)
     for b, ix in enumerate(batches):
         assert len(ix) <= 40
@@ -34,7 +34,7 @@ def test_schedule_invariants():
     assert np.all(seen[ref[p]] < seen[p])                                   # parents in earlier calls
     # one level per word boundary of the deepest path: fewer levels than frames
     assert lv.max() + 1 < wl.frames
-    assert len(level_schedule(wl.session, wl.parent_ref, wl.n_per_frame, 1 << 30)) == lv.max() + 1
+    assert len(level_schedule(wl.session, wl.parent_ref, wl.frame_ptr, 1 << 30)) == lv.max() + 1
 
 
 def test_oracle_offline_equals_online_lossless():
@@ -57,7 +57,7 @@ def test_oracle_offline_equals_online_lossless():
     off = O.Oracle(cfg, m)
     child_off = np.zeros(wl.n_total, np.uint32)
     score_off = np.zeros(wl.n_total, np.float32)
-    for ix in level_schedule(wl.session, wl.parent_ref, wl.n_per_frame, max_batch=50):
+    for ix in level_schedule(wl.session, wl.parent_ref, wl.frame_ptr, max_batch=50):
         par = O.resolve_parents(wl.parent_ref[ix], child_off)
         sc, ch, _ = off.query_frame(wl.session[ix], par, wl.word[ix])
         score_off[ix], child_off[ix] = sc, ch
