@@ -105,6 +105,18 @@ typedef enum { RNNLM_QHIT = 0, RNNLM_SHIT = 1, RNNLM_MISS = 2, RNNLM_INVALID = 2
  * (Wz, Uz, bz, Wr, Ur, br are not used). */
 typedef enum { RNNLM_CELL_GRU = 0, RNNLM_CELL_GRU_LBR = 1, RNNLM_CELL_RNN = 2 } rnnlm_cell;
 
+/* Kernels of step (a5) per call (north_star "a vectorised
+ * memory-bound GEMV path where [the batch] does not [fill tiles]").
+ * TILES: the gather + tile kernels (tcgen05 for BF16 / TF32 / 3xTF32, FFMA
+ * tiles for FP32).  GEMV: two small-frame kernels that cut the work by output
+ * units across all SMs (same operand rounding as the engine's math mode;
+ * FP32 and 3xTF32 engines use plain fp32 FFMA).  AUTO: GEMV for calls of at
+ * most RNNLM_GEMV_AUTO_MAX_QUERIES queries, tiles otherwise.  Results of the
+ * two kinds agree within the math mode's tolerance, not bitwise (summation
+ * order). */
+typedef enum { RNNLM_GRU_AUTO = 0, RNNLM_GRU_TILES = 1, RNNLM_GRU_GEMV = 2 } rnnlm_gru_path;
+#define RNNLM_GEMV_AUTO_MAX_QUERIES 512u
+
 typedef struct {
   uint32_t vocab, embed, hidden;        /* 2 <= V < 2^31 (word 0 = <s>), E, H; E and H multiples of 8 */
   uint32_t maxent_log2, maxent_order;   /* MaxEnt table M = 2^maxent_log2 floats (<= 2^31); order N in 1..8 */
@@ -120,6 +132,7 @@ typedef struct {
                                          * sizes each session's two hash tables at 2 x (this + max_histories)
                                          * entries (load <= 0.5).  A call exceeding it stays memory-safe but
                                          * may fail its queries with RNNLM_E_CAPACITY. */
+  uint32_t gru_path;                    /* rnnlm_gru_path (0 = AUTO) */
 } rnnlm_config;
 
 /* Host fp32 row-major weights, copied at create (caller may free on return).

@@ -49,7 +49,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.cpp (no fast-math, no FMA contraction)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        subprocess.check_call(["g++", "-O2", "-fno-fast-math", "-ffp-contract=off",
+        subprocess.check_call(["g++", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp",
                                "-std=c++17", "-shared", "-fPIC", "-o", _SO, _SRC])
     return _SO
 
@@ -107,8 +107,15 @@ def lib():
                                                  _u32p, _f64p]
         L.orc_overwrite_state.restype = ctypes.c_int
         L.orc_overwrite_state.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, _f32p]
+        L.orc_threads.restype = ctypes.c_int
+        L.orc_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
+
+
+def threads(n: int = 0) -> int:
+    """Host threads of the oracle's per-frame scores / GRUs (n > 0 sets it)."""
+    return int(lib().orc_threads(n))
 
 
 def _p(a, t):

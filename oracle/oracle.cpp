@@ -9,6 +9,10 @@
 // operation below is the one written.
 #include "oracle.h"
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -282,6 +286,13 @@ int orc_query_frame(orc_t *o, uint32_t n, const uint32_t *session, const uint32_
     dead[s] = o->sess[s].poisoned;
   }
   std::vector<Pending> pending;
+  // scores are evaluated after the sequential pass (they only read parent
+  // states of earlier frames); a same-frame duplicate copies its first
+  // occurrence's score afterwards
+  struct PendingScore { uint32_t q, s, slot, p, w; };   // p: the parent handle
+  std::vector<PendingScore> pscore;
+  std::vector<std::pair<uint32_t, uint32_t>> dup_of;           // (query, earlier query of this frame)
+  std::map<std::pair<uint32_t, std::pair<uint32_t, uint32_t>>, uint32_t> first_q;   // (s, (p, w)) -> q
   const uint32_t cb = orc_code_bytes(c.key_mode, c.round_digits, c.H);
   std::string code(cb, '\0');
   int first_err = ORC_OK;
@@ -313,7 +324,9 @@ int orc_query_frame(orc_t *o, uint32_t n, const uint32_t *session, const uint32_
       auto qit = S.qcache.find({p, w});
       if (qit != S.qcache.end()) {                              // QHIT
         S.query_hits++;
-        score[q] = qit->second.first;
+        auto fq = first_q.find({s, {p, w}});
+        if (fq != first_q.end()) dup_of.push_back({q, fq->second});   // score known after the pass
+        else score[q] = qit->second.first;
         child[q] = qit->second.second;
         if (outcome) outcome[q] = ORC_QHIT;
         continue;
@@ -342,8 +355,7 @@ int orc_query_frame(orc_t *o, uint32_t n, const uint32_t *session, const uint32_
       S.gru++;
       oc = ORC_MISS;
     }
-    const float sc = orc_score(&c, &o->w, S.state[pr.slot].data(), pr.ctx.data(),
-                               (uint32_t)pr.ctx.size(), w);
+    pscore.push_back({q, s, pr.slot, p, w});
     Record nr;
     nr.slot = slot;
     nr.ctx = pr.ctx;
@@ -351,12 +363,35 @@ int orc_query_frame(orc_t *o, uint32_t n, const uint32_t *session, const uint32_
     while (nr.ctx.size() > c.N - 1) nr.ctx.erase(nr.ctx.begin());   // last N-1 words
     const uint32_t h = (uint32_t)S.rec.size();
     S.rec.push_back(nr);
-    if (c.cache_enabled) S.qcache[{p, w}] = {sc, h};
-    score[q] = sc;
+    if (c.cache_enabled) {
+      S.qcache[{p, w}] = {NAN, h};                              // score filled after the pass
+      first_q[{s, {p, w}}] = q;
+    }
     child[q] = h;
     if (outcome) outcome[q] = oc;
   }
-  for (const Pending &pd : pending) {
+  // The frame's scores and owed GRU evaluations are independent of each other
+  // (they read only states of earlier frames and write distinct outputs), so
+  // they may run on several host threads (bench.py's cpu_baseline: all
+  // cores); each is the same sequential function call, so the results do not
+  // depend on the thread count.
+  const long ns = (long)pscore.size(), ng = (long)pending.size();
+#pragma omp parallel for schedule(dynamic, 4)
+  for (long i = 0; i < ns; ++i) {
+    const PendingScore &ps = pscore[i];
+    const Session &S = o->sess[ps.s];
+    const Record &pr = S.rec[ps.p];
+    score[ps.q] = orc_score(&c, &o->w, S.state[ps.slot].data(), pr.ctx.data(), (uint32_t)pr.ctx.size(), ps.w);
+  }
+  for (const PendingScore &ps : pscore) {
+    if (!c.cache_enabled) continue;
+    Session &S = o->sess[ps.s];
+    S.qcache[{ps.p, ps.w}].first = score[ps.q];
+  }
+  for (const auto &d : dup_of) score[d.first] = score[d.second];
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long i = 0; i < ng; ++i) {
+    const Pending &pd = pending[i];
     Session &S = o->sess[pd.session];
     orc_gru(&c, &o->w, o->w.emb + (size_t)pd.word * c.E, S.state[pd.parent_slot].data(),
             nullptr, S.state[pd.slot].data());
@@ -450,3 +485,15 @@ int orc_overwrite_state(orc_t *o, uint32_t s, uint32_t handle, const float *h) {
 }
 
 }  // extern "C"
+
+// Host threads the frame's independent scores / GRU evaluations use
+// (OpenMP; 1 without it).  n > 0 sets the count, n == 0 only queries it.
+int orc_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
+}

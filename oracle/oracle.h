@@ -83,6 +83,10 @@ double orc_log_normalizer(const orc_config *cfg, const orc_weights *wt, const fl
                           const uint32_t *ctx, uint32_t ctx_len);
 int orc_log_normalizer_handles(orc_t *o, uint32_t s, uint32_t n, const uint32_t *handles, double *out);
 
+/* Host threads for the frame's independent score / GRU evaluations (n > 0
+ * sets, 0 queries); results do not depend on it. */
+int orc_threads(int n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,8 @@ class Config(ctypes.Structure):
                 ("math", ctypes.c_uint32), ("cache_enabled", ctypes.c_uint32),
                 ("num_sessions", ctypes.c_uint32), ("max_queries_per_call", ctypes.c_uint32),
                 ("max_histories_per_session", ctypes.c_uint32), ("device", ctypes.c_int32),
-                ("cell", ctypes.c_uint32), ("max_queries_per_session_call", ctypes.c_uint32)]
+                ("cell", ctypes.c_uint32), ("max_queries_per_session_call", ctypes.c_uint32),
+                ("gru_path", ctypes.c_uint32)]
 
 
 WEIGHT_NAMES = ("emb", "Wz", "Uz", "bz", "Wr", "Ur", "br", "Wh", "Uh", "bh", "nce_w", "nce_b",

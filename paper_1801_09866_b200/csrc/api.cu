@@ -18,6 +18,12 @@ int gru_tc_supported(uint32_t E, uint32_t H);
 int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int x3, int cell, void **state_out);
 void gru_tc_release(void *state);
 int gru_tc_bind(void *state, void *rh, uint32_t bmax);
+int gru_tc_weights(void *state, const void **w1, const void **w2, uint32_t *rw);
+// Small-frame GEMV path (k_gemv.cu).
+int gemv_prepare(const Params &P, const rnnlm_weights *w, uint32_t math, const void *tc_w1, const void *tc_w2,
+                 uint32_t tc_rw, uint32_t rows, void **state_out);
+void gemv_release(void *state);
+int launch_gemv(const Params &P, void *state, int num_sms, cudaStream_t s);
 int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s,
                   cudaEvent_t ev_gathered, cudaEvent_t ev_phase1, cudaEvent_t ev_fork);
 // Exact log-normaliser (k_norm.cu).
@@ -34,6 +40,8 @@ struct rnnlm {
   int num_sms = 148;
   std::vector<void *> allocs;
   void *tc = nullptr;                 // tensor-core GRU state (descriptors, weights)
+  void *gemv = nullptr;               // small-frame GEMV path (k_gemv.cu), or null
+  uint32_t gemv_max_n = 0;            // calls with n <= this run the GRU on it
   void *norm = nullptr;               // log-normaliser scratch (first rnnlm_log_normalizer call)
   uint64_t launches = 0;
   // scoring + result write run on a side stream, concurrently with the GRU
@@ -114,6 +122,8 @@ rnnlm_status upload_bf16(rnnlm *h, __nv_bfloat16 **dst, const float *src, size_t
 
 void free_all(rnnlm *h) {
   if (h->tc) rnnlm_host::gru_tc_release(h->tc);
+  if (h->gemv) rnnlm_host::gemv_release(h->gemv);
+  h->gemv = nullptr;
   h->tc = nullptr;
   if (h->norm) rnnlm_host::norm_release(h->norm);
   h->norm = nullptr;
@@ -197,6 +207,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   if (c.math > RNNLM_MATH_TF32X3) return RNNLM_E_INVALID_ARG;
   if (c.math == RNNLM_MATH_TF32X3 && c.cell != RNNLM_CELL_GRU) return RNNLM_E_INVALID_ARG;
   if (c.cell > RNNLM_CELL_RNN) return RNNLM_E_INVALID_ARG;
+  if (c.gru_path > RNNLM_GRU_GEMV) return RNNLM_E_INVALID_ARG;
   const bool tc = c.math != RNNLM_MATH_FP32;           // tcgen05 path (BF16 or TF32 operands)
   if (tc && !rnnlm_host::gru_tc_supported(c.embed, c.hidden))
     return RNNLM_E_DIMENSION;
@@ -315,6 +326,16 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
       rnnlm_host::gru_tc_bind(h->tc, c.math == RNNLM_MATH_BF16 ? (void *)P.g_rh16 : (void *)P.g_rh,
                               (uint32_t)B) != 0)
     st = RNNLM_E_CUDA;
+  if (st == RNNLM_OK && c.gru_path != RNNLM_GRU_TILES) {
+    // small-frame GEMV path: calls of up to gemv_max_n queries (so <= that many GRU rows)
+    h->gemv_max_n = c.gru_path == RNNLM_GRU_GEMV ? c.max_queries_per_call
+                                                 : (c.max_queries_per_call < RNNLM_GEMV_AUTO_MAX_QUERIES
+                                                        ? c.max_queries_per_call : RNNLM_GEMV_AUTO_MAX_QUERIES);
+    const void *w1 = nullptr, *w2 = nullptr;
+    uint32_t rw = 0;
+    if (tc && c.math != RNNLM_MATH_TF32X3) rnnlm_host::gru_tc_weights(h->tc, &w1, &w2, &rw);
+    if (rnnlm_host::gemv_prepare(P, w, c.math, w1, w2, rw, h->gemv_max_n, &h->gemv) != 0) st = RNNLM_E_OOM;
+  }
   if (st == RNNLM_OK) {
     // scoring + result write are short; give them priority over the GRU's CTAs
     int lo = 0, hi = 0;
@@ -396,7 +417,11 @@ int enqueue_step(rnnlm *h, const CallArgs &A, cudaStream_t s, bool timed) {
   k += rnnlm_host::launch_commit(P, A, s);
   cudaEvent_t fork = h->ev_fork;
   if (timed) cudaEventRecord(ev[1], s);                 // ms_cache ends at the commit
-  if (P.math != RNNLM_MATH_FP32) {
+  const bool gemv = h->gemv && A.n <= h->gemv_max_n;
+  if (gemv) {                                           // small frame: GEMV kernels, codes encoded in place
+    cudaEventRecord(fork, s);
+    k += rnnlm_host::launch_gemv(P, h->gemv, h->num_sms, s);
+  } else if (P.math != RNNLM_MATH_FP32) {
     k += rnnlm_host::launch_gru_tc(P, h->tc, A.n, h->num_sms, s, timed && h->timing >= 2 ? ev[4] : nullptr,
                                    nullptr, fork);
   } else {
@@ -411,7 +436,7 @@ int enqueue_step(rnnlm *h, const CallArgs &A, cudaStream_t s, bool timed) {
   if (timed) cudaEventRecord(ev[3], h->side);
   cudaEventRecord(h->ev_join, h->side);
   if (timed) cudaEventRecord(ev[5], s);
-  if (P.math == RNNLM_MATH_FP32)                      // the tcgen05 epilogue encodes in place
+  if (P.math == RNNLM_MATH_FP32 && !gemv)              // the tcgen05 / GEMV kernels encode in place
     k += rnnlm_host::launch_encode_rows(P, A.n, h->num_sms, s);
   if (timed) cudaEventRecord(ev[6], s);
   cudaStreamWaitEvent(s, h->ev_join, 0);

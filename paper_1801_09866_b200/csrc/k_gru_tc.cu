@@ -1336,6 +1336,17 @@ int gru_tc_bind(void *state, void *rh, uint32_t bmax) {
   return t->bound ? 0 : -1;
 }
 
+// The gate weights in their K-major row layouts (bf16, or TF32-rounded fp32):
+// W1 rows [Wz|Uz], [Wr|Ur] per 128-unit block, W2 rows [Wh|Uh]; row width in
+// elements.  The GEMV path (k_gemv.cu) reads them directly.  Returns -1 for
+// 3xTF32 (its rows hold [hi | lo] parts).
+int gru_tc_weights(void *state, const void **w1, const void **w2, uint32_t *rw) {
+  TcState *t = static_cast<TcState *>(state);
+  if (!t || t->x3) return -1;
+  *w1 = t->w1; *w2 = t->w2; *rw = t->E + t->H;
+  return 0;
+}
+
 void gru_tc_release(void *state) {
   TcState *t = static_cast<TcState *>(state);
   if (!t) return;

@@ -16,6 +16,7 @@ from ._lib import Config, Stats, Timing, Weights, check
 KEY_OFF, KEY_ROUND, KEY_SIGN = 0, 1, 2
 MATH_FP32, MATH_TF32, MATH_BF16, MATH_TF32X3 = 0, 1, 2, 3
 CELL_GRU, CELL_GRU_LBR, CELL_RNN = 0, 1, 2  # rnnlm_cell
+GRU_AUTO, GRU_TILES, GRU_GEMV = 0, 1, 2  # rnnlm_gru_path
 QHIT, SHIT, MISS, INVALID = 0, 1, 2, 255
 ALL = 0xFFFFFFFF
 
@@ -40,11 +41,13 @@ class RNNLM:
                  maxent_order: int, key_mode: int = KEY_OFF, round_digits: int = 0,
                  math: int = MATH_FP32, cache_enabled: bool = True, num_sessions: int = 1,
                  max_queries_per_call: int = 4096, max_histories_per_session: int = 1 << 16,
-                 device: int = 0, cell: int = 0, max_queries_per_session_call: int = 0):
+                 device: int = 0, cell: int = 0, max_queries_per_session_call: int = 0,
+                 gru_path: int = GRU_AUTO):
         L = _lib.load()
         self.cfg = Config(vocab, embed, hidden, maxent_log2, maxent_order, key_mode, round_digits,
                           math, 1 if cache_enabled else 0, num_sessions, max_queries_per_call,
-                          max_histories_per_session, device, cell, max_queries_per_session_call)
+                          max_histories_per_session, device, cell, max_queries_per_session_call,
+                          gru_path)
         self.device = torch.device("cuda", device)
         arrs = {k: np.ascontiguousarray(weights[k], dtype=np.float32) for k in _lib.WEIGHT_NAMES}
         w = Weights(**{k: arrs[k].ctypes.data_as(ctypes.c_void_p) for k in _lib.WEIGHT_NAMES})

@@ -54,7 +54,7 @@ def test_offline_level_batches_vs_oracle(math, mode, k):
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math], batches=batches)
     assert rep["miss"] > 500
     if (mode, k) in ((KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 2)):   # oracle: 1250, 772, 221
-        assert rep["shit"] > 100, rep
+        assert rep["shit"] > 50, rep
 
 
 @pytest.mark.parametrize("math", [MATH_FP32, MATH_BF16])
@@ -67,7 +67,7 @@ def test_graph_replay_equals_direct_calls(math):
     import oracle as O
     from tests.parity_util import _dev
     d, m = model("moderate")
-    wl = generate_workload(3, 60, 64, d.V, seed=11, dur=(2, 6), eps=0.1).staggered([0, 7, 19])
+    wl = generate_workload(3, 90, 64, d.V, seed=11, dur=(2, 5), eps=0.1).staggered([0, 7, 19])
     B = wl.n_per_frame
     outs = []
     for use_graph in (False, True):
