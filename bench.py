@@ -1,25 +1,34 @@
 #!/usr/bin/env python
 """Benchmark of the frame-batched GRU-RNNLM query step (BASELINE.json metric).
 
-    python bench.py --gpus N --steps K --warmup W [--workload multi] [--math bf16]
+    python bench.py --gpus N --steps K --warmup W
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
     python bench.py --impl reference ...        (the CPU oracle arm)
 
-A step = one decoder frame of every session this rank owns: one
+A step = one decoder frame of every utterance stream this rank owns: one
 rnnlm_query_batch call that runs the whole hot path (keys, both caches,
 compaction, gather + GRU, NCE + MaxEnt scoring, result write) over that
-frame's queries.  Workload: BASELINE.json configs[4] ("multi": 64 utterance
+frame's queries, plus (N > 1) the NCCL all-gather of the per-query
+(score, child) results.
+
+Headline workload: BASELINE.json configs[4] ("multi": 64 concurrent utterance
 streams x 2,048 queries/frame on the large model, V=200k, H=E=1024, 2^27
-4-gram MaxEnt) per GPU (weak scaling: sessions are independent units,
-DESIGN.md "Multi-GPU"); synthetic, seeded (synth/).  The per-query results
-(score, child) of every step are all-gathered over NCCL on a side stream when
-N > 1.
+4-gram MaxEnt, sign keys), the 64 streams SHARDED over the N GPUs (strong
+scaling, "evenly distributing the block").  The streams are not in
+step: stream s joins at frame s * (T0 / 64) of a 400-frame (4-s) run,
+so the timed frames see the streams at every point of their utterances.
+Synthetic and seeded (synth/).  The headline arithmetic is the paper's
+single precision: the fp32-accurate 3xTF32 tensor-core mode, held to
+the FP32 path's 1e-5 in tests; the bf16 tensor-core numbers of the same
+frames are the "bf16" key.  "configs" carries BASELINE configs[0]-[3]
+(tiny, moderate, large, compression sweep), one GPU, measured in the same run.
 
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -35,6 +44,9 @@ from synth import CONFIGS, generate_model, generate_workload, model_dims  # noqa
 
 METRIC = "RNNLM queries/sec (frame-batched, cache on)"
 UNIT = "queries/s"
+UTT_FRAMES = 400            # a 4-s utterance at 10 ms frames
+TOTAL_STREAMS = 64          # BASELINE configs[4]
+MATHS = ("bf16", "tf32", "fp32", "tf32x3")
 
 
 def parse():
@@ -44,21 +56,24 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="multi", choices=list(CONFIGS))
-    ap.add_argument("--sessions", type=int, default=None, help="sessions per rank (default: config)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--math", default="bf16", choices=["bf16", "tf32", "fp32", "tf32x3"])
+    ap.add_argument("--sessions", type=int, default=None, help="streams in the job (default: config)")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong: the job's streams are split over the ranks (BASELINE configs[4]); "
+                         "weak: every rank runs that many streams")
+    ap.add_argument("--math", default="tf32x3", choices=MATHS, help="headline arithmetic")
+    ap.add_argument("--also", default="bf16", help="extra math modes measured on the same frames (comma list, or none)")
     ap.add_argument("--key", default="sign", help="off | sign | round:K")
     ap.add_argument("--cell", default="gru", choices=["gru", "lbr", "rnn"],
                     help="recurrent cell (SURVEY 8(f)-3): gru = Chung GRU (the paper's), lbr = linear before "
                          "reset, rnn = the paper's comparison vanilla RNN (Elman, logistic)")
     ap.add_argument("--no-cache", action="store_true")
+    ap.add_argument("--no-stagger", action="store_true", help="all streams start together (frame 0)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs[0]-[3] block")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--prefill", type=int, default=40,
-                    help="untimed frames run before warm-up so timed frames are mid-utterance")
     ap.add_argument("--uniform-words", action="store_true", help="(ncu evidence) no Zipf reuse")
-    ap.add_argument("--timing-level", type=int, default=1, help="1: kernel groups, 2: + GRU kernels")
+    ap.add_argument("--timing-level", type=int, default=2, help="1: kernel groups, 2: + GRU kernels")
     ap.add_argument("--normalizer", action="store_true",
                     help="SURVEY 8(f)-2 workload: exact log-normalisers/s instead of the query step")
     ap.add_argument("--histories", type=int, default=2048, help="(--normalizer) histories per call")
@@ -78,17 +93,18 @@ def dist_env():
     return rank, world, local
 
 
-def sessions_for(args, world):
-    S = args.sessions or CONFIGS[args.workload]["S"]
-    if args.scaling == "strong":
-        assert S % world == 0, "strong scaling needs sessions divisible by world size"
-        return S // world
-    return S
-
-
 def key_mode(name):
     from paper_1801_09866_b200 import KEY_MODES
     return KEY_MODES[name]
+
+
+def math_id(name):
+    import paper_1801_09866_b200 as R
+    return {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[name]
+
+
+def dtype_of(name):
+    return {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "tf32x3": "f32 (3xTF32)"}[name]
 
 
 def host_cores():
@@ -108,31 +124,60 @@ def cpu_model():
     return "unknown"
 
 
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- workloads
+def stream_starts(total_streams: int, lead: int) -> np.ndarray:
+    """Join frame of every stream: evenly spread over [0, lead] so that, once
+    all have joined, the streams are at every point of their utterances."""
+    return (np.arange(total_streams, dtype=np.int64) * lead) // max(1, total_streams - 1)
+
+
+def multi_workload(args, lo: int, hi: int, frames: int, stagger: bool, uniform: bool):
+    """Streams [lo, hi) of the job (stream s draws from seed 7 + s)."""
+    c = CONFIGS[args.workload]
+    V = model_dims(args.workload).V
+    wl = generate_workload(hi - lo, frames, c["B_s"], V, seed=7 + lo, zipf_s=0.0 if uniform else 1.0)
+    if stagger:
+        tail = args.warmup + 2 * args.steps
+        starts = stream_starts(args.total_streams, max(0, frames - tail - 1))[lo:hi]
+        wl = wl.staggered(starts)
+    return wl
+
+
 # ----------------------------------------------------------------------------- oracle timing
-def time_oracle(dims, model, wl, mode, k, cache, budget_s, max_steps=None, cell=0):
-    """The CPU oracle as it stands (single thread), on a bounded prefix of the
-    workload's first session.  Returns (queries, seconds, frames)."""
+def time_oracle(dims, model, wl, mode, k, cache, budget_s, max_steps=None, cell=0, threads=None):
+    """The CPU oracle as it stands (scores / GRUs of a frame on `threads` host
+    threads, decisions sequential), on a bounded prefix of the workload's
+    first stream.  Returns (queries, seconds, frames, per-frame seconds, threads)."""
     import oracle as O
+    th = O.threads(threads or host_cores())
     one = wl.select_sessions(0, 1)
     cfg = O.make_config(dims.V, dims.E, dims.H, dims.maxent_log2, dims.N, mode, k,
                         1 if cache else 0, 1,
-                        one.max_histories_hint() if cache else one.frames * one.B_s + 2, cell=cell)
+                        one.max_histories_hint() if cache else one.n_total + 2, cell=cell)
     orc = O.Oracle(cfg, model)
     child = np.zeros(one.n_total, np.uint32)
     done_q, t_total, f = 0, 0.0, 0
     per_step = []
     while f < one.frames and t_total < budget_s and (max_steps is None or f < max_steps):
         sl = one.frame_slice(f)
-        par = O.resolve_parents(one.parent_ref[sl], child)
-        t0 = time.perf_counter()
-        _, ch, _ = orc.query_frame(one.session[sl], par, one.word[sl])
-        dt = time.perf_counter() - t0
-        child[sl] = ch
-        done_q += len(par)
-        t_total += dt
-        per_step.append(dt)
+        if sl.stop > sl.start:
+            par = O.resolve_parents(one.parent_ref[sl], child)
+            t0 = time.perf_counter()
+            _, ch, _ = orc.query_frame(one.session[sl], par, one.word[sl])
+            dt = time.perf_counter() - t0
+            child[sl] = ch
+            done_q += len(par)
+            t_total += dt
+            per_step.append((dt, len(par)))
         f += 1
-    return done_q, t_total, f, per_step
+    return done_q, t_total, f, per_step, th
 
 
 def run_reference(args):
@@ -145,23 +190,24 @@ def run_reference(args):
     mode, k = key_mode(args.key)
     steps = args.warmup + args.steps
     wl = generate_workload(1, steps, c["B_s"], dims.V, seed=7)
-    # each step = one frame of one utterance stream (bounded sample of the workload)
-    q, secs, frames, per = time_oracle(dims, model, wl, mode, k, not args.no_cache, 1e30,
-                                       max_steps=steps, cell={"gru": 0, "lbr": 1, "rnn": 2}[args.cell])
+    # each step = one frame of one utterance stream (a bounded sample of the workload)
+    q, secs, frames, per, th = time_oracle(dims, model, wl, mode, k, not args.no_cache, 1e30, max_steps=steps,
+                                           cell={"gru": 0, "lbr": 1, "rnn": 2}[args.cell])
     timed = per[args.warmup:]
-    tq = c["B_s"] * len(timed)
-    value = tq / sum(timed)
+    tq = sum(n for _, n in timed)
+    ts = sum(dt for dt, _ in timed)
+    value = tq / ts
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(timed) / len(timed), "higher_is_better": True,
+        "ms_per_step": 1e3 * ts / len(timed), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "key": args.key,
-                   "sample": f"1 session x {c['B_s']} queries per step (frames {args.warmup}.."
+                   "sample": f"1 stream x {c['B_s']} queries per step (frames {args.warmup}.."
                              f"{steps - 1} of utterance 0)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{len(timed)} frames x {c['B_s']} queries, session 0",
-                         "cpu": cpu_model()},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "oracle",
+                         "sample": f"{len(timed)} frames x {c['B_s']} queries, stream 0",
+                         "cpu": cpu_model(), "host_cores": host_cores()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -210,13 +256,241 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ----------------------------------------------------------------------------- ours
+def burst_clocks(clk) -> bool:
+    """The timed region ran at (near) the maximum SM clock with no power cap:
+    the burst peaks apply (the measured sustained peaks are for seconds-long
+    power-capped runs)."""
+    if not clk.get("sm_mhz") or not clk.get("sm_max_mhz"):
+        return False
+    return clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"] and "sw_power_cap" not in clk.get("reasons", [])
+
+
+def measure_tf32_peak(dev):
+    """cuBLAS TF32 dense throughput on this GPU (fp32 8192^3 matmul with TF32
+    allowed, 2N^3 flop): best of 10 short runs (burst) -- MEASURED_PEAKS.json
+    holds no TF32 figure."""
+    import torch
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        for _ in range(3):
+            torch.matmul(a, b)
+        torch.cuda.synchronize()
+        best = 1e30
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+
+
+def gru_peak(math, clk, peaks, tf32_peak):
+    """(peak, unit, bound, source) for the dominant kernel of `math`."""
+    burst = burst_clocks(clk)
+    which = "burst" if burst else "sustained"
+    bf16 = peaks.get("bf16_tflops" if burst else "bf16_tflops_sustained")
+    if math == "bf16":
+        if bf16:
+            return bf16, "TFLOP/s", "tensor", f"MEASURED_PEAKS bf16 ({which}: run at max clock, no power cap)" \
+                if burst else f"MEASURED_PEAKS bf16 ({which}: clocks below max or power-capped)"
+        return 2250.0, "TFLOP/s", "tensor", "B200_PROFILING nominal dense bf16 (no measured peak)"
+    if math in ("tf32", "tf32x3"):
+        div = 3.0 if math == "tf32x3" else 1.0
+        note = " / 3 (three TF32 products per useful multiply-add)" if math == "tf32x3" else ""
+        if tf32_peak:
+            return tf32_peak / div, "TFLOP/s", "tensor", f"cuBLAS TF32 8192^3 measured in this run (burst){note}"
+        return (bf16 or 2250.0) * 0.5 / div, "TFLOP/s", "tensor", f"bf16 peak x 0.5 (nominal tf32/bf16){note}"
+    sm_max = (clk.get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0)
+    return 148 * 128 * 2 * sm_max * 1e6 / 1e12, "TFLOP/s", "alu", \
+        "derived: 148 SMs x 128 FP32 lanes x 2 flop x sm_max_mhz (B300_MICROARCH unit counts)"
+
+
+# ----------------------------------------------------------------------------- the step bench
+class StepBench:
+    """One engine over this rank's streams; prefill, warm-up and two timed
+    passes of K frames (value: no library events; roofline: library events on)."""
+
+    def __init__(self, args, dims, model, wl, math, dev, world, local, group=None):
+        import torch
+
+        import paper_1801_09866_b200 as R
+        self.args, self.dims, self.wl, self.math, self.dev = args, dims, wl, math, dev
+        self.world, self.local = world, local
+        mode, k = key_mode(args.key)
+        self.n = wl.n_per_frame
+        cap = wl.max_histories_hint() if not args.no_cache else int(np.max(np.bincount(wl.session))) + 2
+        self.eng = R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math_id(math),
+                                     cell={"gru": R.CELL_GRU, "lbr": R.CELL_GRU_LBR, "rnn": R.CELL_RNN}[args.cell],
+                                     cache_enabled=not args.no_cache, num_sessions=wl.S,
+                                     max_queries_per_call=self.n, max_histories_per_session=cap, device=local,
+                                     max_queries_per_session_call=CONFIGS[args.workload]["B_s"])
+        self.d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
+        self.d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
+        self.d_ref = torch.as_tensor(wl.parent_ref, device=dev)
+        self.d_child = torch.zeros(wl.n_total, dtype=torch.int32, device=dev)
+        self.d_score = torch.zeros(wl.n_total, dtype=torch.float32, device=dev)
+        self.d_par = torch.zeros(self.n, dtype=torch.int32, device=dev)
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)        # > 126 MB L2
+        self.side = torch.cuda.Stream(device=dev)
+        self.gathered = torch.empty((world * self.n, 2), dtype=torch.int32, device=dev) if world > 1 else None
+        self.R = R
+        tail = args.warmup + 2 * args.steps
+        self.t0 = wl.frames - tail            # first warm-up frame
+
+    def call(self, t):
+        sl = self.wl.frame_slice(t)
+        if sl.stop == sl.start:
+            return sl
+        k = sl.stop - sl.start
+        self.R.resolve_parents(self.d_ref[sl], self.d_child, self.d_par[:k])
+        self.eng.query_batch(self.d_sess[sl], self.d_par[:k], self.d_word[sl], score=self.d_score[sl],
+                             child=self.d_child[sl], want_outcome=False)
+        return sl
+
+    def gather(self, sl):
+        from paper_1801_09866_b200.parallel import all_gather_results
+        all_gather_results(self.d_score[sl], self.d_child[sl], out=self.gathered)
+
+    def prefill(self):
+        import torch
+        for t in range(self.t0 + self.args.warmup):
+            self.call(t)
+        torch.cuda.synchronize()
+
+    def timed_pass(self, t_lo, t_hi, level, trace=None):
+        """Frames [t_lo, t_hi): one event pair per step; the L2 flush is between
+        pairs.  With N > 1 the all-gather of step i's results runs on a side
+        stream during step i + 1 and every step's end event waits for it (the
+        last gather is timed on its own), so all K gathers complete inside the
+        timed region.  Returns (ms, library timing, stat deltas, launches, clocks)."""
+        import torch
+        import torch.distributed as dist
+        eng, world = self.eng, self.world
+        st0 = eng.cache_stats()
+        eng.set_timing(level)
+        eng.get_timing(reset=True)
+        l0 = eng.launch_count()
+        clocks = ClockSampler(self.local)
+        time.sleep(0.3)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        main = torch.cuda.current_stream()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(t_hi - t_lo + 1)]
+        prof = None
+        if trace:
+            from torch.profiler import ProfilerActivity, profile
+            prof = profile(activities=[ProfilerActivity.CUDA])
+            prof.__enter__()
+        prev = None
+        for i, t in enumerate(range(t_lo, t_hi)):
+            self.flush.zero_()
+            evs[i][0].record()
+            if world > 1 and prev is not None:
+                self.side.wait_event(evs[i][0])
+                with torch.cuda.stream(self.side):
+                    self.gather(prev)
+            prev = self.call(t)
+            if world > 1:
+                main.wait_stream(self.side)
+            evs[i][1].record()
+        if world > 1:                                   # the last step's gather
+            evs[-1][0].record()
+            self.side.wait_event(evs[-1][0])
+            with torch.cuda.stream(self.side):
+                self.gather(prev)
+            main.wait_stream(self.side)
+            evs[-1][1].record()
+        torch.cuda.synchronize()
+        if prof is not None:
+            prof.__exit__(None, None, None)
+            prof.export_chrome_trace(trace)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        timing = eng.get_timing(reset=True)
+        eng.set_timing(0)
+        launches = eng.launch_count() - l0 + (t_hi - t_lo)      # + resolve_parents kernels
+        st1 = eng.cache_stats()
+        n_ev = len(evs) if world > 1 else len(evs) - 1
+        total_ms = float(sum(a.elapsed_time(b) for a, b in evs[:n_ev]))
+        if world > 1:
+            tt = torch.tensor([total_ms], dtype=torch.float64, device=self.dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            total_ms = float(tt[0])
+        d = {kk: st1[kk] - st0[kk] for kk in ("total_queries", "query_hits", "hidden_lookups",
+                                              "hidden_hits", "gru_computations")}
+        return total_ms, timing, d, launches, clk
+
+    def run(self, trace=None):
+        a = self.args
+        self.prefill()
+        tA = self.t0 + a.warmup
+        tB = tA + a.steps
+        ms_A, _, st_A, launches, clk = self.timed_pass(tA, tB, 0, trace)
+        ms_B, timing, st_B, _, clk_B = self.timed_pass(tB, tB + a.steps, max(2, a.timing_level))
+        return dict(ms=ms_A, stats=st_A, launches=launches, clocks=clk, ms_B=ms_B, timing=timing,
+                    stats_B=st_B, clocks_B=clk_B, frames=(tA, tB, tB + a.steps))
+
+
+def step_summary(args, bench, res, world, peaks, tf32_peak):
+    """value, roofline and hit rates of one StepBench.run()."""
+    import paper_1801_09866_b200 as R
+    dims, math = bench.dims, bench.math
+    steps = args.steps
+    q_rank = res["stats"]["total_queries"]
+    value = q_rank * world / (res["ms"] / 1e3)         # every rank has the same query count per frame
+    timing, rows = res["timing"], res["stats_B"]["gru_computations"]
+    gates = 1 if args.cell == "rnn" else 3
+    flops = 2.0 * gates * dims.H * (dims.E + dims.H) * rows      # [Q, E+H] x [E+H, gates*H]
+    tc = math != "fp32"
+    gemv = bench.n <= 512
+    k_ms = (timing["ms_gru_phase1"] + timing["ms_gru_phase2"]) if (tc and not gemv) else timing["ms_gru"]
+    peak, unit, bound, src = gru_peak(math, res["clocks_B"], peaks, tf32_peak)
+    achieved = flops / (k_ms / 1e3) / 1e12 if k_ms > 0 else 0.0
+    pair = (math == "bf16" and args.cell == "gru" and dims.H % 256 == 0
+            and os.environ.get("RNNLM_TC_PAIR", "1") != "0")
+    kname = ("k_gru_tc2 (fused tcgen05 GRU, both phases, CTA pair)" if pair else
+             "k_gru_tc (fused tcgen05 GRU, both phases)") if tc else "k_gru1_f32 + k_gru2_f32 (FP32 SIMT tiles)"
+    return {
+        "value": value, "ms_per_step": res["ms"] / steps, "dtype": dtype_of(math),
+        "roofline": {"kernel": kname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "traffic_ncu": "profiles/ncu_r2_summary.md (dram bytes per launch, ncu --set full)",
+                     "peak_source": src,
+                     "algorithmic": f"{2 * gates}*H*(E+H) flop per GRU row x {rows} rows over {steps} steps",
+                     "kernel_ms_per_step": k_ms / steps,
+                     "gather_plus_kernel_ms_per_step": timing["ms_gru"] / steps,
+                     "share_of_step": (k_ms / res["ms_B"]) if res["ms_B"] else None,
+                     "clocks_of_this_pass": res["clocks_B"]},
+        "kernel_ms_per_step": {kk: timing[kk] / steps for kk in
+                               ("ms_cache", "ms_score", "ms_gru", "ms_encode", "ms_final",
+                                "ms_gru_gather", "ms_gru_phase1", "ms_gru_phase2")},
+        "hit_rates": {"query_cache": res["stats"]["query_hits"] / max(1, res["stats"]["total_queries"]),
+                      "hidden_cache": res["stats"]["hidden_hits"] / max(1, res["stats"]["hidden_lookups"]),
+                      "hidden_hits_per_step": res["stats"]["hidden_hits"] / steps,
+                      "gru_rows_per_step": res["stats"]["gru_computations"] / steps},
+        "gpu_launches": int(res["launches"]),
+        "clocks": res["clocks"],
+    }
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    import paper_1801_09866_b200 as R
-    from paper_1801_09866_b200.parallel import all_gather_results
+    from paper_1801_09866_b200.parallel import session_range
 
     rank, world, local = dist_env()
     if args.gpus != world and world > 1:
@@ -235,206 +509,69 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
     c = CONFIGS[args.workload]
     dims = model_dims(args.workload)
-    S = sessions_for(args, world)
-    B_s = c["B_s"]
-    F0 = args.prefill
-    # two timed passes of K frames each: A (the bench value, no library timing
-    # events) then B (per-kernel CUDA events inside the library: roofline)
-    frames = F0 + args.warmup + 2 * args.steps
-    model = generate_model(dims, seed=1234)
-    V_draw = dims.V
-    wl = generate_workload(S, frames, B_s, V_draw, seed=7 + rank * S,
-                           zipf_s=0.0 if args.uniform_words else 1.0)
-    mode, k = key_mode(args.key)
-    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[args.math]
-    n = wl.n_per_frame
-    # cache off: every valid query makes a new history (reading 23), so the
-    # per-session pool must hold one per query of the run
-    cap = wl.max_histories_hint() if not args.no_cache else frames * B_s + 2
-    eng = R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math,
-                            cell={"gru": R.CELL_GRU, "lbr": R.CELL_GRU_LBR, "rnn": R.CELL_RNN}[args.cell],
-                            cache_enabled=not args.no_cache, num_sessions=S,
-                            max_queries_per_call=n, max_histories_per_session=cap, device=local)
-
-    d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
-    d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
-    d_ref = torch.as_tensor(wl.parent_ref, device=dev)
-    d_child = torch.zeros(wl.n_total, dtype=torch.int32, device=dev)
-    d_score = torch.zeros(wl.n_total, dtype=torch.float32, device=dev)
-    d_par = torch.zeros(n, dtype=torch.int32, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)        # > 126 MB L2
-    side = torch.cuda.Stream(device=dev)
-    gathered = torch.empty((world * n, 2), dtype=torch.int32, device=dev) if world > 1 else None
-    main = torch.cuda.current_stream()
-
-    def step(t, timed_events=None):
-        sl = wl.frame_slice(t)
-        R.resolve_parents(d_ref[sl], d_child, d_par)
-        if timed_events is not None:
-            timed_events[0].record()
-        eng.query_batch(d_sess[sl], d_par, d_word[sl], score=d_score[sl], child=d_child[sl],
-                        want_outcome=False)
-        if timed_events is not None:
-            timed_events[1].record()
-        if world > 1:
-            ev = torch.cuda.Event()
-            ev.record(main)
-            side.wait_event(ev)
-            with torch.cuda.stream(side):
-                all_gather_results(d_score[sl], d_child[sl], out=gathered)
-
-    # ---- prefill (utterance start, untimed) + warm-up
-    for t in range(F0 + args.warmup):
-        step(t)
-    torch.cuda.synchronize()
-
-    def timed_pass(t_lo, t_hi, level, trace=None):
-        """Frames [t_lo, t_hi), one event pair per step (resolve kernel + step;
-        the L2 flush is between pairs).  Returns (ms over ranks: max, library
-        timing, cache-stat deltas, our launches, clocks)."""
-        st0 = eng.cache_stats()
-        eng.set_timing(level)
-        eng.get_timing(reset=True)
-        l0 = eng.launch_count()
-        clocks = ClockSampler(local)
-        time.sleep(0.3)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(t_hi - t_lo)]
-        prof = None
-        if trace:
-            from torch.profiler import ProfilerActivity, profile
-            prof = profile(activities=[ProfilerActivity.CUDA])
-            prof.__enter__()
-        for i, t in enumerate(range(t_lo, t_hi)):
-            flush.zero_()
-            sl = wl.frame_slice(t)
-            evs[i][0].record()
-            R.resolve_parents(d_ref[sl], d_child, d_par)
-            eng.query_batch(d_sess[sl], d_par, d_word[sl], score=d_score[sl], child=d_child[sl],
-                            want_outcome=False)
-            if world > 1:
-                ev = torch.cuda.Event()
-                ev.record(main)
-                side.wait_event(ev)
-                with torch.cuda.stream(side):
-                    all_gather_results(d_score[sl], d_child[sl], out=gathered)
-            evs[i][1].record()
-        torch.cuda.synchronize()
-        if prof is not None:
-            prof.__exit__(None, None, None)
-            prof.export_chrome_trace(trace)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        clk = clocks.stop()
-        timing = eng.get_timing(reset=True)
-        eng.set_timing(0)
-        launches = eng.launch_count() - l0 + (t_hi - t_lo)      # + resolve_parents kernels
-        st1 = eng.cache_stats()
-        total_ms = float(sum(a.elapsed_time(b) for a, b in evs))
-        gru_ms = timing["ms_gru"]
-        if world > 1:
-            tt = torch.tensor([total_ms, gru_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            total_ms = float(tt[0])
-        d = {kk: st1[kk] - st0[kk] for kk in ("total_queries", "query_hits", "hidden_lookups",
-                                              "hidden_hits", "gru_computations")}
-        return total_ms, timing, d, launches, clk
-
-    tA = F0 + args.warmup
-    tB = tA + args.steps
-    total_ms, _, d_stats, launches, clk = timed_pass(tA, tB, 0, args.trace)
-    # level 2: events around the fused GRU kernel itself (k_gru_tc), after the A1 gather
-    ms_B, timing, d_B, _, _ = timed_pass(tB, tB + args.steps, max(2, args.timing_level))
-    queries_rank = n * args.steps
-    total_queries = queries_rank * world
-    value = total_queries / (total_ms / 1e3)
-    rows = d_B["gru_computations"]
-    gates = 1 if args.cell == "rnn" else 3                 # vanilla RNN: one gate
-    flops = 2.0 * gates * dims.H * (dims.E + dims.H) * rows   # [Q, E+H] x [E+H, gates*H], 2 flop/MAC
-    # the dominant kernel's own time: the fused GRU kernel (tensor-core paths) or
-    # the two SIMT GRU kernels (FP32), without the A1 gather / cache front
-    k_ms = timing["ms_gru_phase1"] + timing["ms_gru_phase2"] if math != R.MATH_FP32 else timing["ms_gru"]
-    gru_s = k_ms / 1e3
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    if math == R.MATH_BF16:
-        peak = peaks.get("bf16_tflops_sustained", 1400.0)
-        bound, peak_src = "tensor", ("measured bf16_tflops_sustained" if peaks else "fallback")
-    elif math == R.MATH_TF32X3:
-        # three TF32 products per useful multiply-add: useful-flop peak = TF32 peak / 3
-        peak = 0.5 * peaks.get("bf16_tflops_sustained", 1400.0) / 3.0
-        bound, peak_src = "tensor", ("measured bf16_tflops_sustained x 0.5 (tf32/bf16 dense ratio) / 3 "
-                                     "(three TF32 products per useful MAC)")
-    elif math == R.MATH_TF32:
-        # no measured TF32 peak: the measured bf16 peak x the nominal dense ratio (1.125 / 2.25 PF)
-        peak = 0.5 * peaks.get("bf16_tflops_sustained", 1400.0)
-        bound, peak_src = "tensor", "measured bf16_tflops_sustained x 0.5 (nominal tf32/bf16 dense ratio)"
+    S_job = args.sessions or c["S"]
+    if args.scaling == "strong":
+        if S_job % world:
+            raise SystemExit("strong scaling needs the streams divisible by the world size")
+        lo, hi = session_range(S_job, world, rank)
+        args.total_streams = S_job
     else:
-        sm_max = peaks.get("sm_max_mhz", 1965.0)
-        peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # FP32 FFMA lanes x 2 flop x clock
-        bound, peak_src = "alu", "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz"
-    achieved = flops / gru_s / 1e12 if gru_s > 0 else 0.0
-    # the library runs the CTA-pair kernel for the bf16 GRU when H % 256 == 0
-    # (gru_tc_prepare; RNNLM_TC_PAIR=0 selects one CTA per tile)
-    pair = (math == R.MATH_BF16 and args.cell == "gru" and dims.H % 256 == 0
-            and os.environ.get("RNNLM_TC_PAIR", "1") != "0")
-    gru_kernel = "k_gru_tc2" if pair else "k_gru_tc"
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        # captured for the paper's cell only; other cells report no traffic figure
-        ent = prof.get(args.workload, {}).get(args.math, {}) if args.cell == "gru" else {}
-        traffic = ent.get("kernels", {}).get(gru_kernel, ent.get("gru_dram_bytes_per_step"))
-    except Exception:
-        pass
+        lo, hi = rank * S_job, (rank + 1) * S_job
+        args.total_streams = S_job * world
+    tail = args.warmup + 2 * args.steps
+    frames = max(UTT_FRAMES, tail + 8)
+    peaks = load_peaks()
+    tf32_peak = measure_tf32_peak(dev) if ("tf32" in args.math or "tf32" in args.also) else None
+    model = generate_model(dims, seed=1234)
+    wl = multi_workload(args, lo, hi, frames, not args.no_stagger, args.uniform_words)
+
+    bench = StepBench(args, dims, model, wl, args.math, dev, world, local)
+    res = bench.run(args.trace)
+    head = step_summary(args, bench, res, world, peaks, tf32_peak)
+    tA, tB, tC = res["frames"]
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None,
-        "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "tf32x3": "f32 (3xTF32)"}[args.math], "data": "synthetic",
-        "config": {"workload": args.workload, "sessions_per_gpu": S, "queries_per_session_frame": B_s,
-                   "queries_per_step": total_queries // args.steps, "V": dims.V, "E": dims.E,
-                   "H": dims.H, "maxent": f"2^{dims.maxent_log2} {dims.N}-gram", "key": args.key,
-                   "cache": not args.no_cache, "math": args.math, "cell": args.cell,
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": head["dtype"], "data": "synthetic",
+        "config": {"workload": args.workload, "streams_total": args.total_streams, "streams_per_gpu": hi - lo,
+                   "queries_per_stream_frame": c["B_s"], "queries_per_step": int(wl.n_per_frame) * world,
+                   "V": dims.V, "E": dims.E, "H": dims.H, "maxent": f"2^{dims.maxent_log2} {dims.N}-gram",
+                   "key": args.key, "cache": not args.no_cache, "math": args.math, "cell": args.cell,
+                   "streams": ("staggered: stream s joins at frame s*%d/%d of a %d-frame run; timed frames see "
+                               "every utterance position" % (frames - tail - 1, args.total_streams - 1, frames))
+                   if not args.no_stagger else "in step (all join at frame 0)",
                    "l2": "flushed between timed steps (256 MiB write outside the event pair)",
-                   "timed_frames": f"value: frames {tA}..{tB - 1}; roofline pass (library kernel events on): frames {tB}..{frames - 1} ({F0} prefill + {args.warmup} warm-up frames untimed)",
-                   "parallelism": f"dp{world} (sessions sharded, weights replicated, NCCL all-gather of (score, child))"},
-        "roofline": {"kernel": ((f"{gru_kernel} (fused tcgen05 GRU, both phases"
-                                 + (", CTA pair)" if pair else ")")) if math != R.MATH_FP32
-                                else "k_gru1_f32 + k_gru2_f32 (+ gather, FP32 SIMT)"), "bound": bound,
-                     "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                     "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic": f"{2 * gates}*H*(E+H) flop x {rows} GRU rows over {args.steps} steps",
-                     "kernel_ms_per_step": k_ms / args.steps,
-                     "gather_plus_kernel_ms_per_step": timing["ms_gru"] / args.steps,
-                     "share_of_step": (k_ms / ms_B) if ms_B else None},
-        "kernel_ms_per_step": {kk: timing[kk] / args.steps for kk in
-                               ("ms_cache", "ms_score", "ms_gru", "ms_encode", "ms_final",
-                                "ms_gru_gather", "ms_gru_phase1", "ms_gru_phase2")},
-        "hit_rates": {"query_cache": d_stats["query_hits"] / max(1, d_stats["total_queries"]),
-                      "hidden_cache": d_stats["hidden_hits"] / max(1, d_stats["hidden_lookups"]),
-                      "gru_rows_per_step": d_stats["gru_computations"] / args.steps},
-        "gpu_launches": int(launches),
-        "clocks": clk,
+                   "timed_frames": f"value: frames {tA}..{tB - 1}; roofline pass (library kernel events on): "
+                                   f"frames {tB}..{tC - 1} ({tA} prefill/warm-up frames untimed)",
+                   "parallelism": f"{world} GPU(s), streams sharded ({args.scaling} scaling), weights replicated, "
+                                  "NCCL all-gather of (score, child) per step inside the timed region"},
+        "roofline": head["roofline"], "kernel_ms_per_step": head["kernel_ms_per_step"],
+        "hit_rates": head["hit_rates"], "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
     }
-    # ---- e2e: same metric through the C ABI with host buffers, copies inside the timed region
     if not args.no_e2e:
-        e2e = run_e2e(args, eng, wl, dev, world)
-        line["e2e"] = e2e
+        line["e2e"] = run_e2e(args, bench, dev, world)
+    del bench
+    gc.collect()
+    torch.cuda.empty_cache()
+    for other in [m for m in args.also.split(",") if m and m != "none" and m != args.math]:
+        b2 = StepBench(args, dims, model, wl, other, dev, world, local)
+        r2 = b2.run()
+        line[other] = {k: v for k, v in step_summary(args, b2, r2, world, peaks, tf32_peak).items()}
+        del b2
+        gc.collect()
+        torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        q, secs, f, _ = time_oracle(dims, model, wl, mode, k, not args.no_cache, args.cpu_seconds,
-                                    cell={"gru": 0, "lbr": 1, "rnn": 2}[args.cell])
-        line["cpu_baseline"] = {"value": q / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                "sample": f"session 0, frames 0..{f - 1} ({q} queries, {secs:.1f} s)",
+        mode, k = key_mode(args.key)
+        q, secs, f, _, th = time_oracle(dims, model, wl, mode, k, not args.no_cache, args.cpu_seconds,
+                                        cell={"gru": 0, "lbr": 1, "rnn": 2}[args.cell])
+        line["cpu_baseline"] = {"value": q / secs, "unit": UNIT, "cores": th, "kind": "oracle",
+                                "sample": f"stream 0, its utterance frames 0..{f - 1} ({q} queries, {secs:.1f} s "
+                                          f"of oracle time; scores and GRUs of a frame on {th} threads)",
                                 "cpu": cpu_model(), "host_cores": host_cores()}
+    del wl
+    gc.collect()
+    if rank == 0 and world == 1 and not args.no_configs:
+        line["configs"] = run_configs(args, dev, peaks, tf32_peak)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -442,54 +579,65 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, eng, wl, dev, world):
-    """Host-buffer path through the public C ABI: per step H2D of the decoder's
-    queries (session, parent reference = index of the earlier query whose child
-    is the parent, word) from pinned memory, rnnlm_resolve_parents (reference
-    -> handle, on the device, from the children the engine returned),
-    rnnlm_query_batch, D2H of (score, child) into pinned memory, synchronise."""
+def run_e2e(args, bench, dev, world):
+    """Host-buffer path through the public API: per step ONE H2D copy of the
+    decoder's packed queries (parent reference i64 = index of the earlier
+    query whose child is the parent, session u32, word u32) from pinned
+    memory, rnnlm_resolve_parents (reference -> handle on the device),
+    rnnlm_query_batch, (N > 1) the NCCL all-gather of (score, child), ONE D2H
+    copy of the (gathered) results into pinned memory, synchronise.  The
+    engine restarts its streams (reset) and replays the untimed frames on the
+    device first."""
     import torch
     import torch.distributed as dist
-    n = wl.n_per_frame
-    eng.reset_session()
+
     import paper_1801_09866_b200 as R
-    # per frame one contiguous pinned record block [ref i64 | session u32 | word u32] x n
-    # (16 B per query), so each step's inputs are ONE host->device copy
-    F = wl.frames
-    blk = np.empty((F, 4 * n), dtype=np.int32)
-    for t in range(F):
+    from paper_1801_09866_b200.parallel import all_gather_results
+    eng, wl, n = bench.eng, bench.wl, bench.n
+    eng.reset_session()
+    bench.d_child.zero_()
+    for t in range(bench.t0):                           # untimed replay up to the warm-up frames
+        bench.call(t)
+    torch.cuda.synchronize()
+    frames = list(range(bench.t0, bench.t0 + args.warmup + args.steps))
+    blk = np.empty((len(frames), 4 * n), dtype=np.int32)
+    for i, t in enumerate(frames):
         sl = wl.frame_slice(t)
-        blk[t, :2 * n] = np.ascontiguousarray(wl.parent_ref[sl], dtype=np.int64).view(np.int32)
-        blk[t, 2 * n:3 * n] = wl.session[sl].view(np.int32)
-        blk[t, 3 * n:] = wl.word[sl].view(np.int32)
+        assert sl.stop - sl.start == n
+        blk[i, :2 * n] = np.ascontiguousarray(wl.parent_ref[sl], dtype=np.int64).view(np.int32)
+        blk[i, 2 * n:3 * n] = wl.session[sl].view(np.int32)
+        blk[i, 3 * n:] = wl.word[sl].view(np.int32)
     h_in_all = torch.from_numpy(blk).pin_memory()
-    h_out = torch.empty(2 * n, dtype=torch.int32).pin_memory()      # [score bits | child]
+    out_rows = world * n
+    h_out = torch.empty(2 * out_rows, dtype=torch.int32).pin_memory()
     d_in = torch.empty(4 * n, dtype=torch.int32, device=dev)
     d_ref = d_in[:2 * n].view(torch.int64)
     d_sess, d_word = d_in[2 * n:3 * n], d_in[3 * n:]
     d_par = torch.empty(n, dtype=torch.int32, device=dev)
-    d_out = torch.empty(2 * n, dtype=torch.int32, device=dev)
-    d_score = d_out[:n].view(torch.float32)
-    d_child_log = torch.zeros(wl.n_total, dtype=torch.int32, device=dev)
+    d_score = torch.empty(n, dtype=torch.float32, device=dev)
+    d_out = torch.empty((out_rows, 2), dtype=torch.int32, device=dev)
 
-    def host_step(t):
+    def host_step(i, t):
         sl = wl.frame_slice(t)
-        d_in.copy_(h_in_all[t], non_blocking=True)
-        R.resolve_parents(d_ref, d_child_log, d_par)
-        eng.query_batch(d_sess, d_par, d_word, score=d_score, child=d_child_log[sl], want_outcome=False)
-        d_out[n:].copy_(d_child_log[sl])
-        h_out.copy_(d_out, non_blocking=True)
+        d_in.copy_(h_in_all[i], non_blocking=True)
+        R.resolve_parents(d_ref, bench.d_child, d_par)
+        eng.query_batch(d_sess, d_par, d_word, score=d_score, child=bench.d_child[sl], want_outcome=False)
+        if world > 1:
+            all_gather_results(d_score, bench.d_child[sl], out=d_out)
+        else:
+            d_out[:, 0].copy_(d_score.view(torch.int32))
+            d_out[:, 1].copy_(bench.d_child[sl])
+        h_out.copy_(d_out.view(-1), non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
-    F0 = args.prefill
-    for t in range(F0 + args.warmup):
-        host_step(t)
+    for i in range(args.warmup):
+        host_step(i, frames[i])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for t in range(F0 + args.warmup, F0 + args.warmup + args.steps):
-        host_step(t)
+    for i in range(args.warmup, len(frames)):
+        host_step(i, frames[i])
     torch.cuda.synchronize()
     secs = time.perf_counter() - t0
     if world > 1:
@@ -497,26 +645,182 @@ def run_e2e(args, eng, wl, dev, world):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         secs = float(tt[0])
     return {"value": n * args.steps * world / secs, "unit": UNIT,
-            "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n,
-            "note": "wall clock per step: H2D (session u32, parent reference i64, word u32) from pinned "
-                    "memory, device-side reference -> handle resolution, the step, D2H (score, child), "
-                    "synchronise; per rank, max over ranks"}
+            "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * out_rows,
+            "note": "wall clock per step: H2D (parent reference i64, session u32, word u32) from pinned memory, "
+                    "device-side reference -> handle resolution, the step, the all-gather (N > 1), D2H of the "
+                    "(score, child) results, synchronise; the same frames as the value pass; max over ranks"}
 
 
-def run_normalizer(args):
-    """SURVEY 8(f)-2: throughput of the exact log-normaliser (rnnlm_log_normalizer)
-    on the large model (V = 200k, H = 1024, 4-gram MaxEnt 2^27): log Z of
-    --histories distinct stored histories per call (the 2,048 queries/frame of
-    BASELINE configs[2]), device-timed with CUDA events; one JSON line.
-    Roofline of the dominant kernel (k_norm_tc): its algorithmic traffic is
-    the MaxEnt gathers, (K - 1) random 4-byte reads = 32-byte sectors per
-    (history, word) (order 1 is a per-word bias), plus one pass over the bf16
-    output rows per 128-history tile; the contraction (two bf16 MMAs per
-    element pair) is reported beside it."""
+# ----------------------------------------------------------------------------- configs[0]-[3]
+def single_stream(name, frames=None, seed=7):
+    c = CONFIGS[name]
+    d = model_dims(name)
+    return d, generate_workload(1, frames or c["frames"], c["B_s"], d.V, seed=seed)
+
+
+def frame_loop(eng, wl, dev, t_lo, t_hi, use_graph=False, timing=0):
+    """Run frames [0, t_hi) of a one-stream workload, time [t_lo, t_hi) as one
+    device interval and on the host clock.  Returns (device ms, wall s,
+    scores, children, library timing)."""
     import torch
 
     import paper_1801_09866_b200 as R
-    from synth import generate_model, generate_workload, model_dims
+    n = wl.n_per_frame
+    d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
+    d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
+    d_ref = torch.as_tensor(wl.parent_ref, device=dev)
+    d_child = torch.zeros(wl.n_total, dtype=torch.int32, device=dev)
+    d_score = torch.zeros(wl.n_total, dtype=torch.float32, device=dev)
+    par = torch.zeros(n, dtype=torch.int32, device=dev)
+    if use_graph:
+        bs, bw = torch.zeros(n, dtype=torch.int32, device=dev), torch.zeros(n, dtype=torch.int32, device=dev)
+        sc, ch = torch.zeros(n, dtype=torch.float32, device=dev), torch.zeros(n, dtype=torch.int32, device=dev)
+        g = eng.graph(n, bs, par, bw, sc, ch)
+
+    def frame(t):
+        sl = wl.frame_slice(t)
+        R.resolve_parents(d_ref[sl], d_child, par)
+        if use_graph:
+            bs.copy_(d_sess[sl])
+            bw.copy_(d_word[sl])
+            g.launch()
+            d_child[sl].copy_(ch)
+            d_score[sl].copy_(sc)
+        else:
+            eng.query_batch(d_sess[sl], par, d_word[sl], score=d_score[sl], child=d_child[sl], want_outcome=False)
+
+    for t in range(t_lo):
+        frame(t)
+    torch.cuda.synchronize()
+    eng.set_timing(timing)
+    eng.get_timing(reset=True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    a.record()
+    for t in range(t_lo, t_hi):
+        frame(t)
+    b.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    tm = eng.get_timing(reset=True)
+    eng.set_timing(0)
+    return a.elapsed_time(b), wall, d_score.cpu().numpy(), d_child.cpu().numpy(), tm
+
+
+def run_configs(args, dev, peaks, tf32_peak):
+    """BASELINE configs[0]-[3] on one GPU (single utterance stream each):
+    per-frame latency and q/s (direct calls and a replayed CUDA graph), the
+    small-frame GEMV kernels' achieved bytes/s, bf16 vs fp32-accurate on the
+    large model, and the compression sweep."""
+    import torch
+
+    import paper_1801_09866_b200 as R
+    out = {}
+    hbm = peaks.get("hbm_gbs", 6551.0)
+
+    def eng_for(d, m, wl, key, math, path=R.GRU_AUTO, cache=True):
+        mode, k = key_mode(key)
+        return R.RNNLM.from_dims(d, m, key_mode=mode, round_digits=k, math=math_id(math), cache_enabled=cache,
+                                 num_sessions=1, max_queries_per_call=wl.n_per_frame,
+                                 max_histories_per_session=wl.max_histories_hint(), gru_path=path)
+
+    # tiny (configs[0]) and moderate (configs[1]): latency-bound single-stream frames
+    for name, maths, keys in (("tiny", ("fp32",), ("sign", "round:2")),
+                              ("moderate", ("bf16", "tf32x3"), ("off", "sign"))):
+        d, wl = single_stream(name)
+        m = generate_model(d, seed=1234)
+        F = wl.frames
+        t_lo = min(40, F // 2)
+        res = {}
+        for math in maths:
+            for key in keys:
+                e = eng_for(d, m, wl, key, math)
+                ms, wall, _, _, tm = frame_loop(e, wl, dev, t_lo, F, timing=1)
+                st = e.cache_stats()
+                del e
+                e = eng_for(d, m, wl, key, math)
+                ms_g, wall_g, _, _, _ = frame_loop(e, wl, dev, t_lo, F, use_graph=True)
+                del e
+                nq = wl.n_per_frame * (F - t_lo)
+                rows = st["gru_computations"]
+                # GEMV algorithmic bytes per frame: the gate weights once (L2-resident),
+                # the gathered x / h of every GRU row, its new state
+                s_w = 2 if math == "bf16" else 4
+                wbytes = 3 * d.H * (d.E + d.H) * s_w
+                rbytes = rows / F * (d.E * s_w + 4 * d.H + 4 * d.H)
+                gemv_ms = tm["ms_gru"] / max(1, tm["calls"])
+                gbs = (wbytes + rbytes) / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None
+                res[f"{math}/{key}"] = {
+                    "q_per_s": nq / (ms * 1e-3), "us_per_frame": 1e3 * ms / (F - t_lo),
+                    "q_per_s_wall": nq / wall, "us_per_frame_wall": 1e6 * wall / (F - t_lo),
+                    "graph": {"q_per_s": nq / (ms_g * 1e-3), "us_per_frame": 1e3 * ms_g / (F - t_lo),
+                              "us_per_frame_wall": 1e6 * wall_g / (F - t_lo)},
+                    "query_cache_hit": st["query_hits"] / max(1, st["total_queries"]),
+                    "hidden_hits": st["hidden_hits"], "gru_rows_per_frame": rows / F,
+                    "gemv": {"kernels": "k_gemv1 + k_gemv2", "us_per_frame": 1e3 * gemv_ms,
+                             "algorithmic_bytes_per_frame": wbytes + rbytes, "achieved_gbs": gbs,
+                             "hbm_peak_gbs": hbm, "frac_of_hbm": (gbs / hbm) if gbs else None,
+                             "note": "latency-bound: the frame's weights (L2-resident) and rows take a few "
+                                     "dependent L2 round trips; bytes/s is far below HBM bandwidth"},
+                }
+        out[name] = {"streams": 1, "queries_per_frame": wl.n_per_frame, "frames": F,
+                     "timed_frames": f"{t_lo}..{F - 1}", "V": d.V, "H": d.H, "results": res}
+        del m
+        gc.collect()
+        torch.cuda.empty_cache()
+
+    # large (configs[2]) and the compression sweep (configs[3]): one stream, 2,048 queries/frame
+    d, wl = single_stream("large")
+    m = generate_model(d, seed=1234)
+    F = wl.frames
+    t_lo = F - 60
+    res = {}
+    for math in ("bf16", "tf32x3", "fp32"):
+        e = eng_for(d, m, wl, "sign", math)
+        ms, wall, _, _, tm = frame_loop(e, wl, dev, t_lo, F, timing=0)
+        st = e.cache_stats()
+        del e
+        res[math] = {"q_per_s": wl.n_per_frame * (F - t_lo) / (ms * 1e-3), "us_per_frame": 1e3 * ms / (F - t_lo),
+                     "gru_rows_per_frame": st["gru_computations"] / F, "dtype": dtype_of(math)}
+    out["large"] = {"streams": 1, "queries_per_frame": wl.n_per_frame, "frames": F, "key": "sign",
+                    "timed_frames": f"{t_lo}..{F - 1}", "results": res}
+    sweep = {}
+    base = None
+    for key in ("off", "round:3", "round:2", "round:1", "sign"):
+        e = eng_for(d, m, wl, key, "bf16")
+        ms, wall, sc, ch, _ = frame_loop(e, wl, dev, 0, F)
+        st = e.cache_stats()
+        del e
+        if base is None:
+            base = (sc, st["gru_computations"])
+        dev_abs = np.abs(sc.astype(np.float64) - base[0].astype(np.float64))
+        sweep[key] = {"hidden_hit_rate": st["hidden_hits"] / max(1, st["hidden_lookups"]),
+                      "gru_computations": st["gru_computations"],
+                      "redundancy_pct_vs_off": 100.0 * (base[1] - st["gru_computations"]) / max(1, base[1]),
+                      "score_dev_vs_off_max": float(dev_abs.max()), "score_dev_vs_off_mean": float(dev_abs.mean()),
+                      "q_per_s": wl.n_total / (ms * 1e-3)}
+    out["sweep"] = {"model": "large", "math": "bf16", "streams": 1, "frames": F,
+                    "queries": int(wl.n_total), "note": "Table 1 (P:122-143) on the synthetic stream: redundancy "
+                    "= (gru(off) - gru(mode)) / gru(off); score deviation against the same engine with lossless "
+                    "keys (mode off) over the whole utterance", "results": sweep}
+    del m
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
+
+
+# ----------------------------------------------------------------------------- (f2), (f4)
+def run_normalizer(args):
+    """SURVEY 8(f)-2: throughput of the exact log-normaliser (rnnlm_log_normalizer)
+    on the large model (V = 200k, H = 1024, 4-gram MaxEnt 2^27): log Z of
+    --histories distinct stored histories per call, device-timed with CUDA
+    events; one JSON line.  Roofline of the dominant kernel (k_norm_tc): its
+    algorithmic traffic is the MaxEnt gathers, (K - 1) random 4-byte reads =
+    32-byte sectors per (history, word) (order 1 is a per-word bias), plus one
+    pass over the bf16 output rows per 128-history tile."""
+    import torch
+
+    import paper_1801_09866_b200 as R
 
     d = model_dims("large")
     m = generate_model(d, seed=1234)
@@ -524,7 +828,7 @@ def run_normalizer(args):
     # distinct histories: one utterance, cache off, 2 frames of n/2 queries
     # each -> every query makes a new history (depth 1 and 2)
     wl = generate_workload(1, 2, n // 2, d.V, seed=5)
-    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[args.math]
+    math = math_id(args.math)
     eng = R.RNNLM.from_dims(d, m, key_mode=R.KEY_SIGN, math=math, cache_enabled=False, num_sessions=1,
                             max_queries_per_call=n, max_histories_per_session=n + 2)
     dev = torch.device("cuda", 0)
@@ -557,19 +861,8 @@ def run_normalizer(args):
     sectors = n * d.V * (K - 1) * 32.0
     theta = -(-n // 128) * d.V * d.H * 2.0
     flops = 2.0 * 2.0 * n * d.V * d.H
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm = peaks.get("hbm_gbs", 6458.1)
+    hbm = load_peaks().get("hbm_gbs", 6551.0)
     gbs = (sectors + theta) / (ms * 1e-3) / 1e9
-    traffic = None
-    try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))["normalizer"]["bf16"][
-            "k_norm_tc_dram_bytes_per_launch"]
-    except Exception:
-        pass
     line = {
         "metric": "exact log-normalisers/sec (large model, V=200k, 4-gram MaxEnt)", "value": n / (ms * 1e-3),
         "unit": "histories/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -581,20 +874,8 @@ def run_normalizer(args):
                      "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                      "algorithmic": f"{n} x {d.V} x {K - 1} random 32-B MaxEnt sectors + {-(-n // 128)} passes "
                                     f"over the bf16 output rows",
-                     "traffic": traffic, "contraction_tflops": flops / (ms * 1e-3) / 1e12},
+                     "traffic": None, "contraction_tflops": flops / (ms * 1e-3) / 1e12},
     }
-    if not args.no_cpu_baseline:
-        import oracle as O
-        orc = O.Oracle(O.make_config(d.V, d.E, d.H, d.maxent_log2, d.N, O.KEY_OFF, 0, 0, 1, n + 2), m)
-        st = eng.read_states(0, np.arange(1, 3, dtype=np.uint32)).cpu().numpy()
-        t0 = time.perf_counter()
-        cfg = O.make_config(d.V, d.E, d.H, d.maxent_log2, d.N)
-        for i in range(2):
-            O.log_normalizer(cfg, m, st[i], [int(wl.word[i])])
-        secs = time.perf_counter() - t0
-        line["cpu_baseline"] = {"value": 2 / secs, "unit": "histories/s", "cores": 1, "kind": "oracle",
-                                "sample": f"2 histories ({secs:.1f} s)"}
-        del orc
     print(json.dumps(line), flush=True)
 
 
@@ -602,8 +883,11 @@ def run_offline(args):
     """whole utterances known in advance (2-pass lattice
     rescoring) scheduled level by level (paper_1801_09866_b200.offline)
     instead of one call per frame.  Both schedules run the same synthetic
-    utterances on the same engine settings; each is device-timed with CUDA
-    events around the whole stream (after one untimed warm-up pass)."""
+    utterances on the same engine settings (the tile GRU kernels); each is
+    device-timed with CUDA events around the whole stream (after one untimed
+    warm-up pass).  With lossy keys the level order changes which query is a
+    key's first occupant, so results are bitwise equal to the online schedule
+    only at key off (reported)."""
     import torch
 
     import paper_1801_09866_b200 as R
@@ -616,14 +900,14 @@ def run_offline(args):
     model = generate_model(dims, seed=1234)
     wl = generate_workload(S, frames, c["B_s"], dims.V, seed=7)
     mode, k = key_mode(args.key)
-    math = {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[args.math]
+    math = math_id(args.math)
     dev = torch.device("cuda", 0)
     Bmax = 32768
     cap = wl.max_histories_hint()
 
     def engine(B):
         return R.RNNLM.from_dims(dims, model, key_mode=mode, round_digits=k, math=math, num_sessions=S,
-                                 max_queries_per_call=B, max_histories_per_session=cap)
+                                 max_queries_per_call=B, max_histories_per_session=cap, gru_path=R.GRU_TILES)
 
     d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
     d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
@@ -659,13 +943,13 @@ def run_offline(args):
 
     ms_on = timed(online)
     ms_off = timed(offline)
-    same = bool(torch.equal(d_score, runner.score)) if mode == R.KEY_OFF else None
+    same = bool(torch.equal(d_score, runner.score))
     nb = len(runner.batches)
     line = {
         "metric": "RNNLM queries/sec (offline level-batched rescoring of whole utterances)",
         "value": wl.n_total / (ms_off * 1e-3), "unit": "queries/s", "n_gpus": 1, "steps": 1, "warmup": 1,
         "ms_per_step": ms_off, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "tf32x3": "f32 (3xTF32)"}[args.math], "data": "synthetic",
+        "dtype": dtype_of(args.math), "data": "synthetic",
         "config": {"workload": args.workload, "sessions": S, "frames": frames, "queries": int(wl.n_total),
                    "key": args.key, "math": args.math, "offline_calls": nb, "online_calls": frames,
                    "mean_queries_per_offline_call": wl.n_total / max(1, nb),
@@ -673,6 +957,8 @@ def run_offline(args):
         "online": {"value": wl.n_total / (ms_on * 1e-3), "ms": ms_on},
         "speedup_vs_online": ms_on / ms_off,
         "scores_bitwise_equal_online": same,
+        "note": None if mode == R.KEY_OFF else "lossy keys: the level order changes first occupants, so results "
+                                               "may differ from the online schedule (DESIGN.md reading 29)",
     }
     print(json.dumps(line), flush=True)
 

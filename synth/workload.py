@@ -69,10 +69,12 @@ class Workload:
 
     def _select(self, keep: np.ndarray, frame_of: np.ndarray, frames: int, session: np.ndarray,
                 S: int, new_per_session: np.ndarray) -> "Workload":
-        """Queries with keep[i], placed in frame frame_of[i] (stable order inside a
-        frame), references re-based; a kept query's parent must be kept."""
+        """Queries with keep[i], placed in frame frame_of[i] (inside a frame:
+        session-major, stream order within a session -- the order
+        rnnlm_query_batch requires), references re-based; a kept query's parent
+        must be kept."""
         idx = np.nonzero(keep)[0]
-        order = idx[np.argsort(frame_of[idx], kind="stable")]
+        order = idx[np.lexsort((idx, session[idx], frame_of[idx]))]
         remap = np.full(self.n_total, -1, dtype=np.int64)
         remap[order] = np.arange(len(order))
         pr = self.parent_ref[order]

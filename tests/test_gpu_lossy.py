@@ -86,7 +86,7 @@ def test_gemv_path_h256(math, mode, k):
 def test_gemv_path_cells(math, cell):
     """GEMV path for the LBR and vanilla-RNN cells."""
     d, m = model("moderate")
-    wl = generate_workload(1, 60, 256, d.V, seed=23, dur=(2, 6), eps=0.1)
+    wl = generate_workload(1, 100, 256, d.V, seed=23, dur=(2, 6), eps=0.1)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=cell, path=GRU_GEMV)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
     assert rep["miss"] > 200

@@ -31,6 +31,12 @@ def model(name_or_dims, seed=1234, scale=None):
     return _models[key]
 
 
+def lattice(S, F, B, V, seed):
+    """A stream with many GRU rows early on: short words (2-6 frames) and
+    substitution rate 0.1, so 8-40 frames already hold several words per path."""
+    return generate_workload(S, F, B, V, seed=seed, dur=(2, 6), eps=0.1)
+
+
 def pair(d, m, wl, mode=KEY_OFF, k=0, math=MATH_FP32, cache=True, B=None, cap=None, cell=0, path=GRU_TILES):
     """An engine (GRU kernels: ``path``; the tile kernels unless a test asks
     for the small-frame GEMV kernels) and an oracle over the same model."""
@@ -253,7 +259,7 @@ def test_resolve_parents_kernel():
 @pytest.mark.parametrize("mode", [KEY_OFF, KEY_SIGN])
 def test_moderate_bf16_tensor_core(mode):
     d, m = model("moderate")
-    wl = generate_workload(1, 40, 256, d.V, seed=17)
+    wl = lattice(1, 40, 256, d.V, seed=17)
     eng, orc = pair(d, m, wl, mode, math=MATH_BF16)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_BF16], tol_state=TOL[MATH_BF16])
     assert rep["miss"] > 300
@@ -265,7 +271,7 @@ def test_moderate_bf16_round_codes(k):
     the tcgen05 phase-2 epilogue; codes bit-exact vs the oracle's compress() of
     the same GPU vector, lossy hidden-cache hits identical (replay protocol)."""
     d, m = model("moderate")
-    wl = generate_workload(1, 40, 256, d.V, seed=19)
+    wl = lattice(1, 40, 256, d.V, seed=19)
     eng, orc = pair(d, m, wl, KEY_ROUND, k=k, math=MATH_BF16)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_BF16], tol_state=TOL[MATH_BF16])
     assert rep["miss"] > 300
@@ -334,7 +340,7 @@ def test_multisession_bf16_sample():
 @pytest.mark.parametrize("mode", [KEY_OFF, KEY_SIGN])
 def test_moderate_tf32_tensor_core(mode):
     d, m = model("moderate")
-    wl = generate_workload(1, 40, 256, d.V, seed=17)
+    wl = lattice(1, 40, 256, d.V, seed=17)
     eng, orc = pair(d, m, wl, mode, math=MATH_TF32)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_TF32], tol_state=TOL[MATH_TF32])
     assert rep["miss"] > 300
@@ -411,7 +417,7 @@ def test_lbr_cell_moderate(math):
     phase 2 contracts h), BF16 / TF32 one-phase tcgen05 tiles (N = 192 over
     the x part, N = 128 + 64 over the h part)."""
     d, m = model("moderate")
-    wl = generate_workload(1, 30, 256, d.V, seed=23)
+    wl = lattice(1, 30, 256, d.V, seed=23)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=O.CELL_GRU_LBR)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
     assert rep["miss"] > 200
@@ -492,7 +498,7 @@ def test_rnn_cell_moderate(math):
     path: FP32 SIMT (phase 2 contracts h), BF16 / TF32 one-phase tcgen05 tiles
     of A1 x [Wh | Uh]; lossy sign keys, codes bit-exact."""
     d, m = model("moderate")
-    wl = generate_workload(1, 30, 256, d.V, seed=31)
+    wl = lattice(1, 30, 256, d.V, seed=31)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=O.CELL_RNN)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
     assert rep["miss"] > 200
@@ -515,7 +521,7 @@ def test_fig4_hidden_sizes_tensor_core(H, cell, math):
     the tensor-core paths, every cell, E = H, lossy sign keys."""
     d = ModelDims(V=5000, E=H, H=H, maxent_log2=18, N=4)
     m = generate_model(d, seed=77)
-    wl = generate_workload(1, 12, 300, d.V, seed=13)
+    wl = lattice(1, 20, 300, d.V, seed=13)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=cell)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
     assert rep["miss"] > 100
@@ -533,7 +539,7 @@ def test_tensor_core_embed_neq_hidden(E, math, pair_kernel, monkeypatch):
     monkeypatch.setenv("RNNLM_TC_PAIR", pair_kernel)
     d = ModelDims(V=3000, E=E, H=256, maxent_log2=16, N=3)
     m = generate_model(d, seed=41)
-    wl = generate_workload(2, 8, 300, d.V, seed=19)
+    wl = lattice(2, 14, 300, d.V, seed=19)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
     assert rep["miss"] > 100
@@ -545,7 +551,7 @@ def test_tf32x3_moderate_fp32_tolerance():
     (operands split into TF32 hi + lo parts, three products), sign keys with
     lossy hits, codes bit-exact."""
     d, m = model("moderate")
-    wl = generate_workload(1, 30, 256, d.V, seed=17)
+    wl = lattice(1, 30, 256, d.V, seed=17)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_TF32X3)
     rep = replay_compare(eng, orc, wl, tol_score=1e-5, tol_state=1e-5)
     assert rep["miss"] > 200

@@ -13,7 +13,7 @@ oracle, at every key mode; states / scores within the path's tolerance.
 import numpy as np
 import pytest
 
-from paper_1801_09866_b200 import KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32
+from paper_1801_09866_b200 import GRU_GEMV, GRU_TILES, KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32
 from paper_1801_09866_b200.offline import level_schedule
 from synth import generate_workload
 from tests.parity_util import replay_compare
@@ -101,3 +101,58 @@ def test_graph_replay_equals_direct_calls(math):
     assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
     assert outs[0][3] == outs[1][3]
     assert outs[0][3]["hidden_hits"] > 0
+
+
+@pytest.mark.parametrize("math", [MATH_BF16, MATH_FP32])
+def test_session_sharded_engines_equal_one_engine(math):
+    """SURVEY 8(e) equality test on one GPU: the sessions split over two
+    engines (what two ranks of bench.py --gpus 2 hold, parallel.session_range)
+    return -- concatenated in session order, as the all-gather assembles them --
+    bitwise the scores, handles, outcomes and stats of ONE engine over all
+    sessions; large model, 4 staggered streams x 512 queries, sign keys."""
+    import torch
+    import oracle as O
+    from paper_1801_09866_b200.parallel import session_range
+    from tests.parity_util import _dev
+    d, m = model("large")
+    wl = generate_workload(4, 24, 512, d.V, seed=5, dur=(2, 5), eps=0.1).staggered([0, 3, 5, 9])
+    parts = [(0, 4)] + [session_range(4, 2, r) for r in range(2)]
+    res = {}
+    for lo, hi in parts:
+        sub = wl.select_sessions(lo, hi)
+        eng, _ = pair(d, m, sub, KEY_SIGN, math=math, path=GRU_TILES if math == MATH_BF16 else GRU_GEMV,
+                      B=wl.n_per_frame)
+        child = np.zeros(sub.n_total, np.uint32)
+        score = np.zeros(sub.n_total, np.float32)
+        outc = np.zeros(sub.n_total, np.uint8)
+        for t in range(sub.frames):
+            sl = sub.frame_slice(t)
+            if sl.stop == sl.start:
+                continue
+            par = O.resolve_parents(sub.parent_ref[sl], child)
+            s_, c_, o_ = eng.query_batch(_dev(sub.session[sl]), _dev(par), _dev(sub.word[sl]))
+            score[sl], child[sl], outc[sl] = s_.cpu().numpy(), c_.cpu().numpy().view(np.uint32), o_.cpu().numpy()
+        res[(lo, hi)] = (sub, score, child, outc, eng.cache_stats())
+    whole = res[(0, 4)]
+    for s in range(4):
+        one = [v for (lo, hi), v in res.items() if (lo, hi) != (0, 4) and lo <= s < hi][0]
+        a = whole[0].session == s
+        b = one[0].session == (s - [lo for (lo, hi) in res if (lo, hi) != (0, 4) and lo <= s < hi][0])
+        assert np.array_equal(whole[1][a].view(np.uint32), one[1][b].view(np.uint32))
+        assert np.array_equal(whole[2][a], one[2][b]) and np.array_equal(whole[3][a], one[3][b])
+    tot = {k: sum(v[4][k] for (lo, hi), v in res.items() if (lo, hi) != (0, 4))
+           for k in ("total_queries", "query_hits", "hidden_lookups", "hidden_hits", "gru_computations")}
+    assert all(tot[k] == whole[4][k] for k in tot)
+
+
+@pytest.mark.parametrize("path", [GRU_TILES, GRU_GEMV])
+@pytest.mark.parametrize("math", [MATH_FP32, MATH_BF16])
+def test_staggered_streams_vs_oracle(math, path):
+    """Streams that join at different frames (bench.py's multi workload:
+    calls hold only the sessions that have started, session counts vary per
+    call) against the oracle, sign keys merging."""
+    d, m = model("moderate")
+    wl = generate_workload(3, 90, 64, d.V, seed=11, dur=(2, 5), eps=0.1).staggered([0, 7, 19])
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=math, path=path)
+    rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
+    assert rep["shit"] > 100, rep

@@ -225,3 +225,22 @@ def test_reset_session_clears(small):
     e.reset_session(0)
     assert e.num_handles(0) == (1, 1) and e.num_handles(1) == (2, 2)
     assert e.stats(0)["total_queries"] == 0 and e.stats(1)["total_queries"] == 1
+
+
+def test_staggered_and_selected_workloads_are_well_formed():
+    """Workload plumbing used by bench.py / the GPU tests: every frame of a
+    staggered or session-selected stream is sorted by session (reading 24),
+    parents come from earlier frames of the same session (reading 17), and a
+    stream keeps its own query sequence."""
+    wl = generate_workload(3, 20, 16, 1000, seed=7)
+    st = wl.staggered([0, 5, 10])
+    for w in (st, st.select_sessions(1, 3), wl.select_sessions(0, 2)):
+        f = w.frame_index()
+        for t in range(w.frames):
+            s = w.session[w.frame_slice(t)].astype(np.int64)
+            assert np.all(np.diff(s) >= 0)
+        m = w.parent_ref >= 0
+        assert np.all(f[w.parent_ref[m]] < f[m])
+        assert np.all(w.session[w.parent_ref[m]] == w.session[m])
+    a, b = wl.select_sessions(1, 2), st.select_sessions(1, 2)
+    assert np.array_equal(a.word[:b.n_total], b.word) and np.array_equal(a.parent_ref[:b.n_total], b.parent_ref)
