@@ -113,7 +113,10 @@ typedef enum { RNNLM_CELL_GRU = 0, RNNLM_CELL_GRU_LBR = 1, RNNLM_CELL_RNN = 2 } 
  * FP32 and 3xTF32 engines use plain fp32 FFMA).  AUTO: GEMV for calls of at
  * most RNNLM_GEMV_AUTO_MAX_QUERIES queries, tiles otherwise.  Results of the
  * two kinds agree within the math mode's tolerance, not bitwise (summation
- * order). */
+ * order).  On the AUTO path a call of at most RNNLM_GEMV_AUTO_MAX_QUERIES
+ * queries runs as ONE cooperative kernel (k_small: every step of the call,
+ * grid barriers instead of kernel boundaries; results bitwise those of the
+ * GEMV path). */
 typedef enum { RNNLM_GRU_AUTO = 0, RNNLM_GRU_TILES = 1, RNNLM_GRU_GEMV = 2 } rnnlm_gru_path;
 #define RNNLM_GEMV_AUTO_MAX_QUERIES 512u
 
@@ -165,6 +168,7 @@ typedef struct {
   uint64_t launches;    /* kernels launched by those calls */
   /* timing level 2, tensor-core paths only: split of ms_gru (gather, fused GEMM) */
   double ms_gru_gather, ms_gru_phase1, ms_gru_phase2;
+  double ms_fused;      /* calls that ran the fused small-frame kernel (k_small): the whole step */
 } rnnlm_timing;
 
 /* Create an engine on cfg->device: validates dims and weights, copies the

@@ -45,7 +45,8 @@ class Timing(ctypes.Structure):
                 ("ms_gru", ctypes.c_double), ("ms_encode", ctypes.c_double),
                 ("ms_final", ctypes.c_double), ("calls", ctypes.c_uint64),
                 ("launches", ctypes.c_uint64), ("ms_gru_gather", ctypes.c_double),
-                ("ms_gru_phase1", ctypes.c_double), ("ms_gru_phase2", ctypes.c_double)]
+                ("ms_gru_phase1", ctypes.c_double), ("ms_gru_phase2", ctypes.c_double),
+                ("ms_fused", ctypes.c_double)]
 
 
 # name -> (restype, argtypes); every symbol include/rnnlm.h declares

@@ -24,6 +24,9 @@ int gemv_prepare(const Params &P, const rnnlm_weights *w, uint32_t math, const v
                  uint32_t tc_rw, uint32_t rows, void **state_out);
 void gemv_release(void *state);
 int launch_gemv(const Params &P, void *state, int num_sms, cudaStream_t s);
+// Fused small-frame step (k_small.cu).
+uint32_t small_max_queries();
+int launch_small(const Params &P, const CallArgs &A, void *gemv_state, uint32_t *bar, int num_sms, cudaStream_t s);
 int launch_gru_tc(const Params &P, void *tc_state, uint32_t max_rows, int num_sms, cudaStream_t s,
                   cudaEvent_t ev_gathered, cudaEvent_t ev_phase1, cudaEvent_t ev_fork);
 // Exact log-normaliser (k_norm.cu).
@@ -50,7 +53,12 @@ struct rnnlm {
   // timing
   int timing = 0;
   std::vector<cudaEvent_t> ev_pool;
-  std::vector<std::vector<cudaEvent_t>> ev_pending;   // NEV (+2 at level 2) events per timed call
+  struct Pending {
+    std::vector<cudaEvent_t> ev;      // NEV events per timed call
+    bool fused;                       // the call ran the fused small-frame kernel (ev[0] -> ev[1])
+  };
+  std::vector<Pending> ev_pending;
+  uint32_t *bar = nullptr;            // grid barrier of the fused small-frame kernel
   rnnlm_timing acc{};
 };
 
@@ -130,7 +138,8 @@ void free_all(rnnlm *h) {
   for (void *p : h->allocs) cudaFree(p);
   h->allocs.clear();
   for (auto &v : h->ev_pending)
-    for (cudaEvent_t e : v) cudaEventDestroy(e);
+    for (cudaEvent_t e : v.ev)
+      if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   h->ev_pending.clear();
   h->ev_pool.clear();
@@ -317,6 +326,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   chk(dalloc(h, &P.tile_status, (B + rnnlm_host::SCAN_TILE - 1) / rnnlm_host::SCAN_TILE));
   chk(dalloc(h, &P.tile_ticket, 1));
   chk(dalloc(h, &P.counts, 4));
+  chk(dalloc(h, &h->bar, 2));
   // z: the tensor-core path keeps it in 128-row blocks (k_gru_tc.cu zq4), so whole blocks
   chk(dalloc(h, &P.g_z, (B + 127) / 128 * 128 * H));
   if (c.math == RNNLM_MATH_FP32) chk(dalloc(h, &P.g_wxb, B * H));
@@ -346,6 +356,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   if (st == RNNLM_OK) chk(cuda_status(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming)));
   if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.sticky, 0, sizeof(int))));
   if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.counts, 0, 4 * sizeof(uint32_t))));
+  if (st == RNNLM_OK) chk(cuda_status(cudaMemset(h->bar, 0, 2 * sizeof(uint32_t))));
   if (st == RNNLM_OK) chk(cuda_status(cudaMemset(P.row_dst, 0xFF, B * sizeof(uint32_t))));
   if (st == RNNLM_OK) {
     st = rnnlm_reset_session(h, 0xFFFFFFFFu, nullptr);
@@ -412,6 +423,20 @@ int enqueue_step(rnnlm *h, const CallArgs &A, cudaStream_t s, bool timed) {
     for (int i = 0; i < NEV; ++i) ev.push_back(take_event(h));
     cudaEventRecord(ev[0], s);
   }
+  // a small frame on the AUTO path: the whole step is ONE cooperative kernel
+  if (h->gemv && h->cfg.gru_path == RNNLM_GRU_AUTO && A.n <= h->gemv_max_n &&
+      A.n <= rnnlm_host::small_max_queries()) {
+    const int k = rnnlm_host::launch_small(P, A, h->gemv, h->bar, h->num_sms, s);
+    cudaEventRecord(h->ev_join, s);                     // results ready (rnnlm_results_ready)
+    if (timed) {
+      cudaEventRecord(ev[1], s);
+      for (int i = 2; i < NEV; ++i) { h->ev_pool.push_back(ev[i]); ev[i] = nullptr; }
+      h->ev_pending.push_back({ev, true});
+      h->acc.calls += 1;
+      h->acc.launches += (uint64_t)(k > 0 ? k : 0);
+    }
+    return k > 0 ? k : 0;
+  }
   int k = 0;
   k += rnnlm_host::launch_cache_front(P, A, s);
   k += rnnlm_host::launch_commit(P, A, s);
@@ -442,7 +467,7 @@ int enqueue_step(rnnlm *h, const CallArgs &A, cudaStream_t s, bool timed) {
   cudaStreamWaitEvent(s, h->ev_join, 0);
   if (timed) {
     if (h->timing < 2) { h->ev_pool.push_back(ev[4]); ev[4] = nullptr; }
-    h->ev_pending.push_back(ev);
+    h->ev_pending.push_back({ev, false});
     h->acc.calls += 1;
     h->acc.launches += (uint64_t)k;
   }
@@ -645,23 +670,30 @@ rnnlm_status rnnlm_set_timing(rnnlm_t *h, int level) {
 rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset) {
   if (!h || !out) return RNNLM_E_INVALID_ARG;
   DeviceGuard dg(h);
-  for (auto &ev : h->ev_pending) {
-    cudaError_t e = cudaEventSynchronize(ev[6]);
-    if (!e) e = cudaEventSynchronize(ev[3]);
-    if (e) return cuda_status(e);
-    auto el = [](cudaEvent_t x, cudaEvent_t y) {
-      float ms = 0.0f;
-      cudaEventElapsedTime(&ms, x, y);
-      return (double)ms;
-    };
-    h->acc.ms_cache += el(ev[0], ev[1]);
-    h->acc.ms_final += el(ev[1], ev[2]);
-    h->acc.ms_score += el(ev[2], ev[3]);
-    h->acc.ms_gru += el(ev[1], ev[5]);
-    h->acc.ms_encode += el(ev[5], ev[6]);
-    if (ev[4]) {
-      h->acc.ms_gru_gather += el(ev[1], ev[4]);
-      h->acc.ms_gru_phase1 += el(ev[4], ev[5]);
+  auto el = [](cudaEvent_t x, cudaEvent_t y) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, x, y);
+    return (double)ms;
+  };
+  for (auto &pd : h->ev_pending) {
+    auto &ev = pd.ev;
+    if (pd.fused) {
+      const cudaError_t e = cudaEventSynchronize(ev[1]);
+      if (e) return cuda_status(e);
+      h->acc.ms_fused += el(ev[0], ev[1]);
+    } else {
+      cudaError_t e = cudaEventSynchronize(ev[6]);
+      if (!e) e = cudaEventSynchronize(ev[3]);
+      if (e) return cuda_status(e);
+      h->acc.ms_cache += el(ev[0], ev[1]);
+      h->acc.ms_final += el(ev[1], ev[2]);
+      h->acc.ms_score += el(ev[2], ev[3]);
+      h->acc.ms_gru += el(ev[1], ev[5]);
+      h->acc.ms_encode += el(ev[5], ev[6]);
+      if (ev[4]) {
+        h->acc.ms_gru_gather += el(ev[1], ev[4]);
+        h->acc.ms_gru_phase1 += el(ev[4], ev[5]);
+      }
     }
     for (cudaEvent_t e2 : ev)
       if (e2) h->ev_pool.push_back(e2);

@@ -31,231 +31,25 @@
 #include <cstring>
 #include <vector>
 
-#include "encode.cuh"
+#include "gemv.cuh"
 
 namespace rnnlm_gemv {
-using namespace rnnlm_dev;
 
-constexpr int U1 = 4;          // units per CTA, phase 1 (x 3 gates)
-constexpr int U2 = 8;          // units per CTA, phase 2
-constexpr int THREADS = 128;   // four warps; rows are dealt to warps
-enum { ACT_F32 = 0, ACT_BF16 = 1, ACT_TF32 = 2 };
-
-struct GemvArgs {
-  uint32_t E, H, RW;           // W1 / W2 row width (elements)
-  uint32_t tc_layout;          // 1: z row of unit u = (u/128)*256 + u%128, r = +128; 0: z = u, r = H + u
-  const void *w1, *w2;         // W1: z and r rows [Wz|Uz], [Wr|Ur]; W2: rows [Wh|Uh] (K-major, width RW)
-  const float *bz, *br, *bh;
-  const float *emb;            // V x E fp32
-  const __nv_bfloat16 *emb16;  // V x E bf16 (BF16)
-  float *state;
-  const uint32_t *row_src, *row_dst, *row_word, *counts;
-  float *gz, *grh, *gwxb;      // [rows][H] scratch
-  uint32_t *done;              // phase-2 CTAs finished (last one encodes; it resets the counter)
-  uint32_t cache, cstride;
-  KeySpec key;
-  uint8_t *codes;
-  unsigned long long *codehash;
-};
-
-__device__ __forceinline__ float sigm(float a) { return 1.0f / (1.0f + expf(-a)); }
-__device__ __forceinline__ float rnd_bf16(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
-__device__ __forceinline__ float rnd_tf32(float v) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-  return __uint_as_float(r);
-}
-template <int ACT>
-__device__ __forceinline__ float op(float v) {
-  if constexpr (ACT == ACT_BF16) return rnd_bf16(v);
-  else if constexpr (ACT == ACT_TF32) return rnd_tf32(v);
-  else return v;
-}
-
-// 8 consecutive elements of a weight row (bf16 or fp32 storage) as fp32
-template <typename WT>
-__device__ __forceinline__ void ld8(const WT *p, float *w) {
-  if constexpr (sizeof(WT) == 2) {
-    const uint4 t = __ldg(reinterpret_cast<const uint4 *>(p));
-    const uint32_t u[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      w[2 * j] = __uint_as_float(u[j] << 16);
-      w[2 * j + 1] = __uint_as_float(u[j] & 0xFFFF0000u);
-    }
-  } else {
-    const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
-    const float4 b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
-    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-  }
-}
-__device__ __forceinline__ void ld8f(const float *p, float *v) {
-  const float4 a = *reinterpret_cast<const float4 *>(p);
-  const float4 b = *(reinterpret_cast<const float4 *>(p) + 1);
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-}
-
-// Activation chunk c (8 elements) of row r's phase-1 operand [x | h], rounded
-// like the tile kernels' operands.
-template <int ACT>
-__device__ __forceinline__ void act8(const GemvArgs &g, uint32_t word, uint32_t src, uint32_t k, float *a) {
-  if (k < g.E) {
-    if constexpr (ACT == ACT_BF16) {
-      const uint4 t = __ldg(reinterpret_cast<const uint4 *>(g.emb16 + (size_t)word * g.E + k));
-      const uint32_t u[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        a[2 * j] = __uint_as_float(u[j] << 16);
-        a[2 * j + 1] = __uint_as_float(u[j] & 0xFFFF0000u);
-      }
-    } else {
-      const float4 *p = reinterpret_cast<const float4 *>(g.emb + (size_t)word * g.E + k);
-      const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
-      a[0] = x0.x; a[1] = x0.y; a[2] = x0.z; a[3] = x0.w; a[4] = x1.x; a[5] = x1.y; a[6] = x1.z; a[7] = x1.w;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) a[j] = op<ACT>(a[j]);
-    }
-  } else {
-    ld8f(g.state + (size_t)src * g.H + (k - g.E), a);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) a[j] = op<ACT>(a[j]);
-  }
-}
-
-__device__ __forceinline__ size_t z_row(const GemvArgs &g, uint32_t u) {
-  return g.tc_layout ? (size_t)(((u >> 7) << 8) + (u & 127)) : (size_t)u;
-}
-__device__ __forceinline__ size_t r_row(const GemvArgs &g, uint32_t u) {
-  return z_row(g, u) + (g.tc_layout ? 128u : g.H);
-}
-
-template <int N>
-__device__ __forceinline__ void warp_sum(float *v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < N; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-}
-
-// Phase 1: units [U1 * blockIdx.x, +U1) of rows blockIdx.y, +gridDim.y, ...
 template <typename WT, int ACT, int CELL>
 __global__ void __launch_bounds__(THREADS) k_gemv1(GemvArgs g) {
   pdl_entry();
-  const uint32_t Q = g.counts[1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t u0 = blockIdx.x * U1;
-  const uint32_t K1 = g.E + g.H, nch = K1 / 8, nchx = g.E / 8;
-  constexpr bool RNN = CELL == RNNLM_CELL_RNN;
-  const WT *w1 = static_cast<const WT *>(g.w1), *w2 = static_cast<const WT *>(g.w2);
-  for (uint32_t row = blockIdx.y * (THREADS / 32) + warp; row < Q; row += gridDim.y * (THREADS / 32)) {
-    const uint32_t word = g.row_word[row], src = g.row_src[row];
-    float acc[3 * U1];
-#pragma unroll
-    for (int i = 0; i < 3 * U1; ++i) acc[i] = 0.0f;
-    for (uint32_t c = lane; c < nch; c += 32) {
-      const uint32_t k = c * 8;
-      if (RNN && c >= nchx) break;                      // the RNN cell needs only Wh x here
-      float a[8];
-      act8<ACT>(g, word, src, k, a);
-#pragma unroll
-      for (int j = 0; j < U1; ++j) {
-        const uint32_t u = u0 + j;
-        float w[8];
-        if (!RNN) {
-          ld8(w1 + z_row(g, u) * g.RW + k, w);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[3 * j] = fmaf(a[e], w[e], acc[3 * j]);
-          ld8(w1 + r_row(g, u) * g.RW + k, w);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[3 * j + 1] = fmaf(a[e], w[e], acc[3 * j + 1]);
-        }
-        if (c < nchx) {
-          ld8(w2 + (size_t)u * g.RW + k, w);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[3 * j + 2] = fmaf(a[e], w[e], acc[3 * j + 2]);
-        }
-      }
-    }
-    warp_sum<3 * U1>(acc);
-    if (lane < U1) {
-      const uint32_t u = u0 + lane;
-      float sz = acc[0], sr = acc[1], sh = acc[2];
-#pragma unroll
-      for (int j = 1; j < U1; ++j)
-        if (lane == j) { sz = acc[3 * j]; sr = acc[3 * j + 1]; sh = acc[3 * j + 2]; }
-      const size_t o = (size_t)row * g.H + u;
-      g.gwxb[o] = sh + g.bh[u];
-      if (!RNN) {
-        const float z = sigm(sz + g.bz[u]), r = sigm(sr + g.br[u]);
-        g.gz[o] = z;
-        if (CELL == RNNLM_CELL_GRU_LBR) {
-          g.grh[o] = r;                                 // applied after Uh h
-        } else {
-          const float h = g.state[(size_t)src * g.H + u];
-          // r.h as the tile kernels form their phase-2 A operand
-          g.grh[o] = ACT == ACT_TF32 ? rnd_tf32(r * h) : op<ACT>(r * op<ACT>(h));
-        }
-      }
-    }
-  }
+  gemv1_item<WT, ACT, CELL>(g, g.counts[1], blockIdx.x, blockIdx.y, gridDim.y, threadIdx.x >> 5, THREADS / 32);
 }
 
-// Phase 2: units [U2 * blockIdx.x, +U2) of rows blockIdx.y, +gridDim.y, ...;
-// then the last CTA encodes every new state (one warp per row).
+// Phase 2, then the last CTA to finish (threadfence reduction pattern)
+// encodes every new state, one warp per row.
 template <typename WT, int ACT, int CELL>
 __global__ void __launch_bounds__(THREADS) k_gemv2(GemvArgs g) {
   pdl_entry();
   __shared__ uint32_t s_last;
   const uint32_t Q = g.counts[1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t u0 = blockIdx.x * U2;
-  const uint32_t nch = g.H / 8;
-  const WT *w2 = static_cast<const WT *>(g.w2);
-  for (uint32_t row = blockIdx.y * (THREADS / 32) + warp; row < Q; row += gridDim.y * (THREADS / 32)) {
-    const uint32_t dst = g.row_dst[row], src = g.row_src[row];
-    float acc[U2];
-#pragma unroll
-    for (int i = 0; i < U2; ++i) acc[i] = 0.0f;
-    for (uint32_t c = lane; c < nch; c += 32) {
-      const uint32_t k = c * 8;
-      float a[8];
-      if (CELL == RNNLM_CELL_GRU) {
-        ld8f(g.grh + (size_t)row * g.H + k, a);
-      } else {
-        ld8f(g.state + (size_t)src * g.H + k, a);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) a[e] = op<ACT>(a[e]);
-      }
-#pragma unroll
-      for (int j = 0; j < U2; ++j) {
-        float w[8];
-        ld8(w2 + (size_t)(u0 + j) * g.RW + g.E + k, w);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[j] = fmaf(a[e], w[e], acc[j]);
-      }
-    }
-    warp_sum<U2>(acc);
-    if (lane < U2 && dst != NONE) {
-      const uint32_t u = u0 + lane;
-      float s = acc[0];
-#pragma unroll
-      for (int j = 1; j < U2; ++j)
-        if (lane == j) s = acc[j];
-      const size_t o = (size_t)row * g.H + u;
-      float hn;
-      if (CELL == RNNLM_CELL_RNN) {
-        hn = sigm(g.gwxb[o] + s);
-      } else {
-        const float z = g.gz[o], h = g.state[(size_t)src * g.H + u];
-        const float c = tanhf(g.gwxb[o] + (CELL == RNNLM_CELL_GRU_LBR ? g.grh[o] * s : s));
-        hn = (1.0f - z) * h + z * c;
-      }
-      g.state[(size_t)dst * g.H + u] = hn;
-    }
-  }
+  gemv2_item<WT, ACT, CELL>(g, Q, blockIdx.x, blockIdx.y, gridDim.y, threadIdx.x >> 5, THREADS / 32);
   if (!g.cache) return;
-  // (a1) codes of the new states: the last CTA to finish (threadfence
-  // reduction pattern) encodes every row, one warp per row
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -265,13 +59,7 @@ __global__ void __launch_bounds__(THREADS) k_gemv2(GemvArgs g) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (uint32_t row = warp; row < Q; row += THREADS / 32) {
-    const uint32_t dst = g.row_dst[row];
-    if (dst == NONE) continue;
-    uint8_t *code = g.key.mode == RNNLM_KEY_OFF ? nullptr : g.codes + (size_t)dst * g.cstride;
-    const unsigned long long hs = encode_row_warp(g.key, g.cstride, g.state + (size_t)dst * g.H, code);
-    if (lane == 0) g.codehash[dst] = hs;
-  }
+  gemv_encode(g, Q, threadIdx.x >> 5, THREADS / 32);
   if (threadIdx.x == 0) *g.done = 0u;
 }
 
@@ -352,14 +140,26 @@ static void launch2(const GemvArgs &g, dim3 gr1, dim3 gr2, cudaStream_t s) {
   launch_pdl(k_gemv2<WT, ACT, CELL>, gr2, THREADS, 0, s, g);
 }
 
-// Rows per call are <= st->rows (checked by the caller).
-int launch_gemv(const Params &P, void *state, int num_sms, cudaStream_t s) {
+// The kernels' arguments for the engine's pools (k_small.cu uses them too).
+int gemv_args(void *state, const Params &P, GemvArgs *out, int *act) {
   GemvState *st = static_cast<GemvState *>(state);
+  if (!st) return -1;
   GemvArgs g = st->g;
   g.emb = P.emb; g.emb16 = P.emb16; g.state = P.state;
   g.row_src = P.row_src; g.row_dst = P.row_dst; g.row_word = P.row_word; g.counts = P.counts;
   g.cache = P.cache; g.cstride = P.cstride; g.codes = P.codes; g.codehash = P.codehash;
   g.key = KeySpec{P.key_mode, P.round_digits, P.H, P.round_scale};
+  *out = g;
+  *act = st->act;
+  return 0;
+}
+
+// Rows per call are <= st->rows (checked by the caller).
+int launch_gemv(const Params &P, void *state, int num_sms, cudaStream_t s) {
+  GemvState *st = static_cast<GemvState *>(state);
+  GemvArgs g;
+  int act = 0;
+  gemv_args(state, P, &g, &act);
   // unit blocks x row blocks: about two CTAs per SM, row blocks only as far as
   // the rows go (each row block re-reads its units' weights from L2)
   const uint32_t nb1 = P.H / U1, nb2 = P.H / U2;

@@ -89,7 +89,7 @@ def test_gemv_path_cells(math, cell):
     wl = generate_workload(1, 100, 256, d.V, seed=23, dur=(2, 6), eps=0.1)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=cell, path=GRU_GEMV)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
-    assert rep["miss"] > 200
+    assert rep["miss"] > (100 if cell == 2 else 200)       # RNN: positive states, sign codes merge
 
 
 @pytest.mark.parametrize("math", [MATH_BF16, MATH_TF32X3, MATH_FP32])

@@ -501,7 +501,9 @@ def test_rnn_cell_moderate(math):
     wl = lattice(1, 30, 256, d.V, seed=31)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=O.CELL_RNN)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
-    assert rep["miss"] > 200
+    # logistic states are all positive: every sign code is all ones, so a
+    # word's later queries all merge with its first (many SHITs, few MISSes)
+    assert rep["miss"] > 50 and rep["shit"] > 100
 
 
 def test_rnn_cell_large_full_tiles():
@@ -524,7 +526,7 @@ def test_fig4_hidden_sizes_tensor_core(H, cell, math):
     wl = lattice(1, 20, 300, d.V, seed=13)
     eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cell=cell)
     rep = replay_compare(eng, orc, wl, tol_score=TOL[math], tol_state=TOL[math])
-    assert rep["miss"] > 100
+    assert rep["miss"] > (30 if cell == O.CELL_RNN else 100)   # RNN: positive states, sign codes merge
 
 
 @pytest.mark.parametrize("pair_kernel", ["1", "0"])
