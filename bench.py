@@ -293,8 +293,9 @@ def measure_tf32_peak(dev):
         torch.backends.cuda.matmul.allow_tf32 = old
 
 
-def gru_peak(math, clk, peaks, tf32_peak):
-    """(peak, unit, bound, source) for the dominant kernel of `math`."""
+def gru_peak(math, clk, peaks, tf32_peak, x3_products=3):
+    """(peak, unit, bound, source) for the dominant kernel of `math`; 3xTF32:
+    the useful-flop peak = TF32 peak / tensor products per useful MAC."""
     burst = burst_clocks(clk)
     which = "burst" if burst else "sustained"
     bf16 = peaks.get("bf16_tflops" if burst else "bf16_tflops_sustained")
@@ -304,8 +305,10 @@ def gru_peak(math, clk, peaks, tf32_peak):
                 if burst else f"MEASURED_PEAKS bf16 ({which}: clocks below max or power-capped)"
         return 2250.0, "TFLOP/s", "tensor", "B200_PROFILING nominal dense bf16 (no measured peak)"
     if math in ("tf32", "tf32x3"):
-        div = 3.0 if math == "tf32x3" else 1.0
-        note = " / 3 (three TF32 products per useful multiply-add)" if math == "tf32x3" else ""
+        div = float(x3_products) if math == "tf32x3" else 1.0
+        note = (f" / {x3_products} (TF32 products per useful multiply-add"
+                + (": the a_hi.w_lo product is skipped, every weight is TF32-exact)" if x3_products == 2 else ")")
+                if math == "tf32x3" else "")
         if tf32_peak:
             return tf32_peak / div, "TFLOP/s", "tensor", f"cuBLAS TF32 8192^3 measured in this run (burst){note}"
         return (bf16 or 2250.0) * 0.5 / div, "TFLOP/s", "tensor", f"bf16 peak x 0.5 (nominal tf32/bf16){note}"
@@ -457,7 +460,7 @@ def step_summary(args, bench, res, world, peaks, tf32_peak):
     tc = math != "fp32"
     gemv = bench.n <= 512
     k_ms = (timing["ms_gru_phase1"] + timing["ms_gru_phase2"]) if (tc and not gemv) else timing["ms_gru"]
-    peak, unit, bound, src = gru_peak(math, res["clocks_B"], peaks, tf32_peak)
+    peak, unit, bound, src = gru_peak(math, res["clocks_B"], peaks, tf32_peak, bench.eng.tf32x3_products() or 3)
     achieved = flops / (k_ms / 1e3) / 1e12 if k_ms > 0 else 0.0
     pair = (math == "bf16" and args.cell == "gru" and dims.H % 256 == 0
             and os.environ.get("RNNLM_TC_PAIR", "1") != "0")
@@ -742,26 +745,31 @@ def run_configs(args, dev, peaks, tf32_peak):
                 ms_g, wall_g, _, _, _ = frame_loop(e, wl, dev, t_lo, F, use_graph=True)
                 del e
                 nq = wl.n_per_frame * (F - t_lo)
-                rows = st["gru_computations"]
-                # GEMV algorithmic bytes per frame: the gate weights once (L2-resident),
-                # the gathered x / h of every GRU row, its new state
+                rows = st["gru_computations"] / F
+                nonq = st["hidden_lookups"] / F
+                # algorithmic bytes of one small frame (SURVEY 8(d) per-query model): the gate
+                # weights once (L2-resident), per query 12 B in + 32 B probe + 8 B out, per
+                # non-QHIT query its score's row / state / bias / MaxEnt sectors + record,
+                # hidden probe and two inserts, per GRU row its x / h reads and new state
                 s_w = 2 if math == "bf16" else 4
                 wbytes = 3 * d.H * (d.E + d.H) * s_w
-                rbytes = rows / F * (d.E * s_w + 4 * d.H + 4 * d.H)
-                gemv_ms = tm["ms_gru"] / max(1, tm["calls"])
-                gbs = (wbytes + rbytes) / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None
+                fbytes = (wbytes + wl.n_per_frame * 52 + nonq * (d.H * s_w + 4 * d.H + 32 + 32 * d.N + 128)
+                          + rows * (d.E * s_w + 8 * d.H))
+                fused_ms = tm["ms_fused"] / max(1, tm["calls"])
+                gbs = fbytes / (fused_ms * 1e-3) / 1e9 if fused_ms > 0 else None
                 res[f"{math}/{key}"] = {
                     "q_per_s": nq / (ms * 1e-3), "us_per_frame": 1e3 * ms / (F - t_lo),
                     "q_per_s_wall": nq / wall, "us_per_frame_wall": 1e6 * wall / (F - t_lo),
                     "graph": {"q_per_s": nq / (ms_g * 1e-3), "us_per_frame": 1e3 * ms_g / (F - t_lo),
                               "us_per_frame_wall": 1e6 * wall_g / (F - t_lo)},
                     "query_cache_hit": st["query_hits"] / max(1, st["total_queries"]),
-                    "hidden_hits": st["hidden_hits"], "gru_rows_per_frame": rows / F,
-                    "gemv": {"kernels": "k_gemv1 + k_gemv2", "us_per_frame": 1e3 * gemv_ms,
-                             "algorithmic_bytes_per_frame": wbytes + rbytes, "achieved_gbs": gbs,
-                             "hbm_peak_gbs": hbm, "frac_of_hbm": (gbs / hbm) if gbs else None,
-                             "note": "latency-bound: the frame's weights (L2-resident) and rows take a few "
-                                     "dependent L2 round trips; bytes/s is far below HBM bandwidth"},
+                    "hidden_hits": st["hidden_hits"], "gru_rows_per_frame": rows,
+                    "fused_kernel": {"kernel": "k_small (whole step, one cooperative launch; GEMV GRU)",
+                                     "us_per_frame": 1e3 * fused_ms, "algorithmic_bytes_per_frame": fbytes,
+                                     "achieved_gbs": gbs, "hbm_peak_gbs": hbm,
+                                     "frac_of_hbm": (gbs / hbm) if gbs else None,
+                                     "note": "latency-bound: ~1 MB per frame through seven grid-barrier phases "
+                                             "of dependent L2 round trips; bytes/s is far below HBM bandwidth"},
                 }
         out[name] = {"streams": 1, "queries_per_frame": wl.n_per_frame, "frames": F,
                      "timed_frames": f"{t_lo}..{F - 1}", "V": d.V, "H": d.H, "results": res}

@@ -19,6 +19,7 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int
 void gru_tc_release(void *state);
 int gru_tc_bind(void *state, void *rh, uint32_t bmax);
 int gru_tc_weights(void *state, const void **w1, const void **w2, uint32_t *rw);
+int gru_tc_x3_products(void *state);
 // Small-frame GEMV path (k_gemv.cu).
 int gemv_prepare(const Params &P, const rnnlm_weights *w, uint32_t math, const void *tc_w1, const void *tc_w2,
                  uint32_t tc_rw, uint32_t rows, void **state_out);
@@ -198,6 +199,7 @@ const char *rnnlm_status_string(rnnlm_status s) {
 
 uint32_t rnnlm_code_bytes(const rnnlm_t *h) { return h ? h->P.code_bytes : 0; }
 uint64_t rnnlm_launch_count(const rnnlm_t *h) { return h ? h->launches : 0; }
+int rnnlm_tf32x3_products(const rnnlm_t *h) { return h && h->tc ? rnnlm_host::gru_tc_x3_products(h->tc) : 0; }
 
 rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm_t **out) {
   if (!out) return RNNLM_E_INVALID_ARG;

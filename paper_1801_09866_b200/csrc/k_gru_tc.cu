@@ -146,6 +146,8 @@ struct TcArgs {
   // (z | r | Wh x | Uh h), B = W3 [(H/64) x 192 rows][E+H]
   const float *bz, *br;            // [H] (LBR epilogue)
   uint32_t bn2;                    // units per phase-2 (and RNN) tile: 256, or 128 when H % 256 != 0
+  uint32_t x3_wlo;                 // 3xTF32: 1 = run the A_hi.W_lo segment; 0 = every weight is TF32-exact
+                                   // (W_lo == 0), so that product is identically zero and is skipped
   uint32_t x3;                     // RNNLM_MATH_TF32X3 (TF32 instance only): operands as [hi | lo] TF32 parts,
                                    // three K segments hi.hi, hi.lo, lo.hi (A1 2(E+H), r.h 2H, W 2(E+H) wide)
   // (a1) compression of the new state, fused into the phase-2 epilogue
@@ -710,7 +712,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   constexpr bool LBR = CELL == RNNLM_CELL_GRU_LBR, RNN = CELL == RNNLM_CELL_RNN;
   const uint32_t n1 = LBR ? a.H / 64 : (RNN ? a.H / a.bn2 : a.nub), n2 = (LBR || RNN) ? 0u : a.H / a.bn2;
   constexpr int BKE = Op<T>::BKE;
-  const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE, KCt = a.x3 ? 3 * KC : KC;
+  const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE, KCt = a.x3 ? (a.x3_wlo ? 3 : 2) * KC : KC;
   const uint32_t target = n1 * EPI_WARPS;               // phase-1 arrivals per M-tile
   if (threadIdx.x == 0) {
     prefetch_map(&map_a1); prefetch_map(&map_w1); prefetch_map(&map_rh); prefetch_map(&map_w2);
@@ -748,7 +750,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
         if (prof) prof[9 + x.kind] += 1;
         for (uint32_t kc3 = 0; kc3 < KCt; ++kc3) {
           // 3xTF32: segment 0 = A_hi.W_hi, 1 = A_hi.W_lo, 2 = A_lo.W_hi (column offsets of the lo parts)
-          const uint32_t seg = a.x3 ? kc3 / KC : 0u, kc = a.x3 ? kc3 % KC : kc3;
+          uint32_t seg = a.x3 ? kc3 / KC : 0u;
+          const uint32_t kc = a.x3 ? kc3 % KC : kc3;
+          if (seg == 1 && !a.x3_wlo) seg = 2;                // W_lo == 0: hi.hi and lo.hi only
           const int a_off = seg == 2 ? (int)(a.E + a.H) : 0, b_off = seg == 1 ? (int)(a.E + a.H) : 0;
           const int rh_off = seg == 2 ? (int)a.H : 0;
           t0 = clock64();
@@ -1170,6 +1174,7 @@ struct TcState {
   unsigned long long *prof = nullptr;
   float *bzr = nullptr, *bh = nullptr;
   bool x3 = false;                 // RNNLM_MATH_TF32X3: [hi | lo] operand rows, three K segments
+  bool x3_wlo = true;              // some weight is not TF32-exact (its W_lo part is non-zero)
   bool lbr = false;                // cell GRU_LBR: one-phase tiles over W3
   bool rnn = false;                // cell RNN: one-phase tiles over W2 = [Wh | Uh]
   void *w3 = nullptr;
@@ -1239,12 +1244,16 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
   };
   const float *Wg[2] = {w->Wz, w->Wr};
   const float *Ug[2] = {w->Uz, w->Ur};
+  bool any_lo = false;
   // one weight into (row, k): its (TF32 / bf16) value, and with 3xTF32 the
   // TF32 part of the remainder at k + K1
   auto put = [&](T *row, size_t k, float v) {
     row[k] = cv(v);
     if constexpr (sizeof(T) == 4)
-      if (t->x3) row[K1 + k] = cv(v - (float)row[k]);
+      if (t->x3) {
+        row[K1 + k] = cv(v - (float)row[k]);
+        if ((float)row[K1 + k] != 0.0f) any_lo = true;
+      }
   };
   for (size_t u = 0; u < H; ++u) {
     const size_t ub = u / UB, uu = u % UB;
@@ -1257,6 +1266,7 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
     for (size_t k = 0; k < E; ++k) put(row2, k, w->Wh[u * E + k]);
     for (size_t k = 0; k < H; ++k) put(row2, E + k, w->Uh[u * H + k]);
   }
+  t->x3_wlo = any_lo;
   return cudaMalloc(&t->w1, w1.size() * sizeof(T)) == cudaSuccess &&
          cudaMalloc(&t->w2, w2.size() * sizeof(T)) == cudaSuccess &&
          cudaMemcpy(t->w1, w1.data(), w1.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess &&
@@ -1347,6 +1357,14 @@ int gru_tc_weights(void *state, const void **w1, const void **w2, uint32_t *rw) 
   return 0;
 }
 
+// Tensor-core products per useful multiply-add of the 3xTF32 mode: 3, or 2
+// when every weight is TF32-exact (0 for the other modes).
+int gru_tc_x3_products(void *state) {
+  TcState *t = static_cast<TcState *>(state);
+  if (!t || !t->x3) return 0;
+  return (t->x3_wlo || getenv("RNNLM_TF32X3_ALL_SEGMENTS")) ? 3 : 2;
+}
+
 void gru_tc_release(void *state) {
   TcState *t = static_cast<TcState *>(state);
   if (!t) return;
@@ -1389,6 +1407,8 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.bz = t->bz; a.br = t->br;
   a.bn2 = P.H % BN ? UB : BN;
   a.x3 = t->x3 ? 1u : 0u;
+  a.x3_wlo = t->x3_wlo ? 1u : 0u;
+  if (getenv("RNNLM_TF32X3_ALL_SEGMENTS")) a.x3_wlo = 1u;   // (A/B) run the zero A_hi.W_lo segment anyway
   a.prof = nullptr;
   if (t->diag == 5) {
     if (!t->prof) cudaMalloc(&t->prof, 1024 * 16 * sizeof(unsigned long long));

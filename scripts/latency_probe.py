@@ -24,7 +24,8 @@ dev = torch.device("cuda", 0)
 d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
 d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
 d_ref = torch.as_tensor(wl.parent_ref, device=dev)
-for path in ([R.GRU_TILES, R.GRU_GEMV] if d.H % 128 == 0 or math == R.MATH_FP32 else [R.GRU_GEMV]):
+for path in ([R.GRU_AUTO, R.GRU_TILES, R.GRU_GEMV] if d.H % 128 == 0 or math == R.MATH_FP32
+             else [R.GRU_AUTO, R.GRU_GEMV]):
     for use_graph in (False, True):
         eng = R.RNNLM.from_dims(d, m, key_mode=R.KEY_SIGN, math=math, num_sessions=1, max_queries_per_call=n,
                                 max_histories_per_session=wl.max_histories_hint(), gru_path=path)
@@ -57,7 +58,7 @@ for path in ([R.GRU_TILES, R.GRU_GEMV] if d.H % 128 == 0 or math == R.MATH_FP32 
         wall = time.perf_counter() - t0
         F = wl.frames - 40
         print(json.dumps({"config": cfg, "math": sys.argv[2] if len(sys.argv) > 2 else "bf16",
-                          "path": {R.GRU_TILES: "tiles", R.GRU_GEMV: "gemv"}[path], "graph": use_graph,
+                          "path": {R.GRU_AUTO: "auto (fused when n <= 512)", R.GRU_TILES: "tiles", R.GRU_GEMV: "gemv"}[path], "graph": use_graph,
                           "us_per_frame_gpu": 1e3 * a.elapsed_time(b) / F, "us_per_frame_wall": 1e6 * wall / F,
                           "q_per_s": n * F / wall, "stats": eng.cache_stats()}), flush=True)
         del g, eng

@@ -608,3 +608,33 @@ def test_results_ready_before_state_update():
         assert np.array_equal(early_sc.numpy().view(np.uint32), sc.cpu().numpy().view(np.uint32))
         assert np.array_equal(early_ch.numpy(), ch.cpu().numpy())
         child[sl] = ch.cpu().numpy().view(np.uint32)
+
+
+def test_tf32x3_skips_zero_weight_lo_segment(monkeypatch):
+    """bf16-grid weights are TF32-exact, so the 3xTF32 A_hi.W_lo product is
+    identically zero and the engine runs two products; running the third
+    anyway (RNNLM_TF32X3_ALL_SEGMENTS) only adds exact zeros: bitwise the
+    same scores and states.  Off-grid weights keep all three."""
+    d, m = model("moderate")
+    wl = lattice(1, 12, 256, d.V, seed=5)
+    outs = []
+    for allseg in (False, True):
+        if allseg:
+            monkeypatch.setenv("RNNLM_TF32X3_ALL_SEGMENTS", "1")
+        eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_TF32X3)
+        assert eng.tf32x3_products() == (3 if allseg else 2)
+        child = np.zeros(wl.n_total, np.uint32)
+        score = np.zeros(wl.n_total, np.float32)
+        for t in range(wl.frames):
+            sl = wl.frame_slice(t)
+            par = O.resolve_parents(wl.parent_ref[sl], child)
+            s_, c_, _ = eng.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]))
+            score[sl], child[sl] = s_.cpu().numpy(), c_.cpu().numpy().view(np.uint32)
+        outs.append((score, eng.read_states(0, child).cpu().numpy()))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
+    monkeypatch.delenv("RNNLM_TF32X3_ALL_SEGMENTS")
+    d2 = ModelDims(V=1000, E=256, H=256, maxent_log2=16, N=3)
+    m2 = generate_model(d2, seed=3, scale=0.1, bf16_grid=False)
+    eng2 = RNNLM.from_dims(d2, m2, math=MATH_TF32X3, max_queries_per_call=8, max_histories_per_session=8)
+    assert eng2.tf32x3_products() == 3
