@@ -306,9 +306,8 @@ def gru_peak(math, clk, peaks, tf32_peak, x3_products=3):
         return 2250.0, "TFLOP/s", "tensor", "B200_PROFILING nominal dense bf16 (no measured peak)"
     if math in ("tf32", "tf32x3"):
         div = float(x3_products) if math == "tf32x3" else 1.0
-        note = (f" / {x3_products} (TF32 products per useful multiply-add"
-                + (": the a_hi.w_lo product is skipped, every weight is TF32-exact)" if x3_products == 2 else ")")
-                if math == "tf32x3" else "")
+        note = (f" / {x3_products:g} (TF32 products per useful multiply-add; identically-zero products "
+                "of TF32-exact weights / embeddings are skipped)" if math == "tf32x3" else "")
         if tf32_peak:
             return tf32_peak / div, "TFLOP/s", "tensor", f"cuBLAS TF32 8192^3 measured in this run (burst){note}"
         return (bf16 or 2250.0) * 0.5 / div, "TFLOP/s", "tensor", f"bf16 peak x 0.5 (nominal tf32/bf16){note}"

@@ -87,9 +87,10 @@ typedef enum {
   RNNLM_MATH_TF32X3 = 3     /* fp32-accurate on tcgen05: a = a_hi + a_lo, w = w_hi + w_lo (TF32 parts),
                              * a.w ~ a_hi.w_hi + a_hi.w_lo + a_lo.w_hi (three TF32 products, fp32
                              * accumulation; the 1e-5 path of the FP32 mode at tensor-core rate).
-                             * When every gate weight is TF32-exact (w_lo == 0) the a_hi.w_lo
-                             * product is identically zero and is not computed (two products;
-                             * rnnlm_tf32x3_products). */
+                             * Products that are identically zero are not computed: a_hi.w_lo when
+                             * every gate weight is TF32-exact (w_lo == 0), a_lo.w_hi over the
+                             * embedding part of K when every embedding entry is (x_lo == 0);
+                             * rnnlm_tf32x3_products reports what remains. */
   /* The two tensor-core modes need E % 64 == 0 and H % 128 == 0 (else
    * rnnlm_create returns RNNLM_E_DIMENSION).  BF16 stores bf16 copies of E
    * and the gate weights (and of nce_w when every entry is bf16-exact); TF32
@@ -276,8 +277,9 @@ rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset);
 /* Kernels launched by this handle since create (host-side count). */
 uint64_t rnnlm_launch_count(const rnnlm_t *h);
 /* RNNLM_MATH_TF32X3 engines: tensor-core products per useful multiply-add of
- * the gate contraction (3, or 2 when the weights are TF32-exact); else 0. */
-int rnnlm_tf32x3_products(const rnnlm_t *h);
+ * the gate contraction (3 less the skipped zero products, e.g. 1.5 with
+ * TF32-exact weights and embeddings at E = H); else 0. */
+double rnnlm_tf32x3_products(const rnnlm_t *h);
 const char *rnnlm_status_string(rnnlm_status s);
 int rnnlm_abi_version(void);
 

@@ -75,7 +75,7 @@ SIGNATURES = {
                                           ctypes.POINTER(_vp)]),
     "rnnlm_graph_launch": (ctypes.c_int, [_vp, _vp]),
     "rnnlm_graph_destroy": (None, [_vp]),
-    "rnnlm_tf32x3_products": (ctypes.c_int, [_vp]),
+    "rnnlm_tf32x3_products": (ctypes.c_double, [_vp]),
 }
 
 _lib = None

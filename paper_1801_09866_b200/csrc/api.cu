@@ -15,11 +15,12 @@ namespace rnnlm_host {
 // Tensor-core path (k_gru_tc.cu).  Returns kernels launched, or -1 if the
 // configuration is not supported by it.
 int gru_tc_supported(uint32_t E, uint32_t H);
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int x3, int cell, void **state_out);
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t V, uint32_t E, uint32_t H, int tf32, int x3, int cell,
+                   void **state_out);
 void gru_tc_release(void *state);
 int gru_tc_bind(void *state, void *rh, uint32_t bmax);
 int gru_tc_weights(void *state, const void **w1, const void **w2, uint32_t *rw);
-int gru_tc_x3_products(void *state);
+double gru_tc_x3_products(void *state);
 // Small-frame GEMV path (k_gemv.cu).
 int gemv_prepare(const Params &P, const rnnlm_weights *w, uint32_t math, const void *tc_w1, const void *tc_w2,
                  uint32_t tc_rw, uint32_t rows, void **state_out);
@@ -199,7 +200,7 @@ const char *rnnlm_status_string(rnnlm_status s) {
 
 uint32_t rnnlm_code_bytes(const rnnlm_t *h) { return h ? h->P.code_bytes : 0; }
 uint64_t rnnlm_launch_count(const rnnlm_t *h) { return h ? h->launches : 0; }
-int rnnlm_tf32x3_products(const rnnlm_t *h) { return h && h->tc ? rnnlm_host::gru_tc_x3_products(h->tc) : 0; }
+double rnnlm_tf32x3_products(const rnnlm_t *h) { return h && h->tc ? rnnlm_host::gru_tc_x3_products(h->tc) : 0.0; }
 
 rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm_t **out) {
   if (!out) return RNNLM_E_INVALID_ARG;
@@ -298,7 +299,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
     if (c.math == RNNLM_MATH_BF16)
       chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.emb16), w->emb, V * E));
     if (st == RNNLM_OK &&
-        rnnlm_host::gru_tc_prepare(w, c.embed, c.hidden, c.math == RNNLM_MATH_TF32 || c.math == RNNLM_MATH_TF32X3,
+        rnnlm_host::gru_tc_prepare(w, c.vocab, c.embed, c.hidden, c.math == RNNLM_MATH_TF32 || c.math == RNNLM_MATH_TF32X3,
                                    c.math == RNNLM_MATH_TF32X3,
                                    (int)c.cell, &h->tc) != 0)
       st = RNNLM_E_OOM;

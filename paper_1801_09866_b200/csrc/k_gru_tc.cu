@@ -148,6 +148,8 @@ struct TcArgs {
   uint32_t bn2;                    // units per phase-2 (and RNN) tile: 256, or 128 when H % 256 != 0
   uint32_t x3_wlo;                 // 3xTF32: 1 = run the A_hi.W_lo segment; 0 = every weight is TF32-exact
                                    // (W_lo == 0), so that product is identically zero and is skipped
+  uint32_t x3_xlo;                 // 3xTF32: 1 = run A_lo.W_hi over the x part of K; 0 = every embedding
+                                   // entry is TF32-exact (x_lo == 0): A_lo.W_hi covers the h part only
   uint32_t x3;                     // RNNLM_MATH_TF32X3 (TF32 instance only): operands as [hi | lo] TF32 parts,
                                    // three K segments hi.hi, hi.lo, lo.hi (A1 2(E+H), r.h 2H, W 2(E+H) wide)
   // (a1) compression of the new state, fused into the phase-2 epilogue
@@ -227,7 +229,8 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
           const float4 v = i < nx ? __ldg(x + i) : h[i - nx];
           const float4 hi = to_tf32(v);
           dst[i] = hi;
-          dst[nk + i] = to_tf32(make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w));
+          if (i >= nx || a.x3_xlo)                       // x_lo == 0 is never read (skipped segment)
+            dst[nk + i] = to_tf32(make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w));
         }
       }
     }
@@ -712,7 +715,10 @@ __global__ void __maxnreg__(GRU_MAXREG)
   constexpr bool LBR = CELL == RNNLM_CELL_GRU_LBR, RNN = CELL == RNNLM_CELL_RNN;
   const uint32_t n1 = LBR ? a.H / 64 : (RNN ? a.H / a.bn2 : a.nub), n2 = (LBR || RNN) ? 0u : a.H / a.bn2;
   constexpr int BKE = Op<T>::BKE;
-  const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE, KCt = a.x3 ? (a.x3_wlo ? 3 : 2) * KC : KC;
+  const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE;
+  // 3xTF32 K-chunk list: A_hi.W_hi over all of K, A_hi.W_lo over all of K
+  // (unless W_lo == 0), A_lo.W_hi from chunk k2 (the x part is skipped when x_lo == 0)
+  const uint32_t k2 = a.x3_xlo ? 0u : kx, KCt = a.x3 ? KC + (a.x3_wlo ? KC : 0u) + (KC - k2) : KC;
   const uint32_t target = n1 * EPI_WARPS;               // phase-1 arrivals per M-tile
   if (threadIdx.x == 0) {
     prefetch_map(&map_a1); prefetch_map(&map_w1); prefetch_map(&map_rh); prefetch_map(&map_w2);
@@ -750,9 +756,11 @@ __global__ void __maxnreg__(GRU_MAXREG)
         if (prof) prof[9 + x.kind] += 1;
         for (uint32_t kc3 = 0; kc3 < KCt; ++kc3) {
           // 3xTF32: segment 0 = A_hi.W_hi, 1 = A_hi.W_lo, 2 = A_lo.W_hi (column offsets of the lo parts)
-          uint32_t seg = a.x3 ? kc3 / KC : 0u;
-          const uint32_t kc = a.x3 ? kc3 % KC : kc3;
-          if (seg == 1 && !a.x3_wlo) seg = 2;                // W_lo == 0: hi.hi and lo.hi only
+          uint32_t seg = 0, kc = kc3;
+          if (a.x3 && kc3 >= KC) {
+            if (a.x3_wlo && kc3 < 2 * KC) { seg = 1; kc = kc3 - KC; }
+            else { seg = 2; kc = k2 + kc3 - KC - (a.x3_wlo ? KC : 0u); }
+          }
           const int a_off = seg == 2 ? (int)(a.E + a.H) : 0, b_off = seg == 1 ? (int)(a.E + a.H) : 0;
           const int rh_off = seg == 2 ? (int)a.H : 0;
           t0 = clock64();
@@ -1175,6 +1183,7 @@ struct TcState {
   float *bzr = nullptr, *bh = nullptr;
   bool x3 = false;                 // RNNLM_MATH_TF32X3: [hi | lo] operand rows, three K segments
   bool x3_wlo = true;              // some weight is not TF32-exact (its W_lo part is non-zero)
+  bool x3_xlo = true;              // some embedding entry is not TF32-exact
   bool lbr = false;                // cell GRU_LBR: one-phase tiles over W3
   bool rnn = false;                // cell RNN: one-phase tiles over W2 = [Wh | Uh]
   void *w3 = nullptr;
@@ -1273,10 +1282,19 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
          cudaMemcpy(t->w2, w2.data(), w2.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
 }
 
-int gru_tc_prepare(const rnnlm_weights *w, uint32_t E, uint32_t H, int tf32, int x3, int cell, void **state_out) {
+int gru_tc_prepare(const rnnlm_weights *w, uint32_t V, uint32_t E, uint32_t H, int tf32, int x3, int cell,
+                   void **state_out) {
   *state_out = nullptr;
   TcState *t = new TcState;
   t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0; t->x3 = x3 != 0 && t->tf32;
+  if (t->x3) {                    // is every embedding entry TF32-exact (low 13 mantissa bits zero)?
+    t->x3_xlo = false;
+    for (size_t i = 0; i < (size_t)E * V; ++i) {
+      uint32_t b;
+      std::memcpy(&b, &w->emb[i], 4);
+      if (b & 0x1FFFu) { t->x3_xlo = true; break; }
+    }
+  }
   t->lbr = cell == RNNLM_CELL_GRU_LBR;
   t->rnn = cell == RNNLM_CELL_RNN;
   // the CTA pair (cta_group::2) is the default for the bf16 GRU: ~1.3 % faster kernel
@@ -1357,12 +1375,14 @@ int gru_tc_weights(void *state, const void **w1, const void **w2, uint32_t *rw) 
   return 0;
 }
 
-// Tensor-core products per useful multiply-add of the 3xTF32 mode: 3, or 2
-// when every weight is TF32-exact (0 for the other modes).
-int gru_tc_x3_products(void *state) {
+// Tensor-core products per useful multiply-add of the 3xTF32 mode: 3, less
+// the skipped identically-zero ones (0 for the other modes).
+double gru_tc_x3_products(void *state) {
   TcState *t = static_cast<TcState *>(state);
-  if (!t || !t->x3) return 0;
-  return (t->x3_wlo || getenv("RNNLM_TF32X3_ALL_SEGMENTS")) ? 3 : 2;
+  if (!t || !t->x3) return 0.0;
+  const bool all = getenv("RNNLM_TF32X3_ALL_SEGMENTS") != nullptr;
+  const double K = t->E + t->H;
+  return (K + ((t->x3_wlo || all) ? K : 0.0) + ((t->x3_xlo || all) ? K : (double)t->H)) / K;
 }
 
 void gru_tc_release(void *state) {
@@ -1408,7 +1428,8 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.bn2 = P.H % BN ? UB : BN;
   a.x3 = t->x3 ? 1u : 0u;
   a.x3_wlo = t->x3_wlo ? 1u : 0u;
-  if (getenv("RNNLM_TF32X3_ALL_SEGMENTS")) a.x3_wlo = 1u;   // (A/B) run the zero A_hi.W_lo segment anyway
+  a.x3_xlo = t->x3_xlo ? 1u : 0u;
+  if (getenv("RNNLM_TF32X3_ALL_SEGMENTS")) a.x3_wlo = a.x3_xlo = 1u;   // (A/B) run the zero products anyway
   a.prof = nullptr;
   if (t->diag == 5) {
     if (!t->prof) cudaMalloc(&t->prof, 1024 * 16 * sizeof(unsigned long long));

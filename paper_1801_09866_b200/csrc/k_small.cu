@@ -25,6 +25,7 @@
 // the same claim / barrier / read order, so results are bit-identical to that
 // path with the GEMV GRU kernels (tests/test_gpu_small.py).
 #include <cstdint>
+#include <cstdlib>
 
 #include "cache.cuh"
 #include "gemv.cuh"
@@ -35,6 +36,9 @@ using namespace rnnlm_dev;
 using namespace rnnlm_gemv;
 
 constexpr int SMALL_THREADS = 256;
+#ifndef RNNLM_SMALL_CTAS
+#define RNNLM_SMALL_CTAS 148
+#endif
 constexpr int SI = 2;                  // scan items per thread
 constexpr uint32_t MAX_N = SMALL_THREADS * SI;
 static_assert(MAX_N >= RNNLM_GEMV_AUTO_MAX_QUERIES, "the fused kernel takes every AUTO-path GEMV call");
@@ -47,6 +51,9 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+#ifndef RNNLM_SMALL_SLEEP
+#define RNNLM_SMALL_SLEEP 0
+#endif
 __device__ __forceinline__ void grid_sync(uint32_t *bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -57,7 +64,9 @@ __device__ __forceinline__ void grid_sync(uint32_t *bar) {
       __threadfence();
       atomicAdd(bar + 1, 1u);
     } else {
-      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
+      while (ld_acquire_u32(bar + 1) == gen) {
+        if (RNNLM_SMALL_SLEEP) __nanosleep(RNNLM_SMALL_SLEEP);
+      }
     }
     __threadfence();
   }
@@ -174,8 +183,11 @@ int launch_small(const Params &P, const CallArgs &A, void *gemv_state, uint32_t 
   rnnlm_gemv::GemvArgs g;
   int act = 0;
   if (gemv_args(gemv_state, P, &g, &act) != 0) return -1;
-  // one CTA per SM; GEMV work items: unit blocks x row blocks (~ one per CTA)
-  const uint32_t grid = (uint32_t)num_sms;
+  // CTAs (<= one per SM, co-resident); GEMV work items: unit blocks x row
+  // blocks (~ one per CTA).  RNNLM_SMALL_GRID overrides (A/B).
+  static const int grid_env = getenv("RNNLM_SMALL_GRID") ? atoi(getenv("RNNLM_SMALL_GRID")) : 0;
+  uint32_t grid = grid_env > 0 ? (uint32_t)grid_env : (uint32_t)RNNLM_SMALL_CTAS;
+  if (grid > (uint32_t)num_sms) grid = (uint32_t)num_sms;
   const uint32_t nb1 = P.H / U1, nb2 = P.H / U2, rmax = (A.n + 7) / 8;
   uint32_t rb1 = (grid + nb1 - 1) / nb1, rb2 = (grid + nb2 - 1) / nb2;
   rb1 = rb1 < rmax ? rb1 : rmax; rb2 = rb2 < rmax ? rb2 : rmax;

@@ -179,10 +179,10 @@ class RNNLM:
     def launch_count(self) -> int:
         return int(_lib.load().rnnlm_launch_count(self._h))
 
-    def tf32x3_products(self) -> int:
-        """3xTF32 engines: tensor-core products per useful multiply-add (3, or 2
-        with TF32-exact weights); 0 otherwise."""
-        return int(_lib.load().rnnlm_tf32x3_products(self._h))
+    def tf32x3_products(self) -> float:
+        """3xTF32 engines: tensor-core products per useful multiply-add (3 less
+        the identically-zero ones skipped); 0 otherwise."""
+        return float(_lib.load().rnnlm_tf32x3_products(self._h))
 
 
 class StepGraph:

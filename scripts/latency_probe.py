@@ -24,8 +24,11 @@ dev = torch.device("cuda", 0)
 d_sess = torch.as_tensor(wl.session.view(np.int32), device=dev)
 d_word = torch.as_tensor(wl.word.view(np.int32), device=dev)
 d_ref = torch.as_tensor(wl.parent_ref, device=dev)
-for path in ([R.GRU_AUTO, R.GRU_TILES, R.GRU_GEMV] if d.H % 128 == 0 or math == R.MATH_FP32
-             else [R.GRU_AUTO, R.GRU_GEMV]):
+paths = ([R.GRU_AUTO, R.GRU_TILES, R.GRU_GEMV] if d.H % 128 == 0 or math == R.MATH_FP32
+         else [R.GRU_AUTO, R.GRU_GEMV])
+if len(sys.argv) > 3:
+    paths = [{"auto": R.GRU_AUTO, "tiles": R.GRU_TILES, "gemv": R.GRU_GEMV}[sys.argv[3]]]
+for path in paths:
     for use_graph in (False, True):
         eng = R.RNNLM.from_dims(d, m, key_mode=R.KEY_SIGN, math=math, num_sessions=1, max_queries_per_call=n,
                                 max_histories_per_session=wl.max_histories_hint(), gru_path=path)

@@ -611,10 +611,11 @@ def test_results_ready_before_state_update():
 
 
 def test_tf32x3_skips_zero_weight_lo_segment(monkeypatch):
-    """bf16-grid weights are TF32-exact, so the 3xTF32 A_hi.W_lo product is
-    identically zero and the engine runs two products; running the third
-    anyway (RNNLM_TF32X3_ALL_SEGMENTS) only adds exact zeros: bitwise the
-    same scores and states.  Off-grid weights keep all three."""
+    """bf16-grid weights and embeddings are TF32-exact, so the 3xTF32 A_hi.W_lo
+    product and A_lo.W_hi over the embedding part of K are identically zero
+    and are skipped (1.5 products per MAC at E = H); running them anyway
+    (RNNLM_TF32X3_ALL_SEGMENTS) only adds exact zeros: bitwise the same scores
+    and states.  Off-grid weights keep all three."""
     d, m = model("moderate")
     wl = lattice(1, 12, 256, d.V, seed=5)
     outs = []
@@ -622,7 +623,7 @@ def test_tf32x3_skips_zero_weight_lo_segment(monkeypatch):
         if allseg:
             monkeypatch.setenv("RNNLM_TF32X3_ALL_SEGMENTS", "1")
         eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_TF32X3)
-        assert eng.tf32x3_products() == (3 if allseg else 2)
+        assert eng.tf32x3_products() == (3.0 if allseg else 1.5)   # E = H: (K + H) / K
         child = np.zeros(wl.n_total, np.uint32)
         score = np.zeros(wl.n_total, np.float32)
         for t in range(wl.frames):
@@ -637,4 +638,4 @@ def test_tf32x3_skips_zero_weight_lo_segment(monkeypatch):
     d2 = ModelDims(V=1000, E=256, H=256, maxent_log2=16, N=3)
     m2 = generate_model(d2, seed=3, scale=0.1, bf16_grid=False)
     eng2 = RNNLM.from_dims(d2, m2, math=MATH_TF32X3, max_queries_per_call=8, max_histories_per_session=8)
-    assert eng2.tf32x3_products() == 3
+    assert eng2.tf32x3_products() == 3.0
