@@ -172,6 +172,22 @@ __device__ __forceinline__ void gemv1_item(const GemvArgs &g, uint32_t Q, uint32
   }
 }
 
+// L1 prefetch of unit block ub's phase-1 weight rows (128-byte lines), so a
+// CTA that waits for the frame's rows already holds its weights.
+template <typename WT, int CELL>
+__device__ __forceinline__ void gemv1_prefetch(const GemvArgs &g, uint32_t ub) {
+  const uint32_t K1 = g.E + g.H;
+  const uint32_t lines = (uint32_t)((size_t)K1 * sizeof(WT) / 128);          // per weight row
+  const WT *w1 = static_cast<const WT *>(g.w1), *w2 = static_cast<const WT *>(g.w2);
+  const uint32_t nrows = CELL == RNNLM_CELL_RNN ? U1 : 3 * U1;
+  for (uint32_t i = threadIdx.x; i < nrows * lines; i += blockDim.x) {
+    const uint32_t r = i / lines, l = i % lines, u = ub * U1 + r % U1, gate = r / U1;
+    const WT *row = CELL == RNNLM_CELL_RNN || gate == 2 ? w2 + (size_t)u * g.RW
+                    : w1 + (gate == 0 ? z_row(g, u) : r_row(g, u)) * g.RW;
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char *>(row) + (size_t)l * 128));
+  }
+}
+
 // Phase 2 of unit block ub (units [U2 * ub, +U2)), rows as gemv1_item.
 template <typename WT, int ACT, int CELL>
 __device__ __forceinline__ void gemv2_item(const GemvArgs &g, uint32_t Q, uint32_t ub, uint32_t rb, uint32_t nrb,

@@ -9,12 +9,15 @@
 // scripts/latency_probe.py, profiles/latency_r2.jsonl) for well under a
 // microsecond of memory traffic.  Here one cooperative persistent kernel
 // (one CTA per SM, co-resident by construction) runs every step with grid
-// barriers where the multi-kernel path has kernel boundaries:
+// barriers (three) where the multi-kernel path has kernel boundaries; the
+// cache front (n <= 512 queries) runs in ONE CTA with block barriers, which
+// are ~20x cheaper than grid barriers (measured per phase: ~4 us with grid
+// barriers, profiles/small_phases_r2.txt):
 //
-//   A  (a2) LM-query cache probe + claim          qcache_query   (cache.cuh)
-//   B  (a3) owner resolution, hidden-cache claim  hcache_query
-//   C  (a4) flags + exclusive scan (CTA 0)        scan_flag / scan_store
-//   D  (a4) commit: handles, slots, records       commit_query
+//   A  (a2) LM-query cache probe + claim          qcache_query   (cache.cuh)  } CTA 0 alone, block
+//   B  (a3) owner resolution, hidden-cache claim  hcache_query                } barriers between; the
+//   C  (a4) flags + exclusive scan                scan_flag / scan_store      } other CTAs pull their
+//   D  (a4) commit: handles, slots, records       commit_query                } GEMV weights into L1
 //   E  (a7) result write + counters               final_query    (warp-collective)
 //      (a6) NCE + MaxEnt scores                   score_quad     (score.cuh)
 //      (a5) GEMV phase 1                          gemv1_item     (gemv.cuh)
@@ -25,6 +28,7 @@
 // the same claim / barrier / read order, so results are bit-identical to that
 // path with the GEMV GRU kernels (tests/test_gpu_small.py).
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "cache.cuh"
@@ -105,36 +109,66 @@ __device__ __forceinline__ void block_scan(const Params &P, const CallArgs &A, u
 
 template <typename WT, int ACT, int CELL>
 __global__ void __launch_bounds__(SMALL_THREADS, 1)
-    k_small(Params P, CallArgs A, GemvArgs g, uint32_t *bar, uint32_t rb1, uint32_t rb2) {
+    k_small(Params P, CallArgs A, GemvArgs g, uint32_t *bar, uint32_t rb1, uint32_t rb2,
+            unsigned long long *prof) {
+  // prof (diagnostics, RNNLM_SMALL_PROF): %globaltimer of CTA 0 after every phase
+  auto stamp = [&](int i) {
+    if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      prof[i] = t;
+    }
+  };
+  stamp(0);
   const uint32_t n = call_n(A);
   const uint32_t tid = blockIdx.x * SMALL_THREADS + threadIdx.x, nthr = gridDim.x * SMALL_THREADS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t gw = tid >> 5, ngw = nthr >> 5;
-  // A: (a2)
-  if (tid == 0) P.counts[3] = 0u;
-  for (uint32_t q = tid; q < n; q += nthr) qcache_query(P, A, q);
-  grid_sync(bar);
-  // B: (a3)
-  const bool bad = P.counts[2] != 0u;
-  for (uint32_t q = tid; q < n; q += nthr) hcache_query(P, A, q);
-  grid_sync(bar);
-  // C: (a4) scan
+  const uint32_t nb1 = g.H / U1, nb2 = g.H / U2;
   if (blockIdx.x == 0) {
+    // A-D: the cache front of all n <= MAX_N queries by CTA 0 alone; its
+    // block barriers stand in for the kernel boundaries between claiming and
+    // reading an owner (global atomics + __syncthreads: every access before
+    // the barrier is visible to the whole CTA after it)
+    if (threadIdx.x == 0) P.counts[3] = 0u;
+    for (uint32_t q = threadIdx.x; q < n; q += SMALL_THREADS) qcache_query(P, A, q);   // (a2)
+    __syncthreads();
+    stamp(1);
+    const bool bad = P.counts[2] != 0u;
+    for (uint32_t q = threadIdx.x; q < n; q += SMALL_THREADS) hcache_query(P, A, q);   // (a3)
+    __syncthreads();
+    stamp(2);
     if (n == 0 && threadIdx.x == 0) { P.counts[0] = 0u; P.counts[1] = 0u; }
-    block_scan(P, A, n, bad);
+    block_scan(P, A, n, bad);                                                            // (a4)
+    __syncthreads();
+    stamp(3);
+    for (uint32_t q = threadIdx.x; q < n; q += SMALL_THREADS) commit_query(P, A, q, n);
+  } else {
+    // meanwhile: pull this CTA's phase-1 GEMV weight rows into L1 (CTAs >= 2
+    // take the GEMV items in phase E, see below)
+    const uint32_t SC = gridDim.x >= 8 ? 2u : 1u;
+    if (blockIdx.x >= SC)
+      for (uint32_t j = blockIdx.x - SC; j < nb1 * rb1; j += gridDim.x - SC) gemv1_prefetch<WT, CELL>(g, j % nb1);
   }
   grid_sync(bar);
-  // D: (a4) commit
-  for (uint32_t q = tid; q < n; q += nthr) commit_query(P, A, q, n);
-  grid_sync(bar);
+  stamp(4);
   // E: (a7) result write, (a6) scores, (a5) GEMV phase 1
+  // the first SC CTAs write results and score, the others run the GEMV, so
+  // neither waits behind the other's dependent loads
   const uint32_t total = P.counts[0], Q = P.counts[1];
-  for (uint32_t base = gw * 32; base < n; base += ngw * 32) final_query(P, A, base + lane, n);
-  for (uint32_t base = gw * 4; base < total; base += ngw * 4) score_quad(P, A, base, total);
-  const uint32_t nb1 = g.H / U1, nb2 = g.H / U2;
-  for (uint32_t j = blockIdx.x; j < nb1 * rb1; j += gridDim.x)
-    gemv1_item<WT, ACT, CELL>(g, Q, j % nb1, j / nb1, rb1, warp, SMALL_THREADS / 32);
+  const uint32_t SC = gridDim.x >= 8 ? 2u : 1u;
+  if (blockIdx.x < SC || gridDim.x == 1) {
+    const uint32_t w0 = blockIdx.x * (SMALL_THREADS / 32) + warp, nw0 = SC * (SMALL_THREADS / 32);
+    for (uint32_t base = w0 * 32; base < n; base += nw0 * 32) final_query(P, A, base + lane, n);
+    for (uint32_t base = w0 * 4; base < total; base += nw0 * 4) score_quad(P, A, base, total);
+  }
+  if (blockIdx.x >= SC || gridDim.x == 1) {
+    const uint32_t c0 = gridDim.x == 1 ? 0u : blockIdx.x - SC, nc = gridDim.x == 1 ? 1u : gridDim.x - SC;
+    for (uint32_t j = c0; j < nb1 * rb1; j += nc)
+      gemv1_item<WT, ACT, CELL>(g, Q, j % nb1, j / nb1, rb1, warp, SMALL_THREADS / 32);
+  }
   grid_sync(bar);
+  stamp(5);
   // F: (a5) GEMV phase 2; duplicates of this call's new queries take their owner's score
   for (uint32_t j = blockIdx.x; j < nb2 * rb2; j += gridDim.x)
     gemv2_item<WT, ACT, CELL>(g, Q, j % nb2, j / nb2, rb2, warp, SMALL_THREADS / 32);
@@ -148,9 +182,12 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1)
     return;
   }
   grid_sync(bar);
+  stamp(6);
   // G: (a1) codes of the new states; the bad-batch flag is cleared for the next call
   gemv_encode(g, Q, gw, ngw);
   if (tid == 0) P.counts[2] = 0u;
+  __syncthreads();
+  stamp(7);
 }
 
 }  // namespace rnnlm_small
@@ -172,7 +209,19 @@ static cudaError_t launch_small_t(const Params &P, const CallArgs &A, const rnnl
   cfg.stream = s;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_small<WT, ACT, CELL>, P, A, g, bar, rb1, rb2);
+  static unsigned long long *prof = nullptr;
+  static const bool want = getenv("RNNLM_SMALL_PROF") != nullptr;
+  if (want && !prof) { cudaMalloc(&prof, 8 * sizeof(unsigned long long)); cudaMemset(prof, 0, 64); }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_small<WT, ACT, CELL>, P, A, g, bar, rb1, rb2, prof);
+  if (want && e == cudaSuccess) {        // diagnostics: phase durations of this call to stderr
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[k_small prof] grid=%u us:", grid);
+    for (int i = 1; i < 8; ++i) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, " total %.2f\n", (h[7] - h[0]) * 1e-3);
+  }
+  return e;
 }
 
 uint32_t small_max_queries() { return MAX_N; }
