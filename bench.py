@@ -46,7 +46,7 @@ METRIC = "RNNLM queries/sec (frame-batched, cache on)"
 UNIT = "queries/s"
 UTT_FRAMES = 400            # a 4-s utterance at 10 ms frames
 TOTAL_STREAMS = 64          # BASELINE configs[4]
-MATHS = ("bf16", "tf32", "fp32", "tf32x3")
+MATHS = ("bf16", "tf32", "fp32", "tf32x3", "bf16x3")
 
 
 def parse():
@@ -60,8 +60,8 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="strong: the job's streams are split over the ranks (BASELINE configs[4]); "
                          "weak: every rank runs that many streams")
-    ap.add_argument("--math", default="tf32x3", choices=MATHS, help="headline arithmetic")
-    ap.add_argument("--also", default="bf16", help="extra math modes measured on the same frames (comma list, or none)")
+    ap.add_argument("--math", default="bf16x3", choices=MATHS, help="headline arithmetic")
+    ap.add_argument("--also", default="bf16,tf32x3", help="extra math modes measured on the same frames (comma list, or none)")
     ap.add_argument("--key", default="sign", help="off | sign | round:K")
     ap.add_argument("--cell", default="gru", choices=["gru", "lbr", "rnn"],
                     help="recurrent cell (SURVEY 8(f)-3): gru = Chung GRU (the paper's), lbr = linear before "
@@ -100,11 +100,13 @@ def key_mode(name):
 
 def math_id(name):
     import paper_1801_09866_b200 as R
-    return {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[name]
+    return {"bf16": R.MATH_BF16, "tf32": R.MATH_TF32, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3,
+            "bf16x3": R.MATH_BF16X3}[name]
 
 
 def dtype_of(name):
-    return {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "tf32x3": "f32 (3xTF32)"}[name]
+    return {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "tf32x3": "f32 (3xTF32)",
+            "bf16x3": "f32 (bf16x3 split)"}[name]
 
 
 def host_cores():
@@ -299,11 +301,14 @@ def gru_peak(math, clk, peaks, tf32_peak, x3_products=3):
     burst = burst_clocks(clk)
     which = "burst" if burst else "sustained"
     bf16 = peaks.get("bf16_tflops" if burst else "bf16_tflops_sustained")
-    if math == "bf16":
+    if math in ("bf16", "bf16x3"):
+        div = float(x3_products) if math == "bf16x3" else 1.0
+        note = (f" / {x3_products:g} (bf16 products per useful multiply-add of the three-part split; "
+                "identically-zero products of bf16-exact weights / embeddings are skipped)" if math == "bf16x3" else "")
         if bf16:
-            return bf16, "TFLOP/s", "tensor", f"MEASURED_PEAKS bf16 ({which}: run at max clock, no power cap)" \
-                if burst else f"MEASURED_PEAKS bf16 ({which}: clocks below max or power-capped)"
-        return 2250.0, "TFLOP/s", "tensor", "B200_PROFILING nominal dense bf16 (no measured peak)"
+            return bf16 / div, "TFLOP/s", "tensor", (f"MEASURED_PEAKS bf16 ({which}: run at max clock, no power cap)"
+                if burst else f"MEASURED_PEAKS bf16 ({which}: clocks below max or power-capped)") + note
+        return 2250.0 / div, "TFLOP/s", "tensor", "B200_PROFILING nominal dense bf16 (no measured peak)" + note
     if math in ("tf32", "tf32x3"):
         div = float(x3_products) if math == "tf32x3" else 1.0
         note = (f" / {x3_products:g} (TF32 products per useful multiply-add; identically-zero products "
@@ -461,7 +466,7 @@ def step_summary(args, bench, res, world, peaks, tf32_peak):
     k_ms = (timing["ms_gru_phase1"] + timing["ms_gru_phase2"]) if (tc and not gemv) else timing["ms_gru"]
     peak, unit, bound, src = gru_peak(math, res["clocks_B"], peaks, tf32_peak, bench.eng.tf32x3_products() or 3)
     achieved = flops / (k_ms / 1e3) / 1e12 if k_ms > 0 else 0.0
-    pair = (math == "bf16" and args.cell == "gru" and dims.H % 256 == 0
+    pair = (math in ("bf16", "bf16x3") and args.cell == "gru" and dims.H % 256 == 0
             and os.environ.get("RNNLM_TC_PAIR", "1") != "0")
     kname = ("k_gru_tc2 (fused tcgen05 GRU, both phases, CTA pair)" if pair else
              "k_gru_tc (fused tcgen05 GRU, both phases)") if tc else "k_gru1_f32 + k_gru2_f32 (FP32 SIMT tiles)"

@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define RNNLM_ABI_VERSION 2
+#define RNNLM_ABI_VERSION 3
 
 typedef struct rnnlm rnnlm_t;          /* opaque; one per CUDA device */
 typedef struct rnnlm_graph rnnlm_graph_t;   /* opaque; a captured rnnlm_query_batch (rnnlm_graph_create) */
@@ -84,14 +84,24 @@ typedef enum {
   RNNLM_MATH_FP32 = 0,      /* FP32 FFMA (SIMT) */
   RNNLM_MATH_TF32 = 1,      /* fp32 operands read as TF32, fp32 accumulation on tcgen05 tensor cores */
   RNNLM_MATH_BF16 = 2,      /* bf16 operands, fp32 accumulation on tcgen05 tensor cores */
-  RNNLM_MATH_TF32X3 = 3     /* fp32-accurate on tcgen05: a = a_hi + a_lo, w = w_hi + w_lo (TF32 parts),
+  RNNLM_MATH_TF32X3 = 3,    /* fp32-accurate on tcgen05: a = a_hi + a_lo, w = w_hi + w_lo (TF32 parts),
                              * a.w ~ a_hi.w_hi + a_hi.w_lo + a_lo.w_hi (three TF32 products, fp32
                              * accumulation; the 1e-5 path of the FP32 mode at tensor-core rate).
                              * Products that are identically zero are not computed: a_hi.w_lo when
                              * every gate weight is TF32-exact (w_lo == 0), a_lo.w_hi over the
                              * embedding part of K when every embedding entry is (x_lo == 0);
                              * rnnlm_tf32x3_products reports what remains. */
-  /* The two tensor-core modes need E % 64 == 0 and H % 128 == 0 (else
+  RNNLM_MATH_BF16X3 = 4     /* fp32-accurate on tcgen05 bf16 tensor cores: every fp32 operand is split
+                             * into three bf16 parts v = hi + mid + lo (|v - hi - mid - lo| <= 2^-27 |v|;
+                             * each part times a bf16 weight part is exact in fp32), and the
+                             * contraction sums a_i.w_j over i + j <= 2 (six bf16 products, fp32
+                             * accumulation), held to the FP32 mode's 1e-5 like TF32X3.  Identically
+                             * zero products are skipped: with bf16-exact gate weights only
+                             * a_hi.w + a_mid.w + a_lo.w remain, and over the embedding part of K
+                             * only x_hi.w when every embedding entry is bf16-exact (2 bf16 products
+                             * per useful multiply-add at E = H; rnnlm_tf32x3_products reports it).
+                             * Scores use the fp32 output weights (like TF32 / TF32X3). */
+  /* The tensor-core modes need E % 64 == 0 and H % 128 == 0 (else
    * rnnlm_create returns RNNLM_E_DIMENSION).  BF16 stores bf16 copies of E
    * and the gate weights (and of nce_w when every entry is bf16-exact); TF32
    * keeps every parameter fp32. */
@@ -276,9 +286,11 @@ rnnlm_status rnnlm_set_timing(rnnlm_t *h, int level);
 rnnlm_status rnnlm_get_timing(rnnlm_t *h, rnnlm_timing *out, int reset);
 /* Kernels launched by this handle since create (host-side count). */
 uint64_t rnnlm_launch_count(const rnnlm_t *h);
-/* RNNLM_MATH_TF32X3 engines: tensor-core products per useful multiply-add of
- * the gate contraction (3 less the skipped zero products, e.g. 1.5 with
- * TF32-exact weights and embeddings at E = H); else 0. */
+/* Split (fp32-accurate) engines: tensor-core products per useful multiply-add
+ * of the gate contraction, in the mode's own MMA kind (RNNLM_MATH_TF32X3: TF32
+ * products, 3 less the skipped zero products, e.g. 1.5 with TF32-exact weights
+ * and embeddings at E = H; RNNLM_MATH_BF16X3: bf16 products, 6 less the skipped
+ * ones, e.g. 2 with bf16-exact weights and embeddings at E = H); else 0. */
 double rnnlm_tf32x3_products(const rnnlm_t *h);
 const char *rnnlm_status_string(rnnlm_status s);
 int rnnlm_abi_version(void);

@@ -216,8 +216,9 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   if (c.key_mode > RNNLM_KEY_SIGN) return RNNLM_E_INVALID_ARG;
   if (c.key_mode == RNNLM_KEY_ROUND && (c.round_digits < 1 || c.round_digits > 4))
     return RNNLM_E_INVALID_ARG;
-  if (c.math > RNNLM_MATH_TF32X3) return RNNLM_E_INVALID_ARG;
-  if (c.math == RNNLM_MATH_TF32X3 && c.cell != RNNLM_CELL_GRU) return RNNLM_E_INVALID_ARG;
+  if (c.math > RNNLM_MATH_BF16X3) return RNNLM_E_INVALID_ARG;
+  const bool split = c.math == RNNLM_MATH_TF32X3 || c.math == RNNLM_MATH_BF16X3;   // fp32-accurate splits
+  if (split && c.cell != RNNLM_CELL_GRU) return RNNLM_E_INVALID_ARG;
   if (c.cell > RNNLM_CELL_RNN) return RNNLM_E_INVALID_ARG;
   if (c.gru_path > RNNLM_GRU_GEMV) return RNNLM_E_INVALID_ARG;
   const bool tc = c.math != RNNLM_MATH_FP32;           // tcgen05 path (BF16 or TF32 operands)
@@ -300,7 +301,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
       chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.emb16), w->emb, V * E));
     if (st == RNNLM_OK &&
         rnnlm_host::gru_tc_prepare(w, c.vocab, c.embed, c.hidden, c.math == RNNLM_MATH_TF32 || c.math == RNNLM_MATH_TF32X3,
-                                   c.math == RNNLM_MATH_TF32X3,
+                                   c.math == RNNLM_MATH_TF32X3 ? 2 : (c.math == RNNLM_MATH_BF16X3 ? 3 : 0),
                                    (int)c.cell, &h->tc) != 0)
       st = RNNLM_E_OOM;
   }
@@ -333,10 +334,11 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
   // z: the tensor-core path keeps it in 128-row blocks (k_gru_tc.cu zq4), so whole blocks
   chk(dalloc(h, &P.g_z, (B + 127) / 128 * 128 * H));
   if (c.math == RNNLM_MATH_FP32) chk(dalloc(h, &P.g_wxb, B * H));
-  if (c.math == RNNLM_MATH_BF16) chk(dalloc(h, &P.g_rh16, B * H));
-  else chk(dalloc(h, &P.g_rh, (c.math == RNNLM_MATH_TF32X3 ? 2 : 1) * B * H));   // 3xTF32: [hi | lo]
+  const bool rh16 = c.math == RNNLM_MATH_BF16 || c.math == RNNLM_MATH_BF16X3;
+  if (rh16) chk(dalloc(h, &P.g_rh16, (c.math == RNNLM_MATH_BF16X3 ? 3 : 1) * B * H));   // BF16X3: [hi | mid | lo]
+  else chk(dalloc(h, &P.g_rh, (c.math == RNNLM_MATH_TF32X3 ? 2 : 1) * B * H));      // 3xTF32: [hi | lo]
   if (st == RNNLM_OK && tc &&
-      rnnlm_host::gru_tc_bind(h->tc, c.math == RNNLM_MATH_BF16 ? (void *)P.g_rh16 : (void *)P.g_rh,
+      rnnlm_host::gru_tc_bind(h->tc, rh16 ? (void *)P.g_rh16 : (void *)P.g_rh,
                               (uint32_t)B) != 0)
     st = RNNLM_E_CUDA;
   if (st == RNNLM_OK && c.gru_path != RNNLM_GRU_TILES) {
@@ -346,7 +348,7 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
                                                         ? c.max_queries_per_call : RNNLM_GEMV_AUTO_MAX_QUERIES);
     const void *w1 = nullptr, *w2 = nullptr;
     uint32_t rw = 0;
-    if (tc && c.math != RNNLM_MATH_TF32X3) rnnlm_host::gru_tc_weights(h->tc, &w1, &w2, &rw);
+    if (tc && !split) rnnlm_host::gru_tc_weights(h->tc, &w1, &w2, &rw);
     if (rnnlm_host::gemv_prepare(P, w, c.math, w1, w2, rw, h->gemv_max_n, &h->gemv) != 0) st = RNNLM_E_OOM;
   }
   if (st == RNNLM_OK) {

@@ -108,6 +108,30 @@ __device__ __forceinline__ float4 to_tf32(float4 v) {
   return make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
 }
 
+// fp32 -> bf16 parts v = hi + mid + lo (each round to nearest even of the
+// remainder, which is exact in fp32): |v - hi - mid - lo| <= 2^-27 |v|, and
+// every part times a bf16 weight part is exact in the fp32 accumulator.
+__device__ __forceinline__ float bf16_part(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+__device__ __forceinline__ void split3(float v, float &hi, float &mid, float &lo) {
+  hi = bf16_part(v);
+  const float r = v - hi;
+  mid = bf16_part(r);
+  lo = bf16_part(r - mid);
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {      // a, b already on the bf16 grid
+  return (__float_as_uint(a) >> 16) | (__float_as_uint(b) & 0xFFFF0000u);
+}
+__device__ __forceinline__ void split3_bf16x4(float4 v, uint2 *p) {
+  float h[4], m[4], l[4];
+  split3(v.x, h[0], m[0], l[0]);
+  split3(v.y, h[1], m[1], l[1]);
+  split3(v.z, h[2], m[2], l[2]);
+  split3(v.w, h[3], m[3], l[3]);
+  p[0] = make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
+  p[1] = make_uint2(pack_bf16x2(m[0], m[1]), pack_bf16x2(m[2], m[3]));
+  p[2] = make_uint2(pack_bf16x2(l[0], l[1]), pack_bf16x2(l[2], l[3]));
+}
+
 __device__ __forceinline__ float sigm(float a) { return __fdividef(1.0f, 1.0f + __expf(-a)); }
 // tanh via exp (relative error ~1e-6; the bf16 path's bar is 1e-3)
 __device__ __forceinline__ float tanh_fast(float a) {
@@ -121,6 +145,16 @@ __device__ __forceinline__ void ld_bias16(const float *p, float *b) {
     b[4 * j] = v.x; b[4 * j + 1] = v.y; b[4 * j + 2] = v.z; b[4 * j + 3] = v.w;
   }
 }
+
+// Split (fp32-accurate) modes: a tile's accumulator sums the products
+// A_pa . W_pw of operand parts over K segments, pa + pw <= P - 1 (the terms
+// of order < 2^-(P * bits) relative), identically-zero parts skipped.  One
+// segment = K-chunks [k0, k1) of A part pa against weight part pw; the
+// plain modes have the single segment (0, 0, 0, KC).
+struct SplitSeg {
+  uint16_t pa, pw, k0, k1;
+};
+constexpr int MAX_SEG = 12;
 
 struct TcArgs {
   uint32_t E, H, nub;              // nub = H / 128 phase-1 unit blocks
@@ -146,18 +180,26 @@ struct TcArgs {
   // (z | r | Wh x | Uh h), B = W3 [(H/64) x 192 rows][E+H]
   const float *bz, *br;            // [H] (LBR epilogue)
   uint32_t bn2;                    // units per phase-2 (and RNN) tile: 256, or 128 when H % 256 != 0
-  uint32_t x3_wlo;                 // 3xTF32: 1 = run the A_hi.W_lo segment; 0 = every weight is TF32-exact
-                                   // (W_lo == 0), so that product is identically zero and is skipped
-  uint32_t x3_xlo;                 // 3xTF32: 1 = run A_lo.W_hi over the x part of K; 0 = every embedding
-                                   // entry is TF32-exact (x_lo == 0): A_lo.W_hi covers the h part only
-  uint32_t x3;                     // RNNLM_MATH_TF32X3 (TF32 instance only): operands as [hi | lo] TF32 parts,
-                                   // three K segments hi.hi, hi.lo, lo.hi (A1 2(E+H), r.h 2H, W 2(E+H) wide)
+  uint32_t x3_xlo;                 // split modes: 1 = the embedding has non-zero lower parts (they are
+                                   // gathered); 0 = every entry is exact in the operand type
+  uint32_t x3;                     // split (fp32-accurate) modes: number of operand parts P of every
+                                   // activation, v = sum_p part_p: 2 = RNNLM_MATH_TF32X3 ([hi | lo] TF32,
+                                   // TF32 instance), 3 = RNNLM_MATH_BF16X3 ([hi | mid | lo] bf16); 0 = plain.
+                                   // A1 rows are P (E+H) wide, r.h rows P H, weight rows PW (E+H)
+  uint32_t nseg;                   // K segments of one tile (plain: 1); see SplitSeg
+  SplitSeg seg[MAX_SEG];
   // (a1) compression of the new state, fused into the phase-2 epilogue
   uint32_t cache, key_mode, round_digits, cstride;
   float round_scale;
   uint8_t *codes;
   unsigned long long *codehash;
 };
+
+__host__ __device__ __forceinline__ uint32_t seg_chunks(const TcArgs &a) {
+  uint32_t n = 0;
+  for (uint32_t s = 0; s < a.nseg; ++s) n += a.seg[s].k1 - a.seg[s].k0;
+  return n;
+}
 
 // ---------------------------------------------------------------- A gather
 // Phase-1 A operand: row r = [E[word_r] | bf16(state[src_r])] (bf16, K-major,
@@ -175,6 +217,37 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
     a.done1[i] = 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.tile_ctr = 0u;
   if constexpr (sizeof(T) == 2) {
+    if (a.x3) {
+      // BF16X3: [x_hi | h_hi | x_mid | h_mid | x_lo | h_lo], v = hi + mid + lo
+      // (split3); x parts from the fp32 embedding (x_mid, x_lo only when some
+      // entry is not bf16-exact: otherwise their segments are skipped and
+      // never read).  Four 16-byte loads per lane are in flight before the
+      // first store.
+      const uint32_t nk = K1 / 4, nx = a.E / 4;
+      for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < Q; r += nw) {
+        const float4 *x = reinterpret_cast<const float4 *>(a.emb + (size_t)a.row_word[r] * a.E);
+        const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
+        uint2 *dst = reinterpret_cast<uint2 *>(a.a1 + (size_t)r * 3 * K1);
+        for (uint32_t i0 = lane; i0 < nk; i0 += 128) {
+          float4 v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t i = i0 + 32 * j;
+            if (i < nk) v[j] = i < nx ? __ldg(x + i) : __ldg(h + (i - nx));
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t i = i0 + 32 * j;
+            if (i >= nk) continue;
+            uint2 p[3];
+            split3_bf16x4(v[j], p);
+            dst[i] = p[0];
+            if (i >= nx || a.x3_xlo) { dst[nk + i] = p[1]; dst[2 * nk + i] = p[2]; }
+          }
+        }
+      }
+      return;
+    }
     // bf16: every load of a row chunk (4 x 16 B of x, 8 x 16 B of h per lane)
     // is issued before its stores, and the next row's indices are fetched
     // while the current row is copied, so a warp keeps ~12 loads in flight
@@ -513,6 +586,22 @@ __device__ __forceinline__ void put_row_bf16(uint8_t *stg, uint32_t lane, const 
     *reinterpret_cast<uint4 *>(stg + stg_off<64>(lane, c)) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
+// BF16X3: the bf16 part of x (round to nearest even) into the staging row,
+// x keeps the (exact) remainder; three calls store hi, mid, lo
+__device__ __forceinline__ void put_row_bf16_part(uint8_t *stg, uint32_t lane, float *x) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float p0 = bf16_part(x[8 * c + 2 * j]), p1 = bf16_part(x[8 * c + 2 * j + 1]);
+      x[8 * c + 2 * j] -= p0;
+      x[8 * c + 2 * j + 1] -= p1;
+      w[j] = pack_bf16x2(p0, p1);
+    }
+    *reinterpret_cast<uint4 *>(stg + stg_off<64>(lane, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
 // 32 consecutive accumulator columns of this thread's TMEM lane (wait separately)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
   tmem_ld16(taddr, v);
@@ -545,7 +634,7 @@ __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint
       }
     } else {
       float hv[32];
-      if constexpr (sizeof(T) == 2) {
+      if (sizeof(T) == 2 && !a.x3) {
         coop_load<64>(stg, valid ? a.a1 + (size_t)row * (a.E + a.H) + a.E + u0 + c * 32 : nullptr, lane);
         own_row_bf16(stg, lane, hv);
       } else {
@@ -557,8 +646,16 @@ __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint
       for (int j = 0; j < 32; ++j) hv[j] *= sigm(v[j] + b[j]);
       __syncwarp();
       if constexpr (sizeof(T) == 2) {
-        put_row_bf16(stg, lane, hv);
-        coop_store<64>(stg, valid ? a.g_rh16 + (size_t)row * a.H + u0 + c * 32 : nullptr, lane);
+        if (!a.x3) {
+          put_row_bf16(stg, lane, hv);
+          coop_store<64>(stg, valid ? a.g_rh16 + (size_t)row * a.H + u0 + c * 32 : nullptr, lane);
+        } else {  // BF16X3: r.h as [hi | mid | lo] rows of 3H
+#pragma unroll 1
+          for (int p = 0; p < 3; ++p) {
+            put_row_bf16_part(stg, lane, hv);
+            coop_store<64>(stg, valid ? a.g_rh16 + (size_t)row * 3 * a.H + p * a.H + u0 + c * 32 : nullptr, lane);
+          }
+        }
       } else if (!a.x3) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) hv[j] = to_tf32(hv[j]);
@@ -715,10 +812,8 @@ __global__ void __maxnreg__(GRU_MAXREG)
   constexpr bool LBR = CELL == RNNLM_CELL_GRU_LBR, RNN = CELL == RNNLM_CELL_RNN;
   const uint32_t n1 = LBR ? a.H / 64 : (RNN ? a.H / a.bn2 : a.nub), n2 = (LBR || RNN) ? 0u : a.H / a.bn2;
   constexpr int BKE = Op<T>::BKE;
-  const uint32_t kx = a.E / BKE, KC = (a.E + a.H) / BKE;
-  // 3xTF32 K-chunk list: A_hi.W_hi over all of K, A_hi.W_lo over all of K
-  // (unless W_lo == 0), A_lo.W_hi from chunk k2 (the x part is skipped when x_lo == 0)
-  const uint32_t k2 = a.x3_xlo ? 0u : kx, KCt = a.x3 ? KC + (a.x3_wlo ? KC : 0u) + (KC - k2) : KC;
+  const uint32_t kx = a.E / BKE;
+  const uint32_t KCt = seg_chunks(a);                    // K-chunks per tile over every split segment
   const uint32_t target = n1 * EPI_WARPS;               // phase-1 arrivals per M-tile
   if (threadIdx.x == 0) {
     prefetch_map(&map_a1); prefetch_map(&map_w1); prefetch_map(&map_rh); prefetch_map(&map_w2);
@@ -754,15 +849,11 @@ __global__ void __maxnreg__(GRU_MAXREG)
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         if (prof) prof[9 + x.kind] += 1;
-        for (uint32_t kc3 = 0; kc3 < KCt; ++kc3) {
-          // 3xTF32: segment 0 = A_hi.W_hi, 1 = A_hi.W_lo, 2 = A_lo.W_hi (column offsets of the lo parts)
-          uint32_t seg = 0, kc = kc3;
-          if (a.x3 && kc3 >= KC) {
-            if (a.x3_wlo && kc3 < 2 * KC) { seg = 1; kc = kc3 - KC; }
-            else { seg = 2; kc = k2 + kc3 - KC - (a.x3_wlo ? KC : 0u); }
-          }
-          const int a_off = seg == 2 ? (int)(a.E + a.H) : 0, b_off = seg == 1 ? (int)(a.E + a.H) : 0;
-          const int rh_off = seg == 2 ? (int)a.H : 0;
+        for (uint32_t sg = 0; sg < a.nseg; ++sg)
+        for (uint32_t kc = a.seg[sg].k0; kc < a.seg[sg].k1; ++kc) {
+          // split modes: A part pa, weight part pw of this segment (column offsets into the part blocks)
+          const int a_off = (int)(a.seg[sg].pa * (a.E + a.H)), b_off = (int)(a.seg[sg].pw * (a.E + a.H));
+          const int rh_off = (int)(a.seg[sg].pa * a.H);
           t0 = clock64();
           mbar_wait(&m.empty[stage], phase ^ 1);
           w_empty += clock64() - t0;
@@ -976,7 +1067,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const uint32_t n1 = a.nub, n2 = a.H / BN;
-  const uint32_t kx = a.E / BK, KC = (a.E + a.H) / BK;
+  const uint32_t kx = a.E / BK, KCt = seg_chunks(a);
   const uint32_t target = n1 * 2 * EPI_WARPS;           // phase-1 arrivals per 256-row tile
   // tile-ring consumers (arrivals on the leader's qempty per slot): the
   // leader's MMA lane, the peer's producer, both CTAs' epilogue warps
@@ -1044,7 +1135,11 @@ __global__ void __maxnreg__(GRU_MAXREG)
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         if (prof) prof[9 + x.kind] += 1;
-        for (uint32_t kc = 0; kc < KC; ++kc) {
+        for (uint32_t sg = 0; sg < a.nseg; ++sg)
+        for (uint32_t kc = a.seg[sg].k0; kc < a.seg[sg].k1; ++kc) {
+          // BF16X3: A part pa against weight part pw (column offsets into the part blocks)
+          const int a_off = (int)(a.seg[sg].pa * (a.E + a.H)), b_off = (int)(a.seg[sg].pw * (a.E + a.H));
+          const int rh_off = (int)(a.seg[sg].pa * a.H);
           t0 = clock64();
           mbar_wait(&m.empty[stage], phase ^ 1);
           w_empty += clock64() - t0;
@@ -1057,12 +1152,12 @@ __global__ void __maxnreg__(GRU_MAXREG)
           const uint32_t fb = full0 + stage * 8;
           const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
           if (x.kind == 0) {
-            tma_load_2d_pair(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
-            tma_load_2d_pair(dB, &map_w1h, fb, (int)(kc * BK), (int)b0row);
+            tma_load_2d_pair(dA, &map_a1, fb, a_off + (int)(kc * BK), (int)m0);
+            tma_load_2d_pair(dB, &map_w1h, fb, b_off + (int)(kc * BK), (int)b0row);
           } else {
-            if (kc < kx) tma_load_2d_pair(dA, &map_a1, fb, (int)(kc * BK), (int)m0);
-            else tma_load_2d_pair(dA, &map_rh, fb, (int)((kc - kx) * BK), (int)m0);
-            tma_load_2d_pair(dB, &map_w2h, fb, (int)(kc * BK), (int)b0row);
+            if (kc < kx) tma_load_2d_pair(dA, &map_a1, fb, a_off + (int)(kc * BK), (int)m0);
+            else tma_load_2d_pair(dA, &map_rh, fb, rh_off + (int)((kc - kx) * BK), (int)m0);
+            tma_load_2d_pair(dB, &map_w2h, fb, b_off + (int)(kc * BK), (int)b0row);
           }
           if (++stage == STP) { stage = 0; phase ^= 1; }
         }
@@ -1087,7 +1182,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
         w_tempty += clock64() - t0;
         tc_fence_after();
         const uint32_t tm = tmem_base + acc * BN;
-        for (uint32_t kc = 0; kc < KC; ++kc) {
+        for (uint32_t kc = 0; kc < KCt; ++kc) {
           t0 = clock64();
           mbar_wait_cl(&m.full[stage], phase);            // both CTAs' bytes landed
           w_full += clock64() - t0;
@@ -1099,7 +1194,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
               for (int k = 0; k < BK / 16; ++k)
                 umma_bf16_pair(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
             umma_commit_pair(&m.empty[stage]);
-            if (kc == KC - 1) umma_commit_pair(&m.tfull[acc]);
+            if (kc == KCt - 1) umma_commit_pair(&m.tfull[acc]);
           }
           __syncwarp();
           if (++stage == STP) { stage = 0; phase ^= 1; }
@@ -1181,9 +1276,9 @@ struct TcState {
   uint32_t diag = 0;               // RNNLM_TC_DIAG: timing diagnostics (see TcArgs::diag)
   unsigned long long *prof = nullptr;
   float *bzr = nullptr, *bh = nullptr;
-  bool x3 = false;                 // RNNLM_MATH_TF32X3: [hi | lo] operand rows, three K segments
-  bool x3_wlo = true;              // some weight is not TF32-exact (its W_lo part is non-zero)
-  bool x3_xlo = true;              // some embedding entry is not TF32-exact
+  uint32_t x3 = 0;                 // split modes: operand parts P (2: TF32X3, 3: BF16X3); 0: plain
+  uint32_t wparts = 1;             // weight parts with a non-zero entry (1: every weight is exact in T)
+  bool x3_xlo = true;              // some embedding entry is not exact in the operand type
   bool lbr = false;                // cell GRU_LBR: one-phase tiles over W3
   bool rnn = false;                // cell RNN: one-phase tiles over W2 = [Wh | Uh]
   void *w3 = nullptr;
@@ -1236,8 +1331,8 @@ static bool upload_w3(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H
 
 template <typename T>
 static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H) {
-  // rows of K1 = E + H operands; with 3xTF32 each row is [hi | lo] (2 K1)
-  const size_t K1 = E + H, RW = t->x3 ? 2 * K1 : K1;
+  // rows of K1 = E + H operands; in the split modes each row is [part 0 | .. | part P-1] (P K1)
+  const size_t K1 = E + H, NP = t->x3 ? t->x3 : 1, RW = NP * K1;
   std::vector<T> w1((size_t)2 * H * RW), w2((size_t)H * RW);
   auto cv = [](float v) -> T {
     if constexpr (sizeof(T) == 2) {
@@ -1254,15 +1349,15 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
   const float *Wg[2] = {w->Wz, w->Wr};
   const float *Ug[2] = {w->Uz, w->Ur};
   bool any_lo = false;
-  // one weight into (row, k): its (TF32 / bf16) value, and with 3xTF32 the
-  // TF32 part of the remainder at k + K1
+  // one weight into (row, k): its (TF32 / bf16) value, and in the split modes
+  // the parts of the successive remainders at k + p K1 (exact fp32 differences)
   auto put = [&](T *row, size_t k, float v) {
-    row[k] = cv(v);
-    if constexpr (sizeof(T) == 4)
-      if (t->x3) {
-        row[K1 + k] = cv(v - (float)row[k]);
-        if ((float)row[K1 + k] != 0.0f) any_lo = true;
-      }
+    float r = v;
+    for (size_t p = 0; p < NP; ++p) {
+      row[p * K1 + k] = cv(r);
+      r -= (float)row[p * K1 + k];
+      if (p > 0 && (float)row[p * K1 + k] != 0.0f) any_lo = true;
+    }
   };
   for (size_t u = 0; u < H; ++u) {
     const size_t ub = u / UB, uu = u % UB;
@@ -1275,7 +1370,7 @@ static bool upload_w(TcState *t, const rnnlm_weights *w, uint32_t E, uint32_t H)
     for (size_t k = 0; k < E; ++k) put(row2, k, w->Wh[u * E + k]);
     for (size_t k = 0; k < H; ++k) put(row2, E + k, w->Uh[u * H + k]);
   }
-  t->x3_wlo = any_lo;
+  t->wparts = any_lo ? (uint32_t)NP : 1u;
   return cudaMalloc(&t->w1, w1.size() * sizeof(T)) == cudaSuccess &&
          cudaMalloc(&t->w2, w2.size() * sizeof(T)) == cudaSuccess &&
          cudaMemcpy(t->w1, w1.data(), w1.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess &&
@@ -1286,13 +1381,15 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t V, uint32_t E, uint32_t H, i
                    void **state_out) {
   *state_out = nullptr;
   TcState *t = new TcState;
-  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0; t->x3 = x3 != 0 && t->tf32;
-  if (t->x3) {                    // is every embedding entry TF32-exact (low 13 mantissa bits zero)?
+  t->E = E; t->H = H; t->nub = H / UB; t->tf32 = tf32 != 0;
+  t->x3 = (x3 == 2 && t->tf32) || (x3 == 3 && !t->tf32) ? (uint32_t)x3 : 0u;
+  if (t->x3) {                    // is every embedding entry exact in T (TF32: low 13, bf16: low 16 bits zero)?
+    const uint32_t low = t->tf32 ? 0x1FFFu : 0xFFFFu;
     t->x3_xlo = false;
     for (size_t i = 0; i < (size_t)E * V; ++i) {
       uint32_t b;
       std::memcpy(&b, &w->emb[i], 4);
-      if (b & 0x1FFFu) { t->x3_xlo = true; break; }
+      if (b & low) { t->x3_xlo = true; break; }
     }
   }
   t->lbr = cell == RNNLM_CELL_GRU_LBR;
@@ -1324,14 +1421,13 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t V, uint32_t E, uint32_t H, i
        cudaMalloc(&t->bh, bh.size() * 4) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bzr, bzr.data(), bzr.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(t->bh, bh.data(), bh.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
-  const size_t RW = t->x3 ? 2 * K1 : K1;
+  const size_t RW = (t->x3 ? t->x3 : 1) * K1;
   ok = ok && make_map(&t->map_w1, t->w1, RW, 2 * (uint64_t)H, BN, t->tf32) &&
        make_map(&t->map_w2, t->w2, RW, H, H % BN ? UB : BN, t->tf32);
-  if (t->x3) t->pair = 0;
   if (H % BN) t->pair = 0;        // the CTA pair keeps 256-unit phase-2 tiles
   if (!t->tf32)
-    ok = ok && make_map(&t->map_w1h, t->w1, K1, 2 * (uint64_t)H, BN / 2) &&
-         make_map(&t->map_w2h, t->w2, K1, H, BN / 2);
+    ok = ok && make_map(&t->map_w1h, t->w1, RW, 2 * (uint64_t)H, BN / 2) &&
+         make_map(&t->map_w2h, t->w2, RW, H, BN / 2);
   ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
@@ -1353,7 +1449,7 @@ int gru_tc_bind(void *state, void *rh, uint32_t bmax) {
   t->rh = rh;
   t->bmax = bmax;
   const size_t es = t->tf32 ? 4 : 2;
-  const size_t xw = t->x3 ? 2 : 1;                     // 3xTF32: [hi | lo] rows
+  const size_t xw = t->x3 ? t->x3 : 1;                 // split modes: P operand parts per row
   if (cudaMalloc(&t->a1, (size_t)bmax * (t->E + t->H) * es * xw) != cudaSuccess ||
       cudaMalloc(&t->done1, ((size_t)bmax / BM + 4) * sizeof(uint32_t)) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -1375,14 +1471,37 @@ int gru_tc_weights(void *state, const void **w1, const void **w2, uint32_t *rw) 
   return 0;
 }
 
-// Tensor-core products per useful multiply-add of the 3xTF32 mode: 3, less
-// the skipped identically-zero ones (0 for the other modes).
+// K segments of the split modes (see SplitSeg): the terms A_pa . W_pw with
+// pa + pw < P, lowest order first; weight parts that are all zero and, over
+// the x columns, embedding parts that are all zero are skipped.
+// RNNLM_SPLIT_ALL_SEGMENTS (A/B) runs the identically-zero products anyway.
+static void make_segs(TcArgs &a, const TcState *t) {
+  const uint32_t bke = t->tf32 ? 32u : 64u;
+  const uint32_t kx = t->E / bke, KC = (t->E + t->H) / bke;
+  a.nseg = 0;
+  if (!t->x3) {
+    a.seg[a.nseg++] = SplitSeg{0, 0, 0, (uint16_t)KC};
+    return;
+  }
+  const bool all = getenv("RNNLM_SPLIT_ALL_SEGMENTS") != nullptr;
+  const uint32_t P = t->x3, PW = all ? P : t->wparts;
+  const bool xlo = all || t->x3_xlo;
+  for (uint32_t ord = 0; ord < P; ++ord)
+    for (uint32_t pw = 0; pw <= ord; ++pw) {
+      const uint32_t pa = ord - pw;
+      if (pw >= PW) continue;
+      a.seg[a.nseg++] = SplitSeg{(uint16_t)pa, (uint16_t)pw, (uint16_t)((pa == 0 || xlo) ? 0 : kx), (uint16_t)KC};
+    }
+}
+
+// Tensor-core products per useful multiply-add of a split mode (the chunks
+// of every segment over the chunks of K); 0 for the plain modes.
 double gru_tc_x3_products(void *state) {
   TcState *t = static_cast<TcState *>(state);
   if (!t || !t->x3) return 0.0;
-  const bool all = getenv("RNNLM_TF32X3_ALL_SEGMENTS") != nullptr;
-  const double K = t->E + t->H;
-  return (K + ((t->x3_wlo || all) ? K : 0.0) + ((t->x3_xlo || all) ? K : (double)t->H)) / K;
+  TcArgs a;
+  make_segs(a, t);
+  return (double)seg_chunks(a) * (t->tf32 ? 32.0 : 64.0) / (double)(t->E + t->H);
 }
 
 void gru_tc_release(void *state) {
@@ -1426,10 +1545,9 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.diag = t->diag;
   a.bz = t->bz; a.br = t->br;
   a.bn2 = P.H % BN ? UB : BN;
-  a.x3 = t->x3 ? 1u : 0u;
-  a.x3_wlo = t->x3_wlo ? 1u : 0u;
-  a.x3_xlo = t->x3_xlo ? 1u : 0u;
-  if (getenv("RNNLM_TF32X3_ALL_SEGMENTS")) a.x3_wlo = a.x3_xlo = 1u;   // (A/B) run the zero products anyway
+  a.x3 = t->x3;
+  a.x3_xlo = (t->x3_xlo || getenv("RNNLM_SPLIT_ALL_SEGMENTS")) ? 1u : 0u;
+  make_segs(a, t);
   a.prof = nullptr;
   if (t->diag == 5) {
     if (!t->prof) cudaMalloc(&t->prof, 1024 * 16 * sizeof(unsigned long long));

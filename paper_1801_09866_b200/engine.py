@@ -14,7 +14,7 @@ from . import _lib
 from ._lib import Config, Stats, Timing, Weights, check
 
 KEY_OFF, KEY_ROUND, KEY_SIGN = 0, 1, 2
-MATH_FP32, MATH_TF32, MATH_BF16, MATH_TF32X3 = 0, 1, 2, 3
+MATH_FP32, MATH_TF32, MATH_BF16, MATH_TF32X3, MATH_BF16X3 = 0, 1, 2, 3, 4
 CELL_GRU, CELL_GRU_LBR, CELL_RNN = 0, 1, 2  # rnnlm_cell
 GRU_AUTO, GRU_TILES, GRU_GEMV = 0, 1, 2  # rnnlm_gru_path
 QHIT, SHIT, MISS, INVALID = 0, 1, 2, 255
@@ -180,8 +180,9 @@ class RNNLM:
         return int(_lib.load().rnnlm_launch_count(self._h))
 
     def tf32x3_products(self) -> float:
-        """3xTF32 engines: tensor-core products per useful multiply-add (3 less
-        the identically-zero ones skipped); 0 otherwise."""
+        """Split (fp32-accurate) engines: tensor-core products per useful
+        multiply-add in the mode's MMA kind (TF32X3: 3, BF16X3: 6, less the
+        identically-zero ones skipped); 0 otherwise."""
         return float(_lib.load().rnnlm_tf32x3_products(self._h))
 
 

@@ -21,3 +21,10 @@ timeout 1500 ncu --set full --clock-control none --import-source on \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_small' -s 100 -c 2 \
   -o gpurun_out/prof_small_r2 -f python scripts/latency_probe.py moderate bf16 auto > gpurun_out/ncu_small.log 2>&1
 ls -la gpurun_out
+# 5. memory kernels on the uniform-word stream (no Zipf reuse: DRAM bytes ~ algorithmic bytes), bf16 step
+MM="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,lts__t_sector_hit_rate.pct"
+timeout 900 ncu --metrics $MM --clock-control none -k regex:'k_gather_a1|k_score|k_qcache|k_hcache|k_scan|k_commit|k_final|k_dup_scores' \
+  -s 3000 -c 40 --csv --log-file gpurun_out/ncu_uniform_r2.csv $B --math bf16 --uniform-words > gpurun_out/ncu_uniform_bench.json 2> gpurun_out/ncu_uniform.err
+timeout 900 ncu --metrics $MM --clock-control none -k regex:'k_gather_a1|k_score|k_qcache|k_hcache|k_scan|k_commit|k_final|k_dup_scores' \
+  -s 3000 -c 40 --csv --log-file gpurun_out/ncu_zipf_r2.csv $B --math bf16 > /dev/null 2> gpurun_out/ncu_zipf.err
+ls -la gpurun_out

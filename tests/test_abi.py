@@ -31,7 +31,7 @@ def test_exports_every_declared_symbol(L):
     for n in names:
         assert hasattr(L, n), n
         assert n in _lib.SIGNATURES, f"binding lacks {n}"
-    assert L.rnnlm_abi_version() == 2
+    assert L.rnnlm_abi_version() == 3
 
 
 def test_library_is_sm100a(L):

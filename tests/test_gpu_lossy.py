@@ -20,7 +20,7 @@ are about half of what the CPU oracle produces on the same stream
 import pytest
 
 from paper_1801_09866_b200 import (GRU_AUTO, GRU_GEMV, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32,
-                                   MATH_TF32X3)
+                                   MATH_TF32X3, MATH_BF16X3)
 from synth import generate_workload
 from tests.parity_util import replay_compare
 from tests.test_gpu_parity import TOL, model, pair
@@ -32,8 +32,10 @@ pytestmark = pytest.mark.gpu
 MIN_SHIT_256 = {(KEY_SIGN, 0): 1500, (KEY_ROUND, 1): 1000, (KEY_ROUND, 2): 300, (KEY_ROUND, 3): 50}
 MIN_SHIT_1024 = {(KEY_SIGN, 0): 200, (KEY_ROUND, 1): 150}
 
-# (math, RNNLM_TC_PAIR): bf16 CTA pair (default), bf16 one CTA per tile, TF32, 3xTF32, FP32 SIMT
-PATHS = [(MATH_BF16, "1"), (MATH_BF16, "0"), (MATH_TF32, "0"), (MATH_TF32X3, "0"), (MATH_FP32, "0")]
+# (math, RNNLM_TC_PAIR): bf16 CTA pair (default), bf16 one CTA per tile, TF32, 3xTF32, BF16X3 on the
+# CTA pair and on one CTA per tile, FP32 SIMT
+PATHS = [(MATH_BF16, "1"), (MATH_BF16, "0"), (MATH_TF32, "0"), (MATH_TF32X3, "0"), (MATH_BF16X3, "1"),
+         (MATH_BF16X3, "0"), (MATH_FP32, "0")]
 
 
 def _wl256(V):
@@ -69,7 +71,7 @@ def test_lossy_merges_h1024(math, pk, mode, k, monkeypatch):
 
 # ---------------------------------------------------------------- small-frame GEMV path (a5-q)
 @pytest.mark.parametrize("mode,k", [(KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 2)])
-@pytest.mark.parametrize("math", [MATH_BF16, MATH_TF32, MATH_TF32X3, MATH_FP32])
+@pytest.mark.parametrize("math", [MATH_BF16, MATH_TF32, MATH_TF32X3, MATH_BF16X3, MATH_FP32])
 def test_gemv_path_h256(math, mode, k):
     """The GEMV kernels (k_gemv1 / k_gemv2, codes encoded by the last CTA)
     against the oracle on the H = 256 lattice stream, every math mode, lossy

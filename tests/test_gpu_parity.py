@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import oracle as O
-from paper_1801_09866_b200 import (KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32, MATH_TF32, MATH_TF32X3, RNNLM,
+from paper_1801_09866_b200 import (KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_BF16X3, MATH_FP32, MATH_TF32, MATH_TF32X3, RNNLM,
                                    INVALID, MISS, QHIT, SHIT, GRU_GEMV, GRU_TILES)
 from synth import generate_model, generate_workload, model_dims
 from synth.model import ModelDims
@@ -19,7 +19,7 @@ from tests.parity_util import _dev, replay_compare
 pytestmark = pytest.mark.gpu
 
 TOL = {MATH_FP32: 1e-5, MATH_BF16: 1e-3, MATH_TF32: 1e-3,    # 1e-3 for bf16/tf32
-       MATH_TF32X3: 1e-5}                                      # fp32-accurate tensor-core mode: the FP32 bar
+       MATH_TF32X3: 1e-5, MATH_BF16X3: 1e-5}                   # fp32-accurate tensor-core modes: the FP32 bar
 _models = {}
 
 
@@ -614,14 +614,14 @@ def test_tf32x3_skips_zero_weight_lo_segment(monkeypatch):
     """bf16-grid weights and embeddings are TF32-exact, so the 3xTF32 A_hi.W_lo
     product and A_lo.W_hi over the embedding part of K are identically zero
     and are skipped (1.5 products per MAC at E = H); running them anyway
-    (RNNLM_TF32X3_ALL_SEGMENTS) only adds exact zeros: bitwise the same scores
+    (RNNLM_SPLIT_ALL_SEGMENTS) only adds exact zeros: bitwise the same scores
     and states.  Off-grid weights keep all three."""
     d, m = model("moderate")
     wl = lattice(1, 12, 256, d.V, seed=5)
     outs = []
     for allseg in (False, True):
         if allseg:
-            monkeypatch.setenv("RNNLM_TF32X3_ALL_SEGMENTS", "1")
+            monkeypatch.setenv("RNNLM_SPLIT_ALL_SEGMENTS", "1")
         eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_TF32X3)
         assert eng.tf32x3_products() == (3.0 if allseg else 1.5)   # E = H: (K + H) / K
         child = np.zeros(wl.n_total, np.uint32)
@@ -634,8 +634,80 @@ def test_tf32x3_skips_zero_weight_lo_segment(monkeypatch):
         outs.append((score, eng.read_states(0, child).cpu().numpy()))
     assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
     assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
-    monkeypatch.delenv("RNNLM_TF32X3_ALL_SEGMENTS")
+    monkeypatch.delenv("RNNLM_SPLIT_ALL_SEGMENTS")
     d2 = ModelDims(V=1000, E=256, H=256, maxent_log2=16, N=3)
     m2 = generate_model(d2, seed=3, scale=0.1, bf16_grid=False)
     eng2 = RNNLM.from_dims(d2, m2, math=MATH_TF32X3, max_queries_per_call=8, max_histories_per_session=8)
     assert eng2.tf32x3_products() == 3.0
+
+
+# ---------------------------------------------------------------- BF16X3: fp32-accurate on the bf16 tensor cores
+@pytest.mark.parametrize("pair_kernel", ["1", "0"])
+def test_bf16x3_moderate_fp32_tolerance(pair_kernel, monkeypatch):
+    """RNNLM_MATH_BF16X3 holds the FP32 path's 1e-5 bar on scores and states
+    (activations split into three bf16 parts), sign keys with lossy hits,
+    codes bit-exact; the CTA pair and one CTA per tile."""
+    monkeypatch.setenv("RNNLM_TC_PAIR", pair_kernel)
+    d, m = model("moderate")
+    wl = lattice(1, 30, 256, d.V, seed=17)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16X3)
+    rep = replay_compare(eng, orc, wl, tol_score=1e-5, tol_state=1e-5)
+    assert rep["miss"] > 200
+
+
+@pytest.mark.parametrize("pair_kernel", ["1", "0"])
+def test_bf16x3_large_full_tiles_and_ragged(pair_kernel, monkeypatch):
+    monkeypatch.setenv("RNNLM_TC_PAIR", pair_kernel)
+    d, m = model("large")
+    wl = generate_workload(1, 2, 2048, d.V, seed=5)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16X3, cache=False)
+    rep = replay_compare(eng, orc, wl, tol_score=1e-5, tol_state=1e-5)
+    assert rep["miss"] == wl.n_total
+    wl = generate_workload(3, 3, 300, d.V, seed=6)
+    eng, orc = pair(d, m, wl, KEY_ROUND, k=2, math=MATH_BF16X3)
+    replay_compare(eng, orc, wl, tol_score=1e-5, tol_state=1e-5)
+
+
+@pytest.mark.parametrize("pair_kernel", ["1", "0"])
+def test_bf16x3_off_grid_weights_accuracy(pair_kernel, monkeypatch):
+    """Weights and embeddings NOT on the bf16 grid: all six products run, the
+    states sit at FP32-path error (< 1e-5 from the fp64 oracle), far below
+    plain bf16 operands."""
+    monkeypatch.setenv("RNNLM_TC_PAIR", pair_kernel)
+    d = ModelDims(V=1000, E=256, H=256, maxent_log2=16, N=3)
+    m = generate_model(d, seed=3, scale=0.1, bf16_grid=False)
+    wl = generate_workload(1, 6, 256, d.V, seed=8)
+    errs = {}
+    for math in (MATH_BF16, MATH_BF16X3):
+        eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cache=False)
+        if math == MATH_BF16X3:
+            assert eng.tf32x3_products() == 6.0
+        errs[math] = replay_compare(eng, orc, wl, tol_score=1e-1, tol_state=1e-1)["max_state_err"]
+    assert errs[MATH_BF16X3] < 1e-5, errs
+    assert errs[MATH_BF16X3] < 0.01 * errs[MATH_BF16], errs
+
+
+def test_bf16x3_skips_zero_segments(monkeypatch):
+    """bf16-grid weights and embeddings: the products with a zero weight part
+    and, over the embedding part of K, with a zero embedding part are skipped
+    (2 bf16 products per MAC at E = H: x_hi.W over E, h_hi/mid/lo.W over H);
+    running all six anyway (RNNLM_SPLIT_ALL_SEGMENTS) only adds exact zeros:
+    bitwise the same scores and states."""
+    d, m = model("moderate")
+    wl = lattice(1, 12, 256, d.V, seed=5)
+    outs = []
+    for allseg in (False, True):
+        if allseg:
+            monkeypatch.setenv("RNNLM_SPLIT_ALL_SEGMENTS", "1")
+        eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16X3)
+        assert eng.tf32x3_products() == (6.0 if allseg else 2.0)   # E = H: (E + 3H) / (E + H)
+        child = np.zeros(wl.n_total, np.uint32)
+        score = np.zeros(wl.n_total, np.float32)
+        for t in range(wl.frames):
+            sl = wl.frame_slice(t)
+            par = O.resolve_parents(wl.parent_ref[sl], child)
+            s_, c_, _ = eng.query_batch(_dev(wl.session[sl]), _dev(par), _dev(wl.word[sl]))
+            score[sl], child[sl] = s_.cpu().numpy(), c_.cpu().numpy().view(np.uint32)
+        outs.append((score, eng.read_states(0, child).cpu().numpy()))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))

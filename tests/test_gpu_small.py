@@ -8,7 +8,7 @@ import torch
 
 import oracle as O
 from paper_1801_09866_b200 import (GRU_AUTO, GRU_GEMV, INVALID, KEY_OFF, KEY_ROUND, KEY_SIGN, MATH_BF16, MATH_FP32,
-                                   MATH_TF32, MATH_TF32X3, RNNLM)
+                                   MATH_TF32, MATH_TF32X3, MATH_BF16X3, RNNLM)
 from synth import generate_workload
 from tests.parity_util import _dev, replay_compare
 from tests.test_gpu_parity import TOL, forgetful_model, model, pair
@@ -34,7 +34,7 @@ def test_tiny_config_fused(mode, k):
 
 
 @pytest.mark.parametrize("mode,k", [(KEY_SIGN, 0), (KEY_ROUND, 1), (KEY_ROUND, 2)])
-@pytest.mark.parametrize("math", [MATH_BF16, MATH_TF32, MATH_TF32X3, MATH_FP32])
+@pytest.mark.parametrize("math", [MATH_BF16, MATH_TF32, MATH_TF32X3, MATH_BF16X3, MATH_FP32])
 def test_moderate_fused_lossy(math, mode, k):
     """configs[1] shapes (H = 256, 256 queries/frame) on the lattice stream
     with merging keys, every math mode."""
