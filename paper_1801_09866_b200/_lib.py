@@ -82,7 +82,8 @@ _lib = None
 
 
 def library_path() -> str:
-    return _build.SO
+    # RNNLM_LIBRARY: another in-tree build of the same ABI (A/B experiments only)
+    return os.environ.get("RNNLM_LIBRARY") or _build.SO
 
 
 def load():

@@ -149,10 +149,14 @@ __device__ __forceinline__ void ld_bias16(const float *p, float *b) {
 // Split (fp32-accurate) modes: a tile's accumulator sums the products
 // A_pa . W_pw of operand parts over K segments, pa + pw <= P - 1 (the terms
 // of order < 2^-(P * bits) relative), identically-zero parts skipped.  One
-// segment = K-chunks [k0, k1) of A part pa against weight part pw; the
-// plain modes have the single segment (0, 0, 0, KC).
+// segment = K-chunks [k0, k1) of weight part pw against the A parts
+// pa0 .. pa0 + npa - 1: one smem stage holds one weight chunk and npa A
+// chunks (the CTA-pair kernel loads each weight chunk once for all three
+// BF16X3 parts); the one-CTA kernel runs npa = 1 segments.  The plain modes
+// have the single segment (pa0 0, npa 1, pw 0, [0, KC)).
 struct SplitSeg {
-  uint16_t pa, pw, k0, k1;
+  uint8_t pa0, npa, pw, pad;
+  uint16_t k0, k1;
 };
 constexpr int MAX_SEG = 12;
 
@@ -399,6 +403,11 @@ __device__ __forceinline__ Tile tile_of(uint32_t t, uint32_t mt, uint32_t n1, ui
   return x;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {       // ns (diag 5 timeline)
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -827,6 +836,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   const uint32_t tmem_base = *m.tmem_base;
   unsigned long long *prof = a.prof ? a.prof + blockIdx.x * 16 : nullptr;
   const unsigned long long k_t0 = clock64();
+  if (prof && threadIdx.x == 0) prof[14] = gtimer();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -852,8 +862,8 @@ __global__ void __maxnreg__(GRU_MAXREG)
         for (uint32_t sg = 0; sg < a.nseg; ++sg)
         for (uint32_t kc = a.seg[sg].k0; kc < a.seg[sg].k1; ++kc) {
           // split modes: A part pa, weight part pw of this segment (column offsets into the part blocks)
-          const int a_off = (int)(a.seg[sg].pa * (a.E + a.H)), b_off = (int)(a.seg[sg].pw * (a.E + a.H));
-          const int rh_off = (int)(a.seg[sg].pa * a.H);
+          const int a_off = (int)(a.seg[sg].pa0 * (a.E + a.H)), b_off = (int)(a.seg[sg].pw * (a.E + a.H));
+          const int rh_off = (int)(a.seg[sg].pa0 * a.H);
           t0 = clock64();
           mbar_wait(&m.empty[stage], phase ^ 1);
           w_empty += clock64() - t0;
@@ -950,6 +960,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   }
   if (prof && threadIdx.x == 0) prof[8] = clock64() - k_t0;
   teardown(m, warp, tmem_base);
+  if (prof && threadIdx.x == 0) prof[15] = gtimer();       // every warp of the CTA is done
 }
 
 // =============================================================== CTA-pair variant
@@ -965,8 +976,11 @@ __global__ void __maxnreg__(GRU_MAXREG)
 #endif
 // pair-kernel smem stages (32 KB each): 5 measured faster than 6 on the bench
 // workload (547-549 vs 537-540 M q/s, kernel 194.8 vs 197.6 us, same box)
-constexpr int STP = RNNLM_TC_STP;
 constexpr int BP_BYTES = (BN / 2) * BK * 2;    // 16 KB: this CTA's half of a B chunk
+// stages per A parts per stage: NA = 1 (plain bf16: 32-KB stages), NA = 3
+// (BF16X3: one weight chunk + three A part chunks, 64-KB stages, 3 of them)
+template <int NA>
+__host__ __device__ constexpr int stp_of() { return NA == 1 ? RNNLM_TC_STP : 3; }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -1033,11 +1047,13 @@ struct SmemP {
   uint32_t *tmem_base, *tile_q;
 };
 
+template <int NA>
 __device__ __forceinline__ SmemP carve_pair(uint8_t *raw) {
+  constexpr int STP = stp_of<NA>();
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   SmemP m;
   m.sA = smem;
-  m.sB = smem + STP * A_BYTES;
+  m.sB = smem + STP * NA * A_BYTES;
   m.stg = m.sB + STP * BP_BYTES;
   m.full = reinterpret_cast<uint64_t *>(m.stg + EPI_WARPS * STG_BYTES);
   m.empty = m.full + STP;
@@ -1057,12 +1073,14 @@ __device__ __forceinline__ SmemP carve_pair(uint8_t *raw) {
 // (cp.async.bulk.tensor .cta_group::2), which the leader arms with the bytes
 // of both halves; the MMA commit releases the stage in both CTAs at once
 // (multicast), so no CTA-to-CTA handshake sits on the K loop.
+template <int NA>
 __global__ void __maxnreg__(GRU_MAXREG)
     k_gru_tc2(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1h,
               const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2h,
               TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const SmemP m = carve_pair(smem_raw);
+  constexpr int STP = stp_of<NA>();
+  const SmemP m = carve_pair<NA>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -1095,6 +1113,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   const uint32_t qempty0 = mapa(smem_u32(&m.qempty[0]), 0);
   unsigned long long *prof = a.prof ? a.prof + blockIdx.x * 16 : nullptr;
   const unsigned long long k_t0 = clock64();
+  if (prof && threadIdx.x == 0) prof[14] = gtimer();
 
   // tile id of ring slot `it`; one lane releases the slot on the leader's qempty
   auto take = [&](uint32_t it, bool release) -> uint32_t {
@@ -1137,9 +1156,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
         if (prof) prof[9 + x.kind] += 1;
         for (uint32_t sg = 0; sg < a.nseg; ++sg)
         for (uint32_t kc = a.seg[sg].k0; kc < a.seg[sg].k1; ++kc) {
-          // BF16X3: A part pa against weight part pw (column offsets into the part blocks)
-          const int a_off = (int)(a.seg[sg].pa * (a.E + a.H)), b_off = (int)(a.seg[sg].pw * (a.E + a.H));
-          const int rh_off = (int)(a.seg[sg].pa * a.H);
+          // this stage: weight part pw, A parts pa0 .. pa0 + npa - 1 (column offsets into the part blocks)
+          const uint32_t pa0 = a.seg[sg].pa0, npa = NA == 1 ? 1u : a.seg[sg].npa;
+          const int b_off = (int)(a.seg[sg].pw * (a.E + a.H));
           t0 = clock64();
           mbar_wait(&m.empty[stage], phase ^ 1);
           w_empty += clock64() - t0;
@@ -1148,17 +1167,19 @@ __global__ void __maxnreg__(GRU_MAXREG)
             if (++stage == STP) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (leader) mbar_expect_tx(&m.full[stage], 2 * (A_BYTES + BP_BYTES));
+          if (leader) mbar_expect_tx(&m.full[stage], 2 * (npa * A_BYTES + BP_BYTES));
           const uint32_t fb = full0 + stage * 8;
-          const uint32_t dA = smem_u32(m.sA + stage * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
-          if (x.kind == 0) {
-            tma_load_2d_pair(dA, &map_a1, fb, a_off + (int)(kc * BK), (int)m0);
-            tma_load_2d_pair(dB, &map_w1h, fb, b_off + (int)(kc * BK), (int)b0row);
-          } else {
-            if (kc < kx) tma_load_2d_pair(dA, &map_a1, fb, a_off + (int)(kc * BK), (int)m0);
-            else tma_load_2d_pair(dA, &map_rh, fb, rh_off + (int)((kc - kx) * BK), (int)m0);
-            tma_load_2d_pair(dB, &map_w2h, fb, b_off + (int)(kc * BK), (int)b0row);
+          const uint32_t dA = smem_u32(m.sA + stage * NA * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
+#pragma unroll
+          for (uint32_t p = 0; p < (uint32_t)NA; ++p) {
+            if (p >= npa) break;
+            const uint32_t pa = pa0 + p;
+            if (x.kind == 0 || kc < kx)
+              tma_load_2d_pair(dA + p * A_BYTES, &map_a1, fb, (int)(pa * (a.E + a.H) + kc * BK), (int)m0);
+            else
+              tma_load_2d_pair(dA + p * A_BYTES, &map_rh, fb, (int)(pa * a.H + (kc - kx) * BK), (int)m0);
           }
+          tma_load_2d_pair(dB, x.kind == 0 ? &map_w1h : &map_w2h, fb, b_off + (int)(kc * BK), (int)b0row);
           if (++stage == STP) { stage = 0; phase ^= 1; }
         }
       }
@@ -1182,22 +1203,31 @@ __global__ void __maxnreg__(GRU_MAXREG)
         w_tempty += clock64() - t0;
         tc_fence_after();
         const uint32_t tm = tmem_base + acc * BN;
-        for (uint32_t kc = 0; kc < KCt; ++kc) {
-          t0 = clock64();
-          mbar_wait_cl(&m.full[stage], phase);            // both CTAs' bytes landed
-          w_full += clock64() - t0;
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
-            if (a.diag != 1 && a.diag != 6)
+        uint32_t kc = 0;                                  // stage count of this tile
+        // NA == 1: every stage holds one A chunk, the segment walk is not needed
+        for (uint32_t sg = 0; sg < (NA == 1 ? 1u : a.nseg); ++sg) {
+          const uint32_t npa = NA == 1 ? 1u : a.seg[sg].npa;
+          const uint32_t c0 = NA == 1 ? 0u : a.seg[sg].k0, c1 = NA == 1 ? KCt : a.seg[sg].k1;
+          for (uint32_t c = c0; c < c1; ++c, ++kc) {
+            t0 = clock64();
+            mbar_wait_cl(&m.full[stage], phase);          // both CTAs' bytes landed
+            w_full += clock64() - t0;
+            tc_fence_after();
+            if (lane == 0) {
+              const uint32_t a0 = smem_u32(m.sA + stage * NA * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
+              if (a.diag != 1 && a.diag != 6)
 #pragma unroll
-              for (int k = 0; k < BK / 16; ++k)
-                umma_bf16_pair(tm, sdesc(a0 + k * 32), sdesc(b0 + k * 32), id, (kc | k) != 0);
-            umma_commit_pair(&m.empty[stage]);
-            if (kc == KCt - 1) umma_commit_pair(&m.tfull[acc]);
+                for (uint32_t p = 0; p < (uint32_t)NA; ++p)
+                  if (p < npa)
+#pragma unroll
+                  for (int k = 0; k < BK / 16; ++k)
+                    umma_bf16_pair(tm, sdesc(a0 + p * A_BYTES + k * 32), sdesc(b0 + k * 32), id, (kc | p | k) != 0);
+              umma_commit_pair(&m.empty[stage]);
+              if (kc == KCt - 1) umma_commit_pair(&m.tfull[acc]);
+            }
+            __syncwarp();
+            if (++stage == STP) { stage = 0; phase ^= 1; }
           }
-          __syncwarp();
-          if (++stage == STP) { stage = 0; phase ^= 1; }
         }
       }
       if (prof && lane == 0) { prof[2] = w_full; prof[3] = w_tempty; }
@@ -1255,13 +1285,16 @@ __global__ void __maxnreg__(GRU_MAXREG)
   if (prof && threadIdx.x == 0) prof[8] = clock64() - k_t0;
   tc_fence_before();
   __syncthreads();
+  if (prof && threadIdx.x == 0) prof[15] = gtimer();       // every warp of the CTA is done
   cluster_sync();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, TMEM_COLS);
   }
 }
-constexpr size_t SMEM_PAIR = 1024 + STP * (A_BYTES + BP_BYTES) + EPI_WARPS * STG_BYTES + 256;
+template <int NA>
+constexpr size_t smem_pair() { return 1024 + stp_of<NA>() * (NA * A_BYTES + BP_BYTES) + EPI_WARPS * STG_BYTES + 256; }
+static_assert(smem_pair<3>() <= 232448, "BF16X3 pair stages exceed the 227-KB smem limit");
 
 constexpr size_t smem_of(int nst) { return 1024 + nst * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 256; }
 constexpr size_t SMEM = smem_of(ST), SMEM_RNN = smem_of(st_of<RNNLM_CELL_RNN>());
@@ -1434,7 +1467,8 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t V, uint32_t E, uint32_t H, i
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RNN) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RNN) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_PAIR) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pair<1>()) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pair<3>()) == cudaSuccess;
   *state_out = t;
   if (!ok) {
     (void)cudaGetLastError();
@@ -1475,23 +1509,35 @@ int gru_tc_weights(void *state, const void **w1, const void **w2, uint32_t *rw) 
 // pa + pw < P, lowest order first; weight parts that are all zero and, over
 // the x columns, embedding parts that are all zero are skipped.
 // RNNLM_SPLIT_ALL_SEGMENTS (A/B) runs the identically-zero products anyway.
-static void make_segs(TcArgs &a, const TcState *t) {
+static void make_segs(TcArgs &a, const TcState *t, bool grouped) {
   const uint32_t bke = t->tf32 ? 32u : 64u;
   const uint32_t kx = t->E / bke, KC = (t->E + t->H) / bke;
   a.nseg = 0;
+  auto add = [&](uint32_t npa, uint32_t pw, uint32_t k0, uint32_t k1) {   // A parts 0 .. npa - 1
+    if (grouped) {
+      a.seg[a.nseg++] = SplitSeg{0, (uint8_t)npa, (uint8_t)pw, 0, (uint16_t)k0, (uint16_t)k1};
+    } else {
+      for (uint32_t p = 0; p < npa; ++p)
+        a.seg[a.nseg++] = SplitSeg{(uint8_t)p, 1, (uint8_t)pw, 0, (uint16_t)k0, (uint16_t)k1};
+    }
+  };
   if (!t->x3) {
-    a.seg[a.nseg++] = SplitSeg{0, 0, 0, (uint16_t)KC};
+    add(1, 0, 0, KC);
     return;
   }
   const bool all = getenv("RNNLM_SPLIT_ALL_SEGMENTS") != nullptr;
   const uint32_t P = t->x3, PW = all ? P : t->wparts;
   const bool xlo = all || t->x3_xlo;
-  for (uint32_t ord = 0; ord < P; ++ord)
-    for (uint32_t pw = 0; pw <= ord; ++pw) {
-      const uint32_t pa = ord - pw;
-      if (pw >= PW) continue;
-      a.seg[a.nseg++] = SplitSeg{(uint16_t)pa, (uint16_t)pw, (uint16_t)((pa == 0 || xlo) ? 0 : kx), (uint16_t)KC};
+  for (uint32_t pw = 0; pw < PW; ++pw) {
+    const uint32_t nh = P - pw;                  // A parts pa with pa + pw <= P - 1
+    const uint32_t nx = xlo ? nh : 1;            // over the x columns only part 0 may be non-zero
+    if (nx == nh) {
+      add(nh, pw, 0, KC);
+    } else {
+      add(nx, pw, 0, kx);
+      add(nh, pw, kx, KC);
     }
+  }
 }
 
 // Tensor-core products per useful multiply-add of a split mode (the chunks
@@ -1500,8 +1546,10 @@ double gru_tc_x3_products(void *state) {
   TcState *t = static_cast<TcState *>(state);
   if (!t || !t->x3) return 0.0;
   TcArgs a;
-  make_segs(a, t);
-  return (double)seg_chunks(a) * (t->tf32 ? 32.0 : 64.0) / (double)(t->E + t->H);
+  make_segs(a, t, true);
+  double chunks = 0;
+  for (uint32_t i = 0; i < a.nseg; ++i) chunks += (double)a.seg[i].npa * (a.seg[i].k1 - a.seg[i].k0);
+  return chunks * (t->tf32 ? 32.0 : 64.0) / (double)(t->E + t->H);
 }
 
 void gru_tc_release(void *state) {
@@ -1547,7 +1595,9 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.bn2 = P.H % BN ? UB : BN;
   a.x3 = t->x3;
   a.x3_xlo = (t->x3_xlo || getenv("RNNLM_SPLIT_ALL_SEGMENTS")) ? 1u : 0u;
-  make_segs(a, t);
+  // the CTA pair loads each weight chunk once for all A parts (RNNLM_TC_GROUP=0: one part per stage)
+  const bool grouped = t->pair && !(getenv("RNNLM_TC_GROUP") && atoi(getenv("RNNLM_TC_GROUP")) == 0);
+  make_segs(a, t, grouped);
   a.prof = nullptr;
   if (t->diag == 5) {
     if (!t->prof) cudaMalloc(&t->prof, 1024 * 16 * sizeof(unsigned long long));
@@ -1571,8 +1621,12 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / BN) * 2;
     const uint32_t cap = (uint32_t)num_sms & ~1u;
     if (gp > cap) gp = cap;
-    launch_pdl_cluster(k_gru_tc2, gp, THREADS, SMEM_PAIR, s, 2, t->map_a1, t->map_w1h, t->map_rh,
-                       t->map_w2h, a);
+    if (grouped && t->x3)
+      launch_pdl_cluster(k_gru_tc2<3>, gp, THREADS, smem_pair<3>(), s, 2, t->map_a1, t->map_w1h, t->map_rh,
+                         t->map_w2h, a);
+    else
+      launch_pdl_cluster(k_gru_tc2<1>, gp, THREADS, smem_pair<1>(), s, 2, t->map_a1, t->map_w1h, t->map_rh,
+                         t->map_w2h, a);
   } else {
     if (t->lbr) {
       if (t->tf32) launch_pdl(k_gru_tc<float, 1>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
@@ -1599,6 +1653,17 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
       for (int k = 0; k < 16; ++k) sum[k] += (double)h[b * 16 + k];
     }
     if (nb) {
+      // CTA timeline (globaltimer ns): kernel span, mean CTA busy span, spread of the CTA end times
+      unsigned long long s0 = ~0ull, e0 = ~0ull, s1 = 0, e1 = 0;
+      double busy = 0;
+      for (int b = 0; b < 1024; ++b) {
+        if (!h[b * 16 + 8]) continue;
+        const unsigned long long st = h[b * 16 + 14], en = h[b * 16 + 15];
+        s0 = st < s0 ? st : s0; s1 = st > s1 ? st : s1; e0 = en < e0 ? en : e0; e1 = en > e1 ? en : e1;
+        busy += (double)(en - st);
+      }
+      fprintf(stderr, "[gru_tc timeline] span_us=%.1f mean_cta_busy_us=%.1f start_spread_us=%.1f end_spread_us=%.1f\n",
+              (e1 - s0) * 1e-3, busy / nb * 1e-3, (s1 - s0) * 1e-3, (e1 - e0) * 1e-3);
       static const char *nm[16] = {"prod_wait_empty", "prod_wait_dep", "mma_wait_full", "mma_wait_tempty",
                                    "epi_z_wait_tfull", "epi_z_body_p1", "epi_z_body_p2", "-", "total",
                                    "tiles_p1", "tiles_p2", "epi_r_wait_tfull", "epi_r_body_p1", "epi_r_body_p2",
