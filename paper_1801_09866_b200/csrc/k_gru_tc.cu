@@ -1210,7 +1210,10 @@ __global__ void __maxnreg__(GRU_MAXREG)
           const uint32_t c0 = NA == 1 ? 0u : a.seg[sg].k0, c1 = NA == 1 ? KCt : a.seg[sg].k1;
           for (uint32_t c = c0; c < c1; ++c, ++kc) {
             t0 = clock64();
-            mbar_wait_cl(&m.full[stage], phase);          // both CTAs' bytes landed
+            // both CTAs' bytes landed (complete_tx on this barrier); the MMA reads them
+            // through the async proxy, so a CTA-scope wait suffices -- a cluster-scope
+            // acquire would invalidate this SM's L1 (CCTL.IVALL) on every stage
+            mbar_wait(&m.full[stage], phase);
             w_full += clock64() - t0;
             tc_fence_after();
             if (lane == 0) {
