@@ -1,5 +1,6 @@
 // api.cu -- the C ABI (include/rnnlm.h): engine creation, pools, weight
 // layouts, and the per-frame orchestration of rnnlm_query_batch.
+#include <nvtx3/nvToolsExt.h>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -151,6 +152,14 @@ void free_all(rnnlm *h) {
   h->ev_fork = h->ev_join = nullptr;
   h->side = nullptr;
 }
+
+// NVTX range over a host-side scope (tracing): the calls and the
+// enqueue of each hot-path row group show up on an nsys / ncu --nvtx timeline.
+// Header-only NVTX3: a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Every call that launches or synchronises runs on the handle's device and
 // restores the caller's current device on return (one handle per device).
@@ -431,6 +440,7 @@ int enqueue_step(rnnlm *h, const CallArgs &A, cudaStream_t s, bool timed) {
   // a small frame on the AUTO path: the whole step is ONE cooperative kernel
   if (h->gemv && h->cfg.gru_path == RNNLM_GRU_AUTO && A.n <= h->gemv_max_n &&
       A.n <= rnnlm_host::small_max_queries()) {
+    NvtxRange r("rnnlm fused small-frame step (a1-a7)");
     const int k = rnnlm_host::launch_small(P, A, h->gemv, h->bar, h->num_sms, s);
     cudaEventRecord(h->ev_join, s);                     // results ready (rnnlm_results_ready)
     if (timed) {
@@ -443,8 +453,12 @@ int enqueue_step(rnnlm *h, const CallArgs &A, cudaStream_t s, bool timed) {
     return k > 0 ? k : 0;
   }
   int k = 0;
-  k += rnnlm_host::launch_cache_front(P, A, s);
-  k += rnnlm_host::launch_commit(P, A, s);
+  {
+    NvtxRange r("rnnlm (a1-a4) cache front + commit");
+    k += rnnlm_host::launch_cache_front(P, A, s);
+    k += rnnlm_host::launch_commit(P, A, s);
+  }
+  NvtxRange r5("rnnlm (a5) gather + GRU, (a6-a7) score + result");
   cudaEvent_t fork = h->ev_fork;
   if (timed) cudaEventRecord(ev[1], s);                 // ms_cache ends at the commit
   const bool gemv = h->gemv && A.n <= h->gemv_max_n;
@@ -493,6 +507,7 @@ rnnlm_status rnnlm_query_batch(rnnlm_t *h, uint32_t n, const uint32_t *d_session
                                const uint32_t *d_parent, const uint32_t *d_word, float *d_score,
                                uint32_t *d_child, uint8_t *d_outcome, rnnlm_stream_t stream) {
   if (!h) return RNNLM_E_INVALID_ARG;
+  NvtxRange nv("rnnlm_query_batch");
   DeviceGuard dg(h);
   if (n == 0) return RNNLM_OK;
   if (n > h->cfg.max_queries_per_call) return RNNLM_E_INVALID_ARG;
@@ -544,6 +559,7 @@ rnnlm_status rnnlm_graph_create(rnnlm_t *h, uint32_t max_n, const uint32_t *d_n,
 
 rnnlm_status rnnlm_graph_launch(rnnlm_graph_t *g, rnnlm_stream_t stream) {
   if (!g) return RNNLM_E_INVALID_ARG;
+  NvtxRange nv("rnnlm_graph_launch");
   DeviceGuard dg(g->h);
   g->h->launches += (uint64_t)g->kernels;
   return cuda_status(cudaGraphLaunch(g->exec, reinterpret_cast<cudaStream_t>(stream)));
@@ -643,6 +659,7 @@ rnnlm_status rnnlm_results_ready(rnnlm_t *h, rnnlm_stream_t stream) {
 rnnlm_status rnnlm_log_normalizer(rnnlm_t *h, uint32_t n, const uint32_t *d_session,
                                   const uint32_t *d_history, float *d_log_z, rnnlm_stream_t stream) {
   if (!h) return RNNLM_E_INVALID_ARG;
+  NvtxRange nv("rnnlm_query_batch");
   DeviceGuard dg(h);
   if (n == 0) return RNNLM_OK;
   if (n > h->cfg.max_queries_per_call || !d_session || !d_history || !d_log_z) return RNNLM_E_INVALID_ARG;

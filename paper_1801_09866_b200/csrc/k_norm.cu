@@ -20,6 +20,10 @@
 // bf16 halves, h = hi + lo (lo = bf16(h - hi)), both multiplied with the bf16
 // output rows (two MMAs per K-step), so the contraction carries ~16
 // significant bits of h instead of bf16's 8 at no cost that matters here.
+// Output rows that are not bf16-exact are split the same way, Theta = Theta_hi
+// + Theta_lo, and a third MMA adds h_hi . Theta_lo (k_norm_tc<true>; the
+// dropped h_lo . Theta_lo is ~2^-18 relative): the normaliser then carries
+// ~16 significant bits of both operands in every math mode.
 // The MaxEnt terms: idx_k(v) = (alpha_k v + beta_k) mod M with
 // alpha_k = 237967^(k-1) and beta_k fixed by the context (the S:177
 // recurrence unrolled; M is a power of two, so mod M is a mask and the
@@ -44,14 +48,16 @@ using namespace rnnlm_tc;
 constexpr int NM = 128;                        // histories per tile (UMMA M)
 constexpr int NN = 256;                        // words per tile (UMMA N)
 constexpr int NK = 64;                         // K elements per stage (one 128-byte swizzle atom)
-constexpr int NST = 3;                         // smem stages
 constexpr int A_B = NM * NK * 2;               // 16 KB (hi or lo)
-constexpr int B_B = NN * NK * 2;               // 32 KB
-constexpr int STAGE = 2 * A_B + B_B;           // 64 KB
+constexpr int B_B = NN * NK * 2;               // 32 KB (Theta_hi or Theta_lo)
+// smem stages: [h_hi | h_lo | Theta_hi] (64 KB, 3 deep) or, with the Theta_lo
+// operand, [h_hi | h_lo | Theta_hi | Theta_lo] (96 KB, 2 deep)
+template <bool LO> __host__ __device__ constexpr int nst_of() { return LO ? 2 : 3; }
+template <bool LO> __host__ __device__ constexpr int stage_of() { return 2 * A_B + (LO ? 2 : 1) * B_B; }
+template <bool LO> constexpr size_t nsmem_of() { return 1024 + (size_t)nst_of<LO>() * stage_of<LO>() + 256; }
 constexpr int NEPI = 8;                        // epilogue warps
 constexpr int NTHREADS = (2 + NEPI) * 32;
 constexpr int MAXORD = 8;
-constexpr size_t NSMEM = 1024 + (size_t)NST * STAGE + 256;
 
 struct NormArgs {
   uint32_t n, H, V, nT, mt;
@@ -124,18 +130,29 @@ __global__ void k_norm_bias1(Params P, float *bias1) {
   if (v < P.V) bias1[v] = P.nce_b[v] + P.maxent[v & P.M_mask];
 }
 
-// fp32 output rows -> bf16 (only when the engine keeps no bf16 copy)
-__global__ void k_norm_theta16(const float *w, __nv_bfloat16 *o, size_t count) {
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
-    o[i] = __float2bfloat16_rn(w[i]);
+// fp32 output rows -> bf16 parts hi = bf16(w), lo = bf16(w - hi) (only when
+// the engine keeps no bf16 copy); *any_lo = 1 if some lo part is non-zero
+__global__ void k_norm_theta16(const float *w, __nv_bfloat16 *o, __nv_bfloat16 *lo, size_t count, int *any_lo) {
+  int nz = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w[i]);
+    const __nv_bfloat16 l = __float2bfloat16_rn(w[i] - __bfloat162float(hi));
+    o[i] = hi;
+    lo[i] = l;
+    nz |= __bfloat162float(l) != 0.0f;
+  }
+  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(any_lo, 1);
 }
 
 // Persistent GEMM + epilogue.  Tiles t -> (word tile j = t / mt, history
 // tile m = t % mt): consecutive tiles share the same output rows (L2 reuse).
 // warp 0: TMA producer; warp 1: TMEM owner + MMA issue; warps 2-9: epilogue
 // (TMEM lane quarter warp % 4, column half (warp - 2) / 4).
+template <bool LO>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_norm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_t, NormArgs a) {
+    k_norm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_t,
+              const __grid_constant__ CUtensorMap map_tl, NormArgs a) {
+  constexpr int NST = nst_of<LO>(), STAGE = stage_of<LO>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + NST * STAGE), *empty = full + NST, *tfull = empty + NST,
@@ -145,6 +162,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (threadIdx.x == 0) {
     prefetch_map(&map_a);
     prefetch_map(&map_t);
+    if (LO) prefetch_map(&map_tl);
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], NEPI * 32); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -169,6 +187,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tma_load_2d(d, &map_a, &full[stage], (int)(kc * NK), m0);                  // hi
           tma_load_2d(d + A_B, &map_a, &full[stage], (int)(a.H + kc * NK), m0);      // lo
           tma_load_2d(d + 2 * A_B, &map_t, &full[stage], (int)(kc * NK), n0);        // Theta rows
+          if (LO) tma_load_2d(d + 2 * A_B + B_B, &map_tl, &full[stage], (int)(kc * NK), n0);   // Theta_lo
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
@@ -190,6 +209,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int k = 0; k < NK / 16; ++k) {
             umma_bf16(tm, sdesc(d + k * 32), sdesc(d + 2 * A_B + k * 32), id, (kc | k) != 0);
             umma_bf16(tm, sdesc(d + A_B + k * 32), sdesc(d + 2 * A_B + k * 32), id, 1u);
+            if (LO) umma_bf16(tm, sdesc(d + k * 32), sdesc(d + 2 * A_B + B_B + k * 32), id, 1u);
           }
           umma_commit(&empty[stage]);
           if (kc == KC - 1) umma_commit(&tfull[acc]);
@@ -291,13 +311,14 @@ __global__ void __launch_bounds__(256) k_norm_reduce(uint32_t n, uint32_t nT, co
 struct NormState {
   uint32_t bmax = 0, bmax_pad = 0, nT = 0;
   __nv_bfloat16 *theta16 = nullptr;            // owned only when converted here
-  bool own_theta = false;
+  __nv_bfloat16 *theta_lo = nullptr;           // Theta - Theta_hi (bf16), when some entry is not bf16-exact
+  bool own_theta = false, lo = false;
   __nv_bfloat16 *A = nullptr;
   float *bias1 = nullptr;
   unsigned long long *beta = nullptr;
   uint32_t *nord = nullptr;
   float2 *part = nullptr;
-  CUtensorMap map_a, map_t;
+  CUtensorMap map_a, map_t, map_tl;
 };
 
 }  // namespace rnnlm_norm
@@ -311,6 +332,7 @@ void norm_release(void *state) {
   NormState *t = static_cast<NormState *>(state);
   if (!t) return;
   if (t->own_theta) cudaFree(t->theta16);
+  cudaFree(t->theta_lo);
   cudaFree(t->A);
   cudaFree(t->bias1);
   cudaFree(t->beta);
@@ -331,9 +353,20 @@ int norm_prepare(const Params &P, uint32_t bmax, void **state_out, cudaStream_t 
   if (P.nce_w16) {
     t->theta16 = const_cast<__nv_bfloat16 *>(P.nce_w16);
   } else {
+    int *d_any = nullptr, any = 0;
     ok = cudaMalloc(&t->theta16, (size_t)P.V * P.H * 2) == cudaSuccess;
     t->own_theta = ok;
-    if (ok) k_norm_theta16<<<1184, 256, 0, s>>>(P.nce_w, t->theta16, (size_t)P.V * P.H);
+    ok = ok && cudaMalloc(&t->theta_lo, (size_t)P.V * P.H * 2) == cudaSuccess &&
+         cudaMalloc(&d_any, sizeof(int)) == cudaSuccess && cudaMemsetAsync(d_any, 0, sizeof(int), s) == cudaSuccess;
+    if (ok) k_norm_theta16<<<1184, 256, 0, s>>>(P.nce_w, t->theta16, t->theta_lo, (size_t)P.V * P.H, d_any);
+    ok = ok && cudaMemcpyAsync(&any, d_any, sizeof(int), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+         cudaStreamSynchronize(s) == cudaSuccess;
+    cudaFree(d_any);
+    t->lo = any != 0;
+    if (!t->lo) {                               // bf16-exact rows: no third product
+      cudaFree(t->theta_lo);
+      t->theta_lo = nullptr;
+    }
   }
   ok = ok && cudaMalloc(&t->A, (size_t)t->bmax_pad * 2 * P.H * 2) == cudaSuccess &&
        cudaMemsetAsync(t->A, 0, (size_t)t->bmax_pad * 2 * P.H * 2, s) == cudaSuccess &&
@@ -344,7 +377,10 @@ int norm_prepare(const Params &P, uint32_t bmax, void **state_out, cudaStream_t 
   if (ok) k_norm_bias1<<<(P.V + 255) / 256, 256, 0, s>>>(P, t->bias1);
   ok = ok && make_map(&t->map_a, t->A, 2ull * P.H, t->bmax_pad, NM) &&
        make_map(&t->map_t, t->theta16, P.H, P.V, NN) &&
-       cudaFuncSetAttribute(k_norm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NSMEM) == cudaSuccess;
+       (!t->lo || make_map(&t->map_tl, t->theta_lo, P.H, P.V, NN)) &&
+       cudaFuncSetAttribute(k_norm_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsmem_of<false>()) == cudaSuccess &&
+       cudaFuncSetAttribute(k_norm_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsmem_of<true>()) == cudaSuccess;
+  if (ok && !t->lo) t->map_tl = t->map_t;
   if (!ok) {
     (void)cudaGetLastError();
     norm_release(t);
@@ -373,7 +409,8 @@ int launch_norm(const Params &P, void *state, uint32_t n, const uint32_t *sess, 
   launch_pdl(k_norm_prep, gp, 256, 0, s, P, n, sess, hist, t->A, t->beta, t->nord);
   uint32_t g = a.mt * a.nT;
   if (g > (uint32_t)num_sms) g = num_sms;
-  launch_pdl(k_norm_tc, g, NTHREADS, NSMEM, s, t->map_a, t->map_t, a);
+  if (t->lo) launch_pdl(k_norm_tc<true>, g, NTHREADS, nsmem_of<true>(), s, t->map_a, t->map_t, t->map_tl, a);
+  else launch_pdl(k_norm_tc<false>, g, NTHREADS, nsmem_of<false>(), s, t->map_a, t->map_t, t->map_tl, a);
   launch_pdl(k_norm_reduce, gp, 256, 0, s, n, t->nT, t->part, t->nord, log_z);
   return 3;
 }

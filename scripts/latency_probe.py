@@ -14,7 +14,7 @@ import paper_1801_09866_b200 as R  # noqa: E402
 from synth import CONFIGS, generate_model, generate_workload, model_dims  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "moderate"
-math = {"bf16": R.MATH_BF16, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3}[sys.argv[2] if len(sys.argv) > 2 else "bf16"]
+math = {"bf16": R.MATH_BF16, "fp32": R.MATH_FP32, "tf32x3": R.MATH_TF32X3, "bf16x3": R.MATH_BF16X3}[sys.argv[2] if len(sys.argv) > 2 else "bf16"]
 c = CONFIGS[cfg]
 d = model_dims(cfg)
 m = generate_model(d, seed=1234)

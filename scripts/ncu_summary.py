@@ -20,7 +20,11 @@ METRICS = {
     "dram_read_bytes": "dram__bytes_read.sum",
     "dram_write_bytes": "dram__bytes_write.sum",
     "dram_pct_peak": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-    "tensor_pipe_pct": "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    # tcgen05 utilisation: cycles the tensor pipe is busy over elapsed SM cycles -- agrees with
+    # the kernel's flop rate / (148 SMs x 8192 bf16 flop/clk x the SM clock under ncu)
+    "tensor_pipe_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "utchmma_bf16_ops": "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum",
+    "sm_clock_ghz": "sm__cycles_elapsed.avg.per_second",
     "tensor_mem_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "tensor_bf16_ops_pct": "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
     "l2_pct_peak": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -109,7 +113,7 @@ def main():
         R = full_report(a.report)
         summary["full"] = R
         md += ["## ncu --set full", "",
-               "| kernel | us | DRAM bytes | DRAM % | L2 % | tensor pipe % | tensor mem (TMEM) active % | SM % | regs | grid |",
+               "| kernel | us | DRAM bytes | DRAM % | L2 % | tensor pipe active % (sm__pipe_tensor_cycles_active) | sm__mem_tensor_cycles_active % | SM % | regs | grid |",
                "|---|---|---|---|---|---|---|---|---|---|"]
         for k, lst in R.items():
             for d in lst:
@@ -118,6 +122,18 @@ def main():
                           f" | {d.get('tensor_pipe_pct', 0):.1f} | {d.get('tensor_mem_pct', 0):.1f}"
                           f" | {d.get('sm_pct_peak', 0):.1f}"
                           f" | {d.get('registers', 0):.0f} | {d.get('grid', 0):.0f} |")
+        rec = [(k, d) for k, lst in R.items() for d in lst if d.get("utchmma_bf16_ops")]
+        if rec:
+            md += ["", "Tensor-pipe reconciliation: bf16 UTCHMMA ops (flops, incl. tile padding) / duration"
+                   " vs 148 SMs x 8192 flop/clk x the SM clock ncu ran at:", "",
+                   "| kernel | bf16 flops | us | TFLOP/s | SM GHz | peak at that clock | ratio | tensor pipe active % |",
+                   "|---|---|---|---|---|---|---|---|"]
+            for k, d in rec:
+                ghz = d.get("sm_clock_ghz", 0) / (1e9 if d.get("sm_clock_ghz", 0) > 1e3 else 1)
+                tf = d["utchmma_bf16_ops"] / (d["duration_us"] * 1e-6) / 1e12
+                pk = 148 * 8192 * ghz * 1e9 / 1e12
+                md.append(f"| {k} | {d['utchmma_bf16_ops']:.3e} | {d['duration_us']:.1f} | {tf:.0f} | {ghz:.3f}"
+                          f" | {pk:.0f} | {tf / pk:.3f} | {d.get('tensor_pipe_pct', 0):.1f} |")
     json.dump(summary, open(os.path.join(a.out, f"ncu_{a.tag}.json"), "w"), indent=1)
     open(os.path.join(a.out, f"ncu_{a.tag}.md"), "w").write("\n".join(md) + "\n")
     print("\n".join(md))

@@ -69,6 +69,10 @@ def run(dims, model, wl, key, math, warm=5, timed_from=None):
     return st, qps, d_score.cpu().numpy(), d_child.cpu().numpy().view(np.uint32)
 
 
+MATHS = {"bf16": R.MATH_BF16, "bf16x3": R.MATH_BF16X3, "tf32x3": R.MATH_TF32X3, "tf32": R.MATH_TF32,
+         "fp32": R.MATH_FP32}
+
+
 def sweep(a):
     cfg = a.config
     dims = model_dims(cfg)
@@ -77,13 +81,13 @@ def sweep(a):
     ref_st, _, ref_sc, ref_ch = run(dims, model, wl, "off", R.MATH_FP32)
     base = None
     for key in ("off", "round:3", "round:2", "round:1", "sign"):
-        st, qps, sc, ch = run(dims, model, wl, key, R.MATH_BF16)
+        st, qps, sc, ch = run(dims, model, wl, key, MATHS[a.math])
         assert np.array_equal(ch, ref_ch), "QHIT decisions / handles differ across modes"
         dev = np.abs(sc.astype(np.float64) - ref_sc.astype(np.float64))
         if base is None:
             base = st["gru_computations"]
         print(json.dumps({
-            "sweep": "compression", "config": cfg, "mode": key, "math": "bf16", "sessions": wl.S,
+            "sweep": "compression", "config": cfg, "mode": key, "math": a.math, "sessions": wl.S,
             "frames": wl.frames, "queries": st["total_queries"],
             "query_cache_hit_rate": st["query_hits"] / st["total_queries"],
             "hidden_cache_hit_rate": st["hidden_hits"] / max(1, st["hidden_lookups"]),
@@ -100,7 +104,7 @@ def ablation(a):
     dims = model_dims(a.config)
     model = generate_model(dims, seed=1234)
     wl = generate_workload(1, a.frames, cfg["B_s"], dims.V, seed=7)
-    math = R.MATH_BF16 if a.math == "bf16" else R.MATH_FP32
+    math = MATHS[a.math]
     st, qps_frame, sc_f, ch_f = run(dims, model, wl, "off", math, warm=0)
     # one call per query
     eng = R.RNNLM.from_dims(dims, model, key_mode=R.KEY_OFF, math=math, num_sessions=1,

@@ -113,3 +113,23 @@ def test_log_probabilities_sum_to_one_on_gpu():
     p1 = np.exp(sc1.cpu().numpy().astype(np.float64) - lz1)
     assert abs(p1.sum() - 1.0) < 1e-5
     assert abs(lz1 - lz0) > 1e-3          # a different history, a different normaliser
+
+
+@pytest.mark.parametrize("math", [MATH_FP32, MATH_TF32, MATH_BF16])
+def test_off_grid_output_weights(math):
+    """Output rows NOT on the bf16 grid (U(-0.1, 0.1) fp32, SPEC S:62 scale):
+    the normaliser splits Theta into bf16 hi + lo parts and adds the
+    h_hi . Theta_lo product, so log Z stays far inside 1e-3 (a single bf16
+    rounding of Theta alone gives ~1e-3 at H = 256).  On the BF16 engine the
+    scores themselves round Theta (nce_w is kept fp32 when not bf16-exact)."""
+    d = ModelDims(V=3000, E=256, H=256, maxent_log2=16, N=3)
+    m = generate_model(d, seed=5, scale=0.1, bf16_grid=False)
+    wl = generate_workload(1, 10, 64, d.V, seed=11)
+    cap = wl.max_histories_hint()
+    eng = RNNLM.from_dims(d, m, key_mode=KEY_SIGN, math=math, num_sessions=1,
+                          max_queries_per_call=512, max_histories_per_session=cap)
+    orc = O.Oracle(O.make_config(d.V, d.E, d.H, d.maxent_log2, d.N, O.KEY_SIGN, 0, 1, 1, cap), m)
+    replay_compare(eng, orc, wl, tol_score=1e-2, tol_state=1e-2)
+    nh = orc.num_handles(0)[0]
+    err = _check(eng, orc, [(0, h) for h in range(nh)])
+    assert err < 1e-4, err
