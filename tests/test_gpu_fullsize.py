@@ -23,9 +23,9 @@ import pytest
 import torch
 
 import oracle as O
-from paper_1801_09866_b200 import KEY_SIGN, MATH_BF16, MISS, QHIT, INVALID, RNNLM
+from paper_1801_09866_b200 import KEY_SIGN, MATH_BF16, MATH_BF16X3, MISS, QHIT, INVALID, RNNLM
 from synth import generate_model, generate_workload, model_dims
-from tests.parity_util import _dev
+from tests.parity_util import _dev, replay_compare
 
 pytestmark = pytest.mark.gpu
 
@@ -107,3 +107,23 @@ def test_multi_config_full_size_sampled():
     for s in range(S):
         msk = (wl.session == s) & (outc != QHIT)
         assert np.array_equal(child[msk], np.arange(1, msk.sum() + 1, dtype=np.uint32))
+
+
+@pytest.mark.parametrize("math", [MATH_BF16X3, MATH_BF16])
+def test_multi_config_one_session_replayed(math):
+    """configs[4] launch configuration (64 streams x 2,048 queries per call on
+    the large model, sign keys, cache on) with session 0 replayed through the
+    oracle query by query: outcomes, handles, slots, codes and the session's
+    stats bit-exact, scores / new states within the path's tolerance, parent
+    states taken from the GPU (replay protocol)."""
+    d = model_dims("multi")
+    m = generate_model(d, seed=1234)
+    wl = generate_workload(64, 100, 2048, d.V, seed=7)
+    cap = wl.max_histories_hint()
+    eng = RNNLM.from_dims(d, m, key_mode=KEY_SIGN, math=math, num_sessions=64,
+                          max_queries_per_call=wl.n_per_frame, max_histories_per_session=cap,
+                          max_queries_per_session_call=2048)
+    orc = O.Oracle(O.make_config(d.V, d.E, d.H, d.maxent_log2, d.N, O.KEY_SIGN, 0, 1, 1, cap), m)
+    tol = 1e-5 if math == MATH_BF16X3 else 1e-3
+    rep = replay_compare(eng, orc, wl, tol_score=tol, tol_state=tol, only_session=0)
+    assert rep["queries"] == 100 * 2048 and rep["miss"] > 200, rep

@@ -244,3 +244,32 @@ def test_staggered_and_selected_workloads_are_well_formed():
         assert np.all(w.session[w.parent_ref[m]] == w.session[m])
     a, b = wl.select_sessions(1, 2), st.select_sessions(1, 2)
     assert np.array_equal(a.word[:b.n_total], b.word) and np.array_equal(a.parent_ref[:b.n_total], b.parent_ref)
+
+
+def test_threaded_frames_equal_single_thread():
+    """The oracle evaluates a frame's scores and GRUs after its (sequential)
+    decisions, optionally on several host threads (bench.py's cpu_baseline);
+    the arithmetic of each item is unchanged, so results are bitwise those of
+    one thread."""
+    d = ModelDims(V=500, E=32, H=32, maxent_log2=12, N=3)
+    m = generate_model(d, seed=3)
+    wl = generate_workload(2, 30, 64, d.V, seed=5, dur=(2, 6), eps=0.1)
+    outs = []
+    old = O.threads()
+    try:
+        for th in (1, 4):
+            O.threads(th)
+            orc = engine(d, m, O.KEY_SIGN, S=2, cap=wl.max_histories_hint())
+            child = np.zeros(wl.n_total, np.uint32)
+            score = np.zeros(wl.n_total, np.float32)
+            for t in range(wl.frames):
+                sl = wl.frame_slice(t)
+                par = O.resolve_parents(wl.parent_ref[sl], child)
+                sc, ch, _ = orc.query_frame(wl.session[sl], par, wl.word[sl])
+                score[sl], child[sl] = sc, ch
+            outs.append((score, orc.read_states(0, np.arange(orc.num_handles(0)[0], dtype=np.uint32)), orc.stats()))
+    finally:
+        O.threads(old)
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
+    assert outs[0][2] == outs[1][2]
