@@ -593,14 +593,19 @@ def run_ours(args):
 
 
 def run_e2e(args, bench, dev, world):
-    """Host-buffer path through the public API: per step ONE H2D copy of the
-    decoder's packed queries (parent reference i64 = index of the earlier
-    query whose child is the parent, session u32, word u32) from pinned
-    memory, rnnlm_resolve_parents (reference -> handle on the device),
-    rnnlm_query_batch, (N > 1) the NCCL all-gather of (score, child), ONE D2H
-    copy of the (gathered) results into pinned memory, synchronise.  The
-    engine restarts its streams (reset) and replays the untimed frames on the
-    device first."""
+    """Host-buffer path through the public API, as a streaming decoder runs
+    it: per step ONE H2D copy of the decoder's packed queries (parent
+    reference i64 = index of the earlier query whose child is the parent,
+    session u32, word u32) from pinned memory, rnnlm_resolve_parents
+    (reference -> handle on the device), rnnlm_query_batch, (N > 1) the NCCL
+    all-gather of (score, child), ONE D2H copy of the (gathered) results into
+    pinned memory, and the host waits for that step's results.  Double
+    buffered: step i + 1's H2D (copy stream) overlaps step i's kernels and
+    step i's D2H (copy stream) overlaps step i + 1's kernels; the host reads
+    step i's results after enqueueing step i + 1 (parents are references
+    resolved on the device, so the next frame does not wait for the host).
+    The engine restarts its streams (reset) and replays the untimed frames on
+    the device first."""
     import torch
     import torch.distributed as dist
 
@@ -622,35 +627,61 @@ def run_e2e(args, bench, dev, world):
         blk[i, 3 * n:] = wl.word[sl].view(np.int32)
     h_in_all = torch.from_numpy(blk).pin_memory()
     out_rows = world * n
-    h_out = torch.empty(2 * out_rows, dtype=torch.int32).pin_memory()
-    d_in = torch.empty(4 * n, dtype=torch.int32, device=dev)
-    d_ref = d_in[:2 * n].view(torch.int64)
-    d_sess, d_word = d_in[2 * n:3 * n], d_in[3 * n:]
+    h_out = [torch.empty(2 * out_rows, dtype=torch.int32).pin_memory() for _ in range(2)]
+    d_in = [torch.empty(4 * n, dtype=torch.int32, device=dev) for _ in range(2)]
     d_par = torch.empty(n, dtype=torch.int32, device=dev)
     d_score = torch.empty(n, dtype=torch.float32, device=dev)
-    d_out = torch.empty((out_rows, 2), dtype=torch.int32, device=dev)
+    d_out = [torch.empty((out_rows, 2), dtype=torch.int32, device=dev) for _ in range(2)]
+    main = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    ev_in = [torch.cuda.Event() for _ in frames]        # step i's inputs on the device
+    ev_used = [torch.cuda.Event() for _ in frames]      # step i's inputs consumed, outputs packed
+    ev_out = [torch.cuda.Event() for _ in frames]       # step i's results in host memory
 
-    def host_step(i, t):
+    def upload(i):
+        b = i % 2
+        if i >= 2:
+            h2d.wait_event(ev_used[i - 2])              # the buffer's previous step has consumed it
+        with torch.cuda.stream(h2d):
+            d_in[b].copy_(h_in_all[i], non_blocking=True)
+            ev_in[i].record(h2d)
+
+    def compute(i, t):
+        b = i % 2
         sl = wl.frame_slice(t)
-        d_in.copy_(h_in_all[i], non_blocking=True)
+        main.wait_event(ev_in[i])
+        d_ref, d_sess, d_word = d_in[b][:2 * n].view(torch.int64), d_in[b][2 * n:3 * n], d_in[b][3 * n:]
         R.resolve_parents(d_ref, bench.d_child, d_par)
         eng.query_batch(d_sess, d_par, d_word, score=d_score, child=bench.d_child[sl], want_outcome=False)
+        if i >= 2:
+            main.wait_event(ev_out[i - 2])              # d_out[b] of step i - 2 has been read back
         if world > 1:
-            all_gather_results(d_score, bench.d_child[sl], out=d_out)
+            all_gather_results(d_score, bench.d_child[sl], out=d_out[b])
         else:
-            d_out[:, 0].copy_(d_score.view(torch.int32))
-            d_out[:, 1].copy_(bench.d_child[sl])
-        h_out.copy_(d_out.view(-1), non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+            d_out[b][:, 0].copy_(d_score.view(torch.int32))
+            d_out[b][:, 1].copy_(bench.d_child[sl])
+        ev_used[i].record(main)
+        d2h.wait_event(ev_used[i])
+        with torch.cuda.stream(d2h):
+            h_out[b].copy_(d_out[b].view(-1), non_blocking=True)
+            ev_out[i].record(d2h)
 
-    for i in range(args.warmup):
-        host_step(i, frames[i])
+    def run(lo, hi):
+        upload(lo)
+        for i in range(lo, hi):
+            if i + 1 < hi:
+                upload(i + 1)
+            compute(i, frames[i])
+            if i > lo:
+                ev_out[i - 1].synchronize()             # the host reads step i - 1's results
+        ev_out[hi - 1].synchronize()
+
+    run(0, args.warmup)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for i in range(args.warmup, len(frames)):
-        host_step(i, frames[i])
+    run(args.warmup, len(frames))
     torch.cuda.synchronize()
     secs = time.perf_counter() - t0
     if world > 1:
@@ -659,9 +690,11 @@ def run_e2e(args, bench, dev, world):
         secs = float(tt[0])
     return {"value": n * args.steps * world / secs, "unit": UNIT,
             "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * out_rows,
-            "note": "wall clock per step: H2D (parent reference i64, session u32, word u32) from pinned memory, "
-                    "device-side reference -> handle resolution, the step, the all-gather (N > 1), D2H of the "
-                    "(score, child) results, synchronise; the same frames as the value pass; max over ranks"}
+            "note": "wall clock over the steps: per step H2D (parent reference i64, session u32, word u32) from "
+                    "pinned memory, device-side reference -> handle resolution, the step, the all-gather (N > 1), "
+                    "D2H of the (score, child) results, the host waiting for them; double-buffered copies on "
+                    "copy streams (step i + 1's upload and step i - 1's read-back overlap step i); the same "
+                    "frames as the value pass; max over ranks"}
 
 
 # ----------------------------------------------------------------------------- configs[0]-[3]

@@ -306,7 +306,8 @@ rnnlm_status rnnlm_create(const rnnlm_config *cfg, const rnnlm_weights *w, rnnlm
     chk(upload(h, const_cast<float **>(&P.b1), b1.data(), b1.size()));
     chk(upload(h, const_cast<float **>(&P.w2), w2.data(), w2.size()));
   } else {
-    if (c.math == RNNLM_MATH_BF16)
+    // bf16 embedding rows: the BF16 operands, and BF16X3's x_hi part when every entry is bf16-exact
+    if (c.math == RNNLM_MATH_BF16 || (c.math == RNNLM_MATH_BF16X3 && all_bf16_exact(w->emb, V * E)))
       chk(upload_bf16(h, const_cast<__nv_bfloat16 **>(&P.emb16), w->emb, V * E));
     if (st == RNNLM_OK &&
         rnnlm_host::gru_tc_prepare(w, c.vocab, c.embed, c.hidden, c.math == RNNLM_MATH_TF32 || c.math == RNNLM_MATH_TF32X3,

@@ -232,7 +232,14 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
         const float4 *x = reinterpret_cast<const float4 *>(a.emb + (size_t)a.row_word[r] * a.E);
         const float4 *h = reinterpret_cast<const float4 *>(a.state + (size_t)a.row_src[r] * a.H);
         uint2 *dst = reinterpret_cast<uint2 *>(a.a1 + (size_t)r * 3 * K1);
-        for (uint32_t i0 = lane; i0 < nk; i0 += 128) {
+        uint32_t i1 = 0;                              // first float4 index taken from fp32 rows
+        if (!a.x3_xlo && a.emb16) {                   // bf16-exact embedding: x = x_hi, copied from the bf16 rows
+          const uint4 *x16 = reinterpret_cast<const uint4 *>(a.emb16 + (size_t)a.row_word[r] * a.E);
+          uint4 *d16 = reinterpret_cast<uint4 *>(dst);
+          for (uint32_t i = lane; i < a.E / 8; i += 32) d16[i] = __ldg(x16 + i);
+          i1 = nx;
+        }
+        for (uint32_t i0 = i1 + lane; i0 < nk; i0 += 128) {
           float4 v[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
