@@ -1599,7 +1599,10 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   // phases apart (each phase's weights hot in L2) beats interleaving them tightly
   // CTA pair (5-stage ring): lag 32: 537-540, 48: 543-545, 64: 548-551, 96: 543-553,
   // 128: 546-549 M q/s, kernel 199.5 / 196.5 / 193.3 / 193.7 / 195.4 us (profiles/ab_lag_r1.txt)
-  a.lag = getenv("RNNLM_TC_LAG") ? (uint32_t)atoi(getenv("RNNLM_TC_LAG")) : (t->pair ? 64u : 128u);
+  // BF16X3 on the pair: every phase-1 tile before any phase-2 tile -- lag 16 / 32 / 64 / 128 / 1000:
+  // 264 / 248 / 235 / 228 / 228 us per bench step (profiles/ab_lag_r2.txt)
+  a.lag = getenv("RNNLM_TC_LAG") ? (uint32_t)atoi(getenv("RNNLM_TC_LAG"))
+                                 : (t->pair ? (t->x3 ? 1000u : 64u) : 128u);
   a.diag = t->diag;
   a.bz = t->bz; a.br = t->br;
   a.bn2 = P.H % BN ? UB : BN;
