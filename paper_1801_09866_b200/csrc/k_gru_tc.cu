@@ -629,14 +629,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
 // r.h is, on the bf16 path, the bf16 copy in the row's A1 row (the value
 // phase 1 multiplied); on the TF32 path the exact fp32 state.
 template <typename T>
-__device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tbase, uint32_t row, bool valid,
-                                           int gate, uint32_t ub, uint8_t *stg, uint32_t lane) {
-  const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB;
-  const uint32_t u0 = ub * UB;
+__device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tacc, uint32_t row, bool valid,
+                                           int half, uint32_t ub, uint8_t *stg, uint32_t lane) {
+  // the two epilogue warps of a TMEM lane quarter split the tile's 128 units:
+  // each takes 64 units, their z columns (tacc + u) and r columns (tacc + 128
+  // + u), so both do the same work (r.h, with its parent-state loads and
+  // operand-part stores, costs ~2-3x z)
+  const uint32_t u0 = ub * UB + half * 64;
 #pragma unroll 1
-  for (int c = 0; c < UB / 32; ++c) {
+  for (int cc = 0; cc < 4; ++cc) {
+    const int gate = cc >> 1, c = cc & 1;               // z chunks 0, 1, then r chunks 0, 1
+    const float *bias = a.bzr + (size_t)ub * 2 * UB + gate * UB + half * 64;
     float v[32], b[32];
-    tmem_ld32(tbase + c * 32, v);
+    tmem_ld32(tacc + gate * UB + half * 64 + c * 32, v);
     ld_bias16(bias + c * 32, b);
     ld_bias16(bias + c * 32 + 16, b + 16);
     if (gate == 0) {
@@ -941,7 +946,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
         mbar_arrive(&m.tempty[acc]);
         b1 += clock64() - t0;
       } else if (x.kind == 0) {
-        epi_phase1<T>(a, tbase, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
+        epi_phase1<T>(a, tbase - half * hw, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
         // publish this warp's z / r.h columns to the phase-2 tiles of the M-tile
@@ -1011,6 +1016,13 @@ __device__ __forceinline__ void mbar_wait_cl(uint64_t *b, uint32_t parity) {
       "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+// arrive on a (possibly remote) barrier with the default CTA-scope release: the
+// TMEM-free signal only orders this warp's completed tcgen05.ld (waited and
+// fenced with tcgen05.fence::before_thread_sync) before the peer's MMA, no
+// global memory, so it needs no cluster-scope release (MEMBAR) per tile
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
@@ -1266,21 +1278,24 @@ __global__ void __maxnreg__(GRU_MAXREG)
         tmem_ld16(tbase, v);
         tmem_ld_wait();
       } else if (x.kind == 0) {
-        epi_phase1<__nv_bfloat16>(a, tbase, row, valid, half, x.j, stg, lane);
+        epi_phase1<__nv_bfloat16>(a, tbase - half * (BN / 2), row, valid, half, x.j, stg, lane);
       } else {
         wait_phase1(a.done1 + x.m, target);
         epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), BN / 2, stg, lane);
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cl(tempty0 + acc * 8);
+      if (lane == 0) mbar_arrive_remote(tempty0 + acc * 8);
       if (x.kind == 0) {
-        // publish this warp's z / r.h columns to the phase-2 tiles of the pair tile
+        // publish this CTA's z / r.h columns to the phase-2 tiles of the pair tile:
+        // every writer orders its generic stores for the async proxy (the phase-2
+        // TMA reads r.h), the 8 epilogue warps meet on a named barrier, and one
+        // thread releases them at GPU scope with ONE fence + counter add
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
+        asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32) : "memory");
+        if (warp == 2 && lane == 0) {
           __threadfence();
-          atomicAdd(a.done1 + x.m, 1u);
+          atomicAdd(a.done1 + x.m, (uint32_t)EPI_WARPS);
         }
         b1 += clock64() - t0;
       } else {
