@@ -205,6 +205,21 @@ __host__ __device__ __forceinline__ uint32_t seg_chunks(const TcArgs &a) {
   return n;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {       // ns (diag 5 timeline)
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// diag 5: the gather's last block end time, max over blocks (prof slot 1023 * 16)
+struct GatherClock {
+  unsigned long long *prof;
+  __device__ ~GatherClock() {
+    if (!prof) return;
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(prof + 1023 * 16, gtimer());
+  }
+};
+
 // ---------------------------------------------------------------- A gather
 // Phase-1 A operand: row r = [E[word_r] | bf16(state[src_r])] (bf16, K-major,
 // dense), one warp per row, 16-byte loads/stores (the paper's per-frame
@@ -213,6 +228,7 @@ __host__ __device__ __forceinline__ uint32_t seg_chunks(const TcArgs &a) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
   pdl_entry();
+  const GatherClock clock_end{a.prof};
   const uint32_t Q = a.counts[1];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -410,11 +426,6 @@ __device__ __forceinline__ Tile tile_of(uint32_t t, uint32_t mt, uint32_t n1, ui
   return x;
 }
 
-__device__ __forceinline__ unsigned long long gtimer() {       // ns (diag 5 timeline)
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1099,6 +1110,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
               TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr int STP = stp_of<NA>();
+  const unsigned long long t_entry = a.prof ? gtimer() : 0ull;   // diag 5: kernel entry (before setup)
   const SmemP m = carve_pair<NA>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -1132,7 +1144,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   const uint32_t qempty0 = mapa(smem_u32(&m.qempty[0]), 0);
   unsigned long long *prof = a.prof ? a.prof + blockIdx.x * 16 : nullptr;
   const unsigned long long k_t0 = clock64();
-  if (prof && threadIdx.x == 0) prof[14] = gtimer();
+  if (prof && threadIdx.x == 0) { prof[14] = gtimer(); prof[7] = t_entry; }
 
   // tile id of ring slot `it`; one lane releases the slot on the leader's qempty
   auto take = [&](uint32_t it, bool release) -> uint32_t {
@@ -1641,10 +1653,13 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   uint32_t bps = t->tf32 ? 4u : 3u;
   if (const char *e = getenv("RNNLM_TC_GATHER_BPS")) bps = (uint32_t)atoi(e);
   if (gg > (uint32_t)num_sms * bps) gg = num_sms * bps;
+  // side-stream fork before the gather (RNNLM_FORK_EARLY=1; A/B) or after it
+  static const bool fork_early = getenv("RNNLM_FORK_EARLY") && atoi(getenv("RNNLM_FORK_EARLY")) != 0;
+  if (ev_fork && fork_early) cudaEventRecord(ev_fork, s);
   if (t->tf32) launch_pdl(k_gather_a1<float>, gg, 256, 0, s, a);
   else launch_pdl(k_gather_a1<__nv_bfloat16>, gg, 256, 0, s, a);
   if (ev_gathered) cudaEventRecord(ev_gathered, s);
-  if (ev_fork) cudaEventRecord(ev_fork, s);
+  if (ev_fork && !fork_early) cudaEventRecord(ev_fork, s);
   if (t->pair) {
     uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / BN) * 2;
     const uint32_t cap = (uint32_t)num_sms & ~1u;
@@ -1675,7 +1690,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     cudaStreamSynchronize(s);
     int nb = 0;
     double sum[16] = {0};
-    for (int b = 0; b < 1024; ++b) {
+    for (int b = 0; b < 1023; ++b) {
       if (!h[b * 16 + 8]) continue;
       ++nb;
       for (int k = 0; k < 16; ++k) sum[k] += (double)h[b * 16 + k];
@@ -1684,14 +1699,21 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
       // CTA timeline (globaltimer ns): kernel span, mean CTA busy span, spread of the CTA end times
       unsigned long long s0 = ~0ull, e0 = ~0ull, s1 = 0, e1 = 0;
       double busy = 0;
-      for (int b = 0; b < 1024; ++b) {
+      for (int b = 0; b < 1023; ++b) {
         if (!h[b * 16 + 8]) continue;
         const unsigned long long st = h[b * 16 + 14], en = h[b * 16 + 15];
         s0 = st < s0 ? st : s0; s1 = st > s1 ? st : s1; e0 = en < e0 ? en : e0; e1 = en > e1 ? en : e1;
         busy += (double)(en - st);
       }
-      fprintf(stderr, "[gru_tc timeline] span_us=%.1f mean_cta_busy_us=%.1f start_spread_us=%.1f end_spread_us=%.1f\n",
-              (e1 - s0) * 1e-3, busy / nb * 1e-3, (s1 - s0) * 1e-3, (e1 - e0) * 1e-3);
+      unsigned long long en0 = ~0ull;
+      for (int b = 0; b < 1023; ++b)
+        if (h[b * 16 + 8] && h[b * 16 + 7] && h[b * 16 + 7] < en0) en0 = h[b * 16 + 7];
+      const unsigned long long gend = h[1023 * 16];
+      fprintf(stderr, "[gru_tc timeline] span_us=%.1f mean_cta_busy_us=%.1f start_spread_us=%.1f end_spread_us=%.1f"
+              " gather_end_to_first_entry_us=%.1f first_entry_to_first_start_us=%.1f\n",
+              (e1 - s0) * 1e-3, busy / nb * 1e-3, (s1 - s0) * 1e-3, (e1 - e0) * 1e-3,
+              (gend && en0 != ~0ull) ? ((double)en0 - (double)gend) * 1e-3 : -1.0,
+              en0 != ~0ull ? ((double)s0 - (double)en0) * 1e-3 : -1.0);
       static const char *nm[16] = {"prod_wait_empty", "prod_wait_dep", "mma_wait_full", "mma_wait_tempty",
                                    "epi_z_wait_tfull", "epi_z_body_p1", "epi_z_body_p2", "-", "total",
                                    "tiles_p1", "tiles_p2", "epi_r_wait_tfull", "epi_r_body_p1", "epi_r_body_p2",
