@@ -177,6 +177,7 @@ struct TcArgs {
   uint32_t *done1;                 // per M-tile phase-1 epilogue arrivals (zeroed by the gather)
   uint32_t *tile_ctr;              // dynamic tile scheduler (zeroed by the gather)
   uint32_t lag;                    // phase-2 tiles trail phase-1 tiles by this many M-tiles
+  uint32_t gm;                     // CTA pair, separated phases: tile groups of gm M-tiles (see tile_of)
   uint32_t diag;                   // timing diagnostics: 1 no MMA, 2 no TMA, 3 no epilogue, 4 = 3 + no phase
                                    // dependency, 6 = 1 + 2 (results invalid); 5 cycle counters (results valid)
   unsigned long long *prof;        // diag 5: per-CTA cycle counters, else nullptr
@@ -410,8 +411,25 @@ struct Tile {
   uint32_t kind, m, j;             // kind 0: phase 1, 1: phase 2
 };
 
-__device__ __forceinline__ Tile tile_of(uint32_t t, uint32_t mt, uint32_t n1, uint32_t n2, uint32_t L) {
+// Fully separated phases (L >= mt) in groups of gm M-tiles: inside a group the
+// tiles run N-tile-major, so gm consecutive tiles read the same weight chunks
+// at about the same time (the L2 serves concurrent identical requests once);
+// gm = 1 is M-tile-major (the n1 / n2 tiles of an M-tile share its A rows).
+__device__ __forceinline__ void grouped(uint32_t t, uint32_t mt, uint32_t n, uint32_t gm, uint32_t &m, uint32_t &j) {
+  const uint32_t g = t / (gm * n), r = t - g * gm * n;
+  const uint32_t gsz = mt - g * gm < gm ? mt - g * gm : gm;
+  j = r / gsz;
+  m = g * gm + r % gsz;
+}
+
+__device__ __forceinline__ Tile tile_of(uint32_t t, uint32_t mt, uint32_t n1, uint32_t n2, uint32_t L,
+                                        uint32_t gm = 1) {
   Tile x;
+  if (gm > 1 && L >= mt) {
+    if (t < mt * n1) { x.kind = 0; grouped(t, mt, n1, gm, x.m, x.j); }
+    else { x.kind = 1; grouped(t - mt * n1, mt, n2, gm, x.m, x.j); }
+    return x;
+  }
   const uint32_t a = L * n1, b = (mt - L) * (n1 + n2);
   if (t < a) {
     x.kind = 0; x.m = t / n1; x.j = t % n1;
@@ -635,6 +653,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
   tmem_ld16(taddr + 16, v + 16);
 }
 
+// Epilogue knock-outs for timing experiments only (build flag -DEPI_KO=bits, results
+// invalid): 1 no global loads of parent states / z, 2 no global stores, 4 no code
+// encoding, 8 no transcendental math.  The default build has none.
+#ifndef EPI_KO
+#define EPI_KO 0
+#endif
+constexpr bool KO_LOAD = EPI_KO & 1, KO_STORE = EPI_KO & 2, KO_ENC = EPI_KO & 4, KO_MATH = EPI_KO & 8;
+
 // Phase-1 epilogue of one thread: row `row` of the tile, the 128 z columns
 // (gate 0) or r columns (gate 1) of unit block ub.  The parent state h of
 // r.h is, on the bf16 path, the bf16 copy in the row's A1 row (the value
@@ -657,7 +683,7 @@ __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tacc, uint3
     ld_bias16(bias + c * 32 + 16, b + 16);
     if (gate == 0) {
       tmem_ld_wait();
-      if (valid) {
+      if (valid && !KO_STORE) {
         float4 *zq = reinterpret_cast<float4 *>(a.g_z) + zq4(row, u0 + c * 32, a.H);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -667,25 +693,25 @@ __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tacc, uint3
     } else {
       float hv[32];
       if (sizeof(T) == 2 && !a.x3) {
-        coop_load<64>(stg, valid ? a.a1 + (size_t)row * (a.E + a.H) + a.E + u0 + c * 32 : nullptr, lane);
+        coop_load<64>(stg, valid && !KO_LOAD ? a.a1 + (size_t)row * (a.E + a.H) + a.E + u0 + c * 32 : nullptr, lane);
         own_row_bf16(stg, lane, hv);
       } else {
-        coop_load<128>(stg, valid ? a.state + (size_t)a.row_src[row] * a.H + u0 + c * 32 : nullptr, lane);
+        coop_load<128>(stg, valid && !KO_LOAD ? a.state + (size_t)a.row_src[row] * a.H + u0 + c * 32 : nullptr, lane);
         own_row_f32(stg, lane, hv);
       }
       tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) hv[j] *= sigm(v[j] + b[j]);
+      for (int j = 0; j < 32; ++j) hv[j] *= KO_MATH ? v[j] + b[j] : sigm(v[j] + b[j]);
       __syncwarp();
       if constexpr (sizeof(T) == 2) {
         if (!a.x3) {
           put_row_bf16(stg, lane, hv);
-          coop_store<64>(stg, valid ? a.g_rh16 + (size_t)row * a.H + u0 + c * 32 : nullptr, lane);
+          coop_store<64>(stg, valid && !KO_STORE ? a.g_rh16 + (size_t)row * a.H + u0 + c * 32 : nullptr, lane);
         } else {  // BF16X3: r.h as [hi | mid | lo] rows of 3H
 #pragma unroll 1
           for (int p = 0; p < 3; ++p) {
             put_row_bf16_part(stg, lane, hv);
-            coop_store<64>(stg, valid ? a.g_rh16 + (size_t)row * 3 * a.H + p * a.H + u0 + c * 32 : nullptr, lane);
+            coop_store<64>(stg, valid && !KO_STORE ? a.g_rh16 + (size_t)row * 3 * a.H + p * a.H + u0 + c * 32 : nullptr, lane);
           }
         }
       } else if (!a.x3) {
@@ -724,7 +750,7 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
   for (uint32_t c = 0; c < units / 32; ++c) {           // chunks of 32 units
     float v[32], b[32], z[32], h[32];
     tmem_ld32(tbase + c * 32, v);
-    if (live) {
+    if (live && !KO_LOAD) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float4 t = zq[(c * 8 + j) << 7];
@@ -733,15 +759,15 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
     }
     ld_bias16(a.bh + n0 + c * 32, b);
     ld_bias16(a.bh + n0 + c * 32 + 16, b + 16);
-    coop_load<128>(stg, hp ? hp + c * 32 : nullptr, lane);
+    coop_load<128>(stg, hp && !KO_LOAD ? hp + c * 32 : nullptr, lane);
     own_row_f32(stg, lane, h);
     tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) h[j] = (1.0f - z[j]) * h[j] + z[j] * tanh_fast(v[j] + b[j]);
+    for (int j = 0; j < 32; ++j) h[j] = (1.0f - z[j]) * h[j] + z[j] * (KO_MATH ? v[j] + b[j] : tanh_fast(v[j] + b[j]));
     __syncwarp();
     put_row_f32(stg, lane, h);
-    coop_store<128>(stg, hout ? hout + c * 32 : nullptr, lane);
-    if (a.cache && live) hs += encode32(key_spec(a), h, n0 + c * 32, code);
+    coop_store<128>(stg, hout && !KO_STORE ? hout + c * 32 : nullptr, lane);
+    if (a.cache && live && !KO_ENC) hs += encode32(key_spec(a), h, n0 + c * 32, code);
   }
   if (a.cache && live) atomicAdd(&a.codehash[dst], hs);
 }
@@ -1175,7 +1201,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
           t = take(it, true);
         }
         if (t == NO_TILE) break;
-        const Tile x = tile_of(t, mt, n1, n2, L);
+        const Tile x = tile_of(t, mt, n1, n2, L, a.gm);
         const uint32_t m0 = x.m * 2 * BM + rank * BM;
         const uint32_t b0row = x.j * BN + rank * (BN / 2);
         if (x.kind == 1 && a.diag != 4) {
@@ -1275,7 +1301,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
     for (uint32_t it = 0;; ++it) {
       const uint32_t t = take(it, lane == 0);
       if (t == NO_TILE) break;
-      const Tile x = tile_of(t, mt, n1, n2, L);
+      const Tile x = tile_of(t, mt, n1, n2, L, a.gm);
       const uint32_t acc = it & 1;
       t0 = clock64();
       mbar_wait(&m.tfull[acc], (it >> 1) & 1);
@@ -1630,6 +1656,8 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   // 264 / 248 / 235 / 228 / 228 us per bench step (profiles/ab_lag_r2.txt)
   a.lag = getenv("RNNLM_TC_LAG") ? (uint32_t)atoi(getenv("RNNLM_TC_LAG"))
                                  : (t->pair ? (t->x3 ? 1000u : 64u) : 128u);
+  a.gm = getenv("RNNLM_TC_GM") ? (uint32_t)atoi(getenv("RNNLM_TC_GM")) : 1u;
+  if (!a.gm) a.gm = 1;
   a.diag = t->diag;
   a.bz = t->bz; a.br = t->br;
   a.bn2 = P.H % BN ? UB : BN;
