@@ -659,7 +659,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
 #ifndef EPI_KO
 #define EPI_KO 0
 #endif
-constexpr bool KO_LOAD = EPI_KO & 1, KO_STORE = EPI_KO & 2, KO_ENC = EPI_KO & 4, KO_MATH = EPI_KO & 8;
+constexpr bool KO_LOAD = EPI_KO & 1, KO_STORE = EPI_KO & 2, KO_ENC = EPI_KO & 4, KO_MATH = EPI_KO & 8,
+               KO_Z = EPI_KO & 16;    // 16: no z round trip (phase-1 z stores, phase-2 z loads)
 
 // Phase-1 epilogue of one thread: row `row` of the tile, the 128 z columns
 // (gate 0) or r columns (gate 1) of unit block ub.  The parent state h of
@@ -683,7 +684,7 @@ __device__ __forceinline__ void epi_phase1(const TcArgs &a, uint32_t tacc, uint3
     ld_bias16(bias + c * 32 + 16, b + 16);
     if (gate == 0) {
       tmem_ld_wait();
-      if (valid && !KO_STORE) {
+      if (valid && !KO_STORE && !KO_Z) {
         float4 *zq = reinterpret_cast<float4 *>(a.g_z) + zq4(row, u0 + c * 32, a.H);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -750,7 +751,10 @@ __device__ __forceinline__ void epi_phase2(const TcArgs &a, uint32_t tbase, uint
   for (uint32_t c = 0; c < units / 32; ++c) {           // chunks of 32 units
     float v[32], b[32], z[32], h[32];
     tmem_ld32(tbase + c * 32, v);
-    if (live && !KO_LOAD) {
+    if (KO_Z) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) z[j] = 0.5f;
+    } else if (live && !KO_LOAD) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float4 t = zq[(c * 8 + j) << 7];
