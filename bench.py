@@ -566,6 +566,23 @@ def run_ours(args):
     del bench
     gc.collect()
     torch.cuda.empty_cache()
+    if world > 1 and args.scaling == "strong":
+        # the weak-scaling companion (BASELINE configs[4] read per GPU): every rank
+        # runs its own full 64-stream job, same math, same timing rules
+        ts = args.total_streams
+        args.total_streams = S_job * world
+        wl_w = multi_workload(args, rank * S_job, (rank + 1) * S_job, frames, not args.no_stagger, args.uniform_words)
+        bw = StepBench(args, dims, model, wl_w, args.math, dev, world, local)
+        rw = bw.run()
+        sw = step_summary(args, bw, rw, world, peaks, tf32_peak)
+        line["weak_scaling"] = {"value": sw["value"], "unit": UNIT, "ms_per_step": sw["ms_per_step"],
+                                "streams_total": S_job * world, "streams_per_gpu": S_job,
+                                "queries_per_step": int(wl_w.n_per_frame) * world,
+                                "roofline_frac": sw["roofline"]["frac"], "clocks": sw["clocks"]}
+        args.total_streams = ts
+        del bw, wl_w
+        gc.collect()
+        torch.cuda.empty_cache()
     for other in [m for m in args.also.split(",") if m and m != "none" and m != args.math]:
         b2 = StepBench(args, dims, model, wl, other, dev, world, local)
         r2 = b2.run()
