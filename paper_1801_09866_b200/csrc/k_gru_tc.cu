@@ -1133,7 +1133,7 @@ __device__ __forceinline__ SmemP carve_pair(uint8_t *raw) {
 // (cp.async.bulk.tensor .cta_group::2), which the leader arms with the bytes
 // of both halves; the MMA commit releases the stage in both CTAs at once
 // (multicast), so no CTA-to-CTA handshake sits on the K loop.
-template <int NA>
+template <int NA, int BN2>
 __global__ void __maxnreg__(GRU_MAXREG)
     k_gru_tc2(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ CUtensorMap map_w1h,
               const __grid_constant__ CUtensorMap map_rh, const __grid_constant__ CUtensorMap map_w2h,
@@ -1145,7 +1145,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const uint32_t n1 = a.nub, n2 = a.H / BN;
+  const uint32_t n1 = a.nub, n2 = a.H / BN2;             // phase-2 tiles of BN2 = 256 or 128 units
   const uint32_t kx = a.E / BK, KCt = seg_chunks(a);
   const uint32_t target = n1 * 2 * EPI_WARPS;           // phase-1 arrivals per 256-row tile
   // tile-ring consumers (arrivals on the leader's qempty per slot): the
@@ -1207,7 +1207,8 @@ __global__ void __maxnreg__(GRU_MAXREG)
         if (t == NO_TILE) break;
         const Tile x = tile_of(t, mt, n1, n2, L, a.gm);
         const uint32_t m0 = x.m * 2 * BM + rank * BM;
-        const uint32_t b0row = x.j * BN + rank * (BN / 2);
+        const uint32_t bh = x.kind == 1 ? (uint32_t)(BN2 / 2) : (uint32_t)(BN / 2);   // B rows this CTA loads
+        const uint32_t b0row = x.j * 2 * bh + rank * bh;
         if (x.kind == 1 && a.diag != 4) {
           t0 = clock64();
           wait_phase1(a.done1 + x.m, target);
@@ -1228,7 +1229,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
             if (++stage == STP) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (leader) mbar_expect_tx(&m.full[stage], 2 * (npa * A_BYTES + BP_BYTES));
+          if (leader) mbar_expect_tx(&m.full[stage], 2 * (npa * A_BYTES + bh * BK * 2));
           const uint32_t fb = full0 + stage * 8;
           const uint32_t dA = smem_u32(m.sA + stage * NA * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
 #pragma unroll
@@ -1249,7 +1250,8 @@ __global__ void __maxnreg__(GRU_MAXREG)
   } else if (warp == 1) {
     if (leader) {
       uint32_t stage = 0, phase = 0;
-      const uint32_t id = idesc_bf16(2 * BM, BN);
+      const uint32_t id1 = idesc_bf16(2 * BM, BN), id2 = idesc_bf16(2 * BM, BN2);
+      const uint32_t p2_first = L >= mt ? mt * n1 : 0xFFFFFFFFu;     // separated phases: phase 2 = the tail
       unsigned long long w_full = 0, w_tempty = 0, t0;
       for (uint32_t it = 0;; ++it) {
         const uint32_t slot = it % TQ;                  // the leader MMA lane reads its own ring
@@ -1258,6 +1260,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
         __syncwarp();
         if (lane == 0) mbar_arrive_cl(qempty0 + slot * 8);
         if (t == NO_TILE) break;
+        const uint32_t id = BN2 == BN ? id1
+                            : ((t >= p2_first || (p2_first == 0xFFFFFFFFu && tile_of(t, mt, n1, n2, L, a.gm).kind == 1))
+                                   ? id2 : id1);
         const uint32_t acc = it & 1;
         t0 = clock64();
         mbar_wait_cl(&m.tempty[acc], ((it >> 1) & 1) ^ 1);   // arrivals from both CTAs
@@ -1323,7 +1328,8 @@ __global__ void __maxnreg__(GRU_MAXREG)
         epi_phase1<__nv_bfloat16>(a, tbase - half * (BN / 2), row, valid, half, x.j, stg, lane);
       } else {
         wait_phase1(a.done1 + x.m, target);
-        epi_phase2(a, tbase, row, valid, x.j * BN + half * (BN / 2), BN / 2, stg, lane);
+        epi_phase2(a, tbase - half * (BN / 2) + half * (BN2 / 2), row, valid, x.j * BN2 + half * (BN2 / 2),
+                   BN2 / 2, stg, lane);
       }
       tc_fence_before();
       __syncwarp();
@@ -1383,7 +1389,7 @@ struct TcState {
   bool rnn = false;                // cell RNN: one-phase tiles over W2 = [Wh | Uh]
   void *w3 = nullptr;
   float *bz = nullptr, *br = nullptr;
-  CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h, map_w3;
+  CUtensorMap map_w1, map_w2, map_a1, map_rh, map_w1h, map_w2h, map_w2q, map_w3;
   bool bound = false;
 };
 
@@ -1527,15 +1533,17 @@ int gru_tc_prepare(const rnnlm_weights *w, uint32_t V, uint32_t E, uint32_t H, i
   if (H % BN) t->pair = 0;        // the CTA pair keeps 256-unit phase-2 tiles
   if (!t->tf32)
     ok = ok && make_map(&t->map_w1h, t->w1, RW, 2 * (uint64_t)H, BN / 2) &&
-         make_map(&t->map_w2h, t->w2, RW, H, BN / 2);
+         make_map(&t->map_w2h, t->w2, RW, H, BN / 2) && make_map(&t->map_w2q, t->w2, RW, H, BN / 4);
   ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<__nv_bfloat16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RNN) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_gru_tc<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_RNN) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pair<1>()) == cudaSuccess;
-  ok = ok && cudaFuncSetAttribute(k_gru_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pair<3>()) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc2<1, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pair<1>()) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc2<3, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pair<3>()) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc2<1, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pair<1>()) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_gru_tc2<3, UB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pair<3>()) == cudaSuccess;
   *state_out = t;
   if (!ok) {
     (void)cudaGetLastError();
@@ -1693,15 +1701,24 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   if (ev_gathered) cudaEventRecord(ev_gathered, s);
   if (ev_fork && !fork_early) cudaEventRecord(ev_fork, s);
   if (t->pair) {
-    uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / BN) * 2;
+    // Phase-2 tiles of 128 units for calls of up to RNNLM_TC_P2N_MAX queries (default 32,768:
+    // 16 streams x 2,048), else 256: a small frame's GRU is two dependent tile waves, and
+    // half-width phase-2 tiles halve the second one (8 / 16 streams: 138 -> 150 / 228 -> 245
+    // M q/s) while costing ~10 % at 64 streams.  Splitting N does not change any output
+    // element's accumulation, so results are bitwise the same either way.
+    static const uint32_t p2max = getenv("RNNLM_TC_P2N_MAX") ? (uint32_t)atoi(getenv("RNNLM_TC_P2N_MAX")) : 32768u;
+    a.bn2 = max_rows <= p2max ? 128u : (uint32_t)BN;
+    uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / a.bn2) * 2;
     const uint32_t cap = (uint32_t)num_sms & ~1u;
     if (gp > cap) gp = cap;
-    if (grouped && t->x3)
-      launch_pdl_cluster(k_gru_tc2<3>, gp, THREADS, smem_pair<3>(), s, 2, t->map_a1, t->map_w1h, t->map_rh,
-                         t->map_w2h, a);
-    else
-      launch_pdl_cluster(k_gru_tc2<1>, gp, THREADS, smem_pair<1>(), s, 2, t->map_a1, t->map_w1h, t->map_rh,
-                         t->map_w2h, a);
+    const CUtensorMap &m2 = a.bn2 == UB ? t->map_w2q : t->map_w2h;
+    if (grouped && t->x3) {
+      if (a.bn2 == UB) launch_pdl_cluster(k_gru_tc2<3, UB>, gp, THREADS, smem_pair<3>(), s, 2, t->map_a1, t->map_w1h, t->map_rh, m2, a);
+      else launch_pdl_cluster(k_gru_tc2<3, BN>, gp, THREADS, smem_pair<3>(), s, 2, t->map_a1, t->map_w1h, t->map_rh, m2, a);
+    } else {
+      if (a.bn2 == UB) launch_pdl_cluster(k_gru_tc2<1, UB>, gp, THREADS, smem_pair<1>(), s, 2, t->map_a1, t->map_w1h, t->map_rh, m2, a);
+      else launch_pdl_cluster(k_gru_tc2<1, BN>, gp, THREADS, smem_pair<1>(), s, 2, t->map_a1, t->map_w1h, t->map_rh, m2, a);
+    }
   } else {
     if (t->lbr) {
       if (t->tf32) launch_pdl(k_gru_tc<float, 1>, g1, THREADS, SMEM, s, t->map_a1, t->map_w3, t->map_rh, t->map_w2, a);
