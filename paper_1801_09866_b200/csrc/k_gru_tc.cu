@@ -1706,7 +1706,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     // half-width phase-2 tiles halve the second one (8 / 16 streams: 138 -> 150 / 228 -> 245
     // M q/s) while costing ~10 % at 64 streams.  Splitting N does not change any output
     // element's accumulation, so results are bitwise the same either way.
-    static const uint32_t p2max = getenv("RNNLM_TC_P2N_MAX") ? (uint32_t)atoi(getenv("RNNLM_TC_P2N_MAX")) : 32768u;
+    const uint32_t p2max = getenv("RNNLM_TC_P2N_MAX") ? (uint32_t)atoi(getenv("RNNLM_TC_P2N_MAX")) : 32768u;
     a.bn2 = max_rows <= p2max ? 128u : (uint32_t)BN;
     uint32_t gp = ((max_rows + 2 * BM - 1) / (2 * BM)) * (t->nub + P.H / a.bn2) * 2;
     const uint32_t cap = (uint32_t)num_sms & ~1u;

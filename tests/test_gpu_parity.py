@@ -286,8 +286,12 @@ def test_bf16_interleaved_phase_schedule(lag, monkeypatch):
         monkeypatch.setenv("RNNLM_TC_LAG", lag)
     d, m = model("large")
     wl = generate_workload(2, 2, 2000, d.V, seed=23)
-    for pk in ("1", "0"):
+    for pk, p2n in (("1", None), ("1", "0"), ("0", None)):
         monkeypatch.setenv("RNNLM_TC_PAIR", pk)
+        if p2n is not None:     # 256-unit phase-2 tiles (the large-call instance)
+            monkeypatch.setenv("RNNLM_TC_P2N_MAX", p2n)
+        else:
+            monkeypatch.delenv("RNNLM_TC_P2N_MAX", raising=False)
         eng, orc = pair(d, m, wl, KEY_SIGN, math=MATH_BF16, cache=False)
         rep = replay_compare(eng, orc, wl, tol_score=TOL[MATH_BF16], tol_state=TOL[MATH_BF16])
         assert rep["miss"] == wl.n_total
@@ -310,6 +314,27 @@ def test_bf16_cta_pair_kernel(shape, pair_kernel, monkeypatch):
         wl = generate_workload(3, 3, 300, d.V, seed=6)
         eng, orc = pair(d, m, wl, KEY_ROUND, k=2, math=MATH_BF16)
         replay_compare(eng, orc, wl, tol_score=1e-3, tol_state=1e-3)
+
+
+@pytest.mark.parametrize("math", [MATH_BF16, MATH_BF16X3])
+@pytest.mark.parametrize("p2n_max", ["0", None])
+def test_cta_pair_phase2_tile_widths(math, p2n_max, monkeypatch):
+    """The CTA-pair kernel's two phase-2 tile shapes against the oracle:
+    256-unit tiles (RNNLM_TC_P2N_MAX=0: the instance calls of more than 32k
+    queries run) and 128-unit tiles (the default for these small calls).
+    All-miss full tiles, then a ragged multi-session batch with round keys."""
+    monkeypatch.setenv("RNNLM_TC_PAIR", "1")
+    if p2n_max is not None:
+        monkeypatch.setenv("RNNLM_TC_P2N_MAX", p2n_max)
+    tol = TOL[math]
+    d, m = model("large")
+    wl = generate_workload(1, 2, 2048, d.V, seed=5)
+    eng, orc = pair(d, m, wl, KEY_SIGN, math=math, cache=False)
+    rep = replay_compare(eng, orc, wl, tol_score=tol, tol_state=tol)
+    assert rep["miss"] == wl.n_total
+    wl = generate_workload(3, 3, 300, d.V, seed=6)
+    eng, orc = pair(d, m, wl, KEY_ROUND, k=2, math=math)
+    replay_compare(eng, orc, wl, tol_score=tol, tol_state=tol)
 
 
 def test_large_bf16_cache_off_full_tiles():
