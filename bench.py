@@ -480,7 +480,8 @@ def step_summary(args, bench, res, world, peaks, tf32_peak):
         "value": value, "ms_per_step": res["ms"] / steps, "dtype": dtype_of(math),
         "roofline": {"kernel": kname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak if peak else None, "traffic": None,
-                     "traffic_ncu": "profiles/ncu_r2_summary.md (dram bytes per launch, ncu --set full)",
+                     "traffic_ncu": (f"profiles/ncu_r2_gru_{math}.md (dram bytes per launch, ncu --set full)"
+                                     if math in ("bf16", "bf16x3") else "profiles/ncu_r2_start_tf32x3.md"),
                      "peak_source": src,
                      "algorithmic": f"{2 * gates}*H*(E+H) flop per GRU row x {rows} rows over {steps} steps",
                      "kernel_ms_per_step": k_ms / steps,
