@@ -178,6 +178,7 @@ struct TcArgs {
   uint32_t *tile_ctr;              // dynamic tile scheduler (zeroed by the gather)
   uint32_t lag;                    // phase-2 tiles trail phase-1 tiles by this many M-tiles
   uint32_t gm;                     // CTA pair, separated phases: tile groups of gm M-tiles (see tile_of)
+  uint32_t pack;                   // CTA pair, 3-part stages: single-part segments carry 2 K-chunks per stage
   uint32_t diag;                   // timing diagnostics: 1 no MMA, 2 no TMA, 3 no epilogue, 4 = 3 + no phase
                                    // dependency, 6 = 1 + 2 (results invalid); 5 cycle counters (results valid)
   unsigned long long *prof;        // diag 5: per-CTA cycle counters, else nullptr
@@ -1216,33 +1217,52 @@ __global__ void __maxnreg__(GRU_MAXREG)
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         if (prof) prof[9 + x.kind] += 1;
-        for (uint32_t sg = 0; sg < a.nseg; ++sg)
-        for (uint32_t kc = a.seg[sg].k0; kc < a.seg[sg].k1; ++kc) {
-          // this stage: weight part pw, A parts pa0 .. pa0 + npa - 1 (column offsets into the part blocks)
+        for (uint32_t sg = 0; sg < a.nseg; ++sg) {
+          // this segment: weight part pw, A parts pa0 .. pa0 + npa - 1 (column offsets into the part blocks)
           const uint32_t pa0 = a.seg[sg].pa0, npa = NA == 1 ? 1u : a.seg[sg].npa;
           const int b_off = (int)(a.seg[sg].pw * (a.E + a.H));
-          t0 = clock64();
-          mbar_wait(&m.empty[stage], phase ^ 1);
-          w_empty += clock64() - t0;
-          if (a.diag == 2 || a.diag == 6) {
-            if (leader) mbar_arrive(&m.full[stage]);
-            if (++stage == STP) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          if (leader) mbar_expect_tx(&m.full[stage], 2 * (npa * A_BYTES + bh * BK * 2));
-          const uint32_t fb = full0 + stage * 8;
-          const uint32_t dA = smem_u32(m.sA + stage * NA * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
+          // packed single-part stage (3-part ring): A(kc), A(kc+1) in A slots 0, 1, B(kc) in the
+          // B slot and B(kc+1) in A slot 2, so the stage carries as many bytes as a 3-part stage
+          const uint32_t step = (NA == 3 && npa == 1 && a.pack) ? 2u : 1u;
+          for (uint32_t kc = a.seg[sg].k0; kc < a.seg[sg].k1; kc += step) {
+            const uint32_t nk = kc + step <= a.seg[sg].k1 ? step : 1u;   // K-chunks in this stage
+            t0 = clock64();
+            mbar_wait(&m.empty[stage], phase ^ 1);
+            w_empty += clock64() - t0;
+            if (a.diag == 2 || a.diag == 6) {
+              if (leader) mbar_arrive(&m.full[stage]);
+              if (++stage == STP) { stage = 0; phase ^= 1; }
+              continue;
+            }
+            if (leader) mbar_expect_tx(&m.full[stage], 2 * (npa * nk * A_BYTES + nk * bh * BK * 2));
+            const uint32_t fb = full0 + stage * 8;
+            const uint32_t dA = smem_u32(m.sA + stage * NA * A_BYTES), dB = smem_u32(m.sB + stage * BP_BYTES);
+            const CUtensorMap *mapb = x.kind == 0 ? &map_w1h : &map_w2h;
+            if (nk == 2) {
 #pragma unroll
-          for (uint32_t p = 0; p < (uint32_t)NA; ++p) {
-            if (p >= npa) break;
-            const uint32_t pa = pa0 + p;
-            if (x.kind == 0 || kc < kx)
-              tma_load_2d_pair(dA + p * A_BYTES, &map_a1, fb, (int)(pa * (a.E + a.H) + kc * BK), (int)m0);
-            else
-              tma_load_2d_pair(dA + p * A_BYTES, &map_rh, fb, (int)(pa * a.H + (kc - kx) * BK), (int)m0);
+              for (uint32_t c = 0; c < 2; ++c) {
+                const uint32_t k = kc + c;
+                if (x.kind == 0 || k < kx)
+                  tma_load_2d_pair(dA + c * A_BYTES, &map_a1, fb, (int)(pa0 * (a.E + a.H) + k * BK), (int)m0);
+                else
+                  tma_load_2d_pair(dA + c * A_BYTES, &map_rh, fb, (int)(pa0 * a.H + (k - kx) * BK), (int)m0);
+              }
+              tma_load_2d_pair(dB, mapb, fb, b_off + (int)(kc * BK), (int)b0row);
+              tma_load_2d_pair(dA + 2 * A_BYTES, mapb, fb, b_off + (int)((kc + 1) * BK), (int)b0row);
+            } else {
+#pragma unroll
+              for (uint32_t p = 0; p < (uint32_t)NA; ++p) {
+                if (p >= npa) break;
+                const uint32_t pa = pa0 + p;
+                if (x.kind == 0 || kc < kx)
+                  tma_load_2d_pair(dA + p * A_BYTES, &map_a1, fb, (int)(pa * (a.E + a.H) + kc * BK), (int)m0);
+                else
+                  tma_load_2d_pair(dA + p * A_BYTES, &map_rh, fb, (int)(pa * a.H + (kc - kx) * BK), (int)m0);
+              }
+              tma_load_2d_pair(dB, mapb, fb, b_off + (int)(kc * BK), (int)b0row);
+            }
+            if (++stage == STP) { stage = 0; phase ^= 1; }
           }
-          tma_load_2d_pair(dB, x.kind == 0 ? &map_w1h : &map_w2h, fb, b_off + (int)(kc * BK), (int)b0row);
-          if (++stage == STP) { stage = 0; phase ^= 1; }
         }
       }
       if (prof) { prof[0] = w_empty; prof[1] = w_dep; }
@@ -1251,6 +1271,11 @@ __global__ void __maxnreg__(GRU_MAXREG)
     if (leader) {
       uint32_t stage = 0, phase = 0;
       const uint32_t id1 = idesc_bf16(2 * BM, BN), id2 = idesc_bf16(2 * BM, BN2);
+      uint32_t KSt = 0;                                 // smem stages per tile (packed single-part stages)
+      for (uint32_t sg = 0; sg < (NA == 1 ? 1u : a.nseg); ++sg) {
+        const uint32_t len = NA == 1 ? KCt : (uint32_t)(a.seg[sg].k1 - a.seg[sg].k0);
+        KSt += (NA == 3 && a.seg[sg].npa == 1 && a.pack) ? (len + 1) / 2 : len;
+      }
       const uint32_t p2_first = L >= mt ? mt * n1 : 0xFFFFFFFFu;     // separated phases: phase 2 = the tail
       unsigned long long w_full = 0, w_tempty = 0, t0;
       for (uint32_t it = 0;; ++it) {
@@ -1274,7 +1299,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
         for (uint32_t sg = 0; sg < (NA == 1 ? 1u : a.nseg); ++sg) {
           const uint32_t npa = NA == 1 ? 1u : a.seg[sg].npa;
           const uint32_t c0 = NA == 1 ? 0u : a.seg[sg].k0, c1 = NA == 1 ? KCt : a.seg[sg].k1;
-          for (uint32_t c = c0; c < c1; ++c, ++kc) {
+          const uint32_t step = (NA == 3 && npa == 1 && a.pack) ? 2u : 1u;   // packed stages (producer)
+          for (uint32_t c = c0; c < c1; c += step, ++kc) {
+            const uint32_t nk = c + step <= c1 ? step : 1u;
             t0 = clock64();
             // both CTAs' bytes landed (complete_tx on this barrier); the MMA reads them
             // through the async proxy, so a CTA-scope wait suffices -- a cluster-scope
@@ -1284,15 +1311,25 @@ __global__ void __maxnreg__(GRU_MAXREG)
             tc_fence_after();
             if (lane == 0) {
               const uint32_t a0 = smem_u32(m.sA + stage * NA * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
-              if (a.diag != 1 && a.diag != 6)
+              if (a.diag != 1 && a.diag != 6) {
+                if (nk == 2) {                            // A(c) . B(c), then A(c+1) . B(c+1) (in A slot 2)
 #pragma unroll
-                for (uint32_t p = 0; p < (uint32_t)NA; ++p)
-                  if (p < npa)
+                  for (uint32_t q = 0; q < 2; ++q)
 #pragma unroll
-                  for (int k = 0; k < BK / 16; ++k)
-                    umma_bf16_pair(tm, sdesc(a0 + p * A_BYTES + k * 32), sdesc(b0 + k * 32), id, (kc | p | k) != 0);
+                    for (int k = 0; k < BK / 16; ++k)
+                      umma_bf16_pair(tm, sdesc(a0 + q * A_BYTES + k * 32),
+                                     sdesc((q ? a0 + 2 * A_BYTES : b0) + k * 32), id, (kc | q | k) != 0);
+                } else {
+#pragma unroll
+                  for (uint32_t p = 0; p < (uint32_t)NA; ++p)
+                    if (p < npa)
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                      umma_bf16_pair(tm, sdesc(a0 + p * A_BYTES + k * 32), sdesc(b0 + k * 32), id, (kc | p | k) != 0);
+                }
+              }
               umma_commit_pair(&m.empty[stage]);
-              if (kc == KCt - 1) umma_commit_pair(&m.tfull[acc]);
+              if (kc == KSt - 1) umma_commit_pair(&m.tfull[acc]);
             }
             __syncwarp();
             if (++stage == STP) { stage = 0; phase ^= 1; }
@@ -1669,6 +1706,7 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
   a.lag = getenv("RNNLM_TC_LAG") ? (uint32_t)atoi(getenv("RNNLM_TC_LAG"))
                                  : (t->pair ? (t->x3 ? 1000u : 64u) : 128u);
   a.gm = getenv("RNNLM_TC_GM") ? (uint32_t)atoi(getenv("RNNLM_TC_GM")) : 1u;
+  a.pack = getenv("RNNLM_TC_PACK") ? (uint32_t)atoi(getenv("RNNLM_TC_PACK")) : 1u;
   if (!a.gm) a.gm = 1;
   a.diag = t->diag;
   a.bz = t->bz; a.br = t->br;
