@@ -1750,7 +1750,10 @@ int launch_gru_tc(const Params &P, void *state, uint32_t max_rows, int num_sms, 
     const uint32_t cap = (uint32_t)num_sms & ~1u;
     if (gp > cap) gp = cap;
     const CUtensorMap &m2 = a.bn2 == UB ? t->map_w2q : t->map_w2h;
-    if (grouped && t->x3) {
+    // plain bf16 runs on the 3-part ring too: packed 64-KB stages of 2 K-chunks, 6 chunks in flight
+    // instead of 5 (RNNLM_TC_BF16_NA3=0: the 5-deep 32-KB ring; 143.6 -> 141.7 us, profiles/ab_pack_r2.txt)
+    const bool na3 = grouped && (t->x3 || !(getenv("RNNLM_TC_BF16_NA3") && atoi(getenv("RNNLM_TC_BF16_NA3")) == 0));
+    if (na3) {
       if (a.bn2 == UB) launch_pdl_cluster(k_gru_tc2<3, UB>, gp, THREADS, smem_pair<3>(), s, 2, t->map_a1, t->map_w1h, t->map_rh, m2, a);
       else launch_pdl_cluster(k_gru_tc2<3, BN>, gp, THREADS, smem_pair<3>(), s, 2, t->map_a1, t->map_w1h, t->map_rh, m2, a);
     } else {
