@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import argparse
 import gc
+import ctypes
 import json
 import os
 import subprocess
@@ -741,17 +742,32 @@ def frame_loop(eng, wl, dev, t_lo, t_hi, use_graph=False, timing=0):
         sc, ch = torch.zeros(n, dtype=torch.float32, device=dev), torch.zeros(n, dtype=torch.int32, device=dev)
         g = eng.graph(n, bs, par, bw, sc, ch)
 
+    # Direct calls go through the C ABI with every frame's pointers precomputed:
+    # per frame the host pays two ctypes calls, as a C/C++ decoder would, instead
+    # of torch slicing + the Python wrappers (~30 us per frame, which made the
+    # tiny config host-bound: 32 vs 18 us per frame, profiles/host_rate_r2.jsonl)
+    from paper_1801_09866_b200 import _lib
+    lib = _lib.load()
+    cst = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    vp = lambda x: ctypes.c_void_p(x.data_ptr())
+    slices = [wl.frame_slice(t) for t in range(t_hi)]
+    pre = [(s_.stop - s_.start, vp(d_ref[s_]), vp(d_sess[s_]), vp(d_word[s_]), vp(d_score[s_]), vp(d_child[s_]))
+           for s_ in slices]
+    p_par, p_log = vp(par), vp(d_child)
+
     def frame(t):
-        sl = wl.frame_slice(t)
-        R.resolve_parents(d_ref[sl], d_child, par)
         if use_graph:
+            sl = slices[t]
+            R.resolve_parents(d_ref[sl], d_child, par)
             bs.copy_(d_sess[sl])
             bw.copy_(d_word[sl])
             g.launch()
             d_child[sl].copy_(ch)
             d_score[sl].copy_(sc)
         else:
-            eng.query_batch(d_sess[sl], par, d_word[sl], score=d_score[sl], child=d_child[sl], want_outcome=False)
+            nn, pr, ps, pw, psc, pch = pre[t]
+            _lib.check(lib.rnnlm_resolve_parents(nn, pr, p_log, p_par, cst), "resolve_parents")
+            _lib.check(lib.rnnlm_query_batch(eng._h, nn, ps, p_par, pw, psc, pch, None, cst), "rnnlm_query_batch")
 
     for t in range(t_lo):
         frame(t)
