@@ -207,6 +207,16 @@ __host__ __device__ __forceinline__ uint32_t seg_chunks(const TcArgs &a) {
   return n;
 }
 
+// Cycle counters of the RNNLM_TC_DIAG=5 profile: compiled in only with
+// -DRNNLM_TC_PROF=1 (scripts/diag_r2.sh); otherwise every counter is the
+// constant 0 and the producer / MMA / epilogue loops carry no clock reads
+#ifndef RNNLM_TC_PROF
+#define RNNLM_TC_PROF 0
+#endif
+__device__ __forceinline__ unsigned long long pclk() {
+  if constexpr (RNNLM_TC_PROF != 0) return clock64();
+  else return 0ull;
+}
 __device__ __forceinline__ unsigned long long gtimer() {       // ns (diag 5 timeline)
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -485,15 +495,15 @@ __device__ __forceinline__ void mma_loop(const Smem &m, uint32_t tmem_base, uint
     if (tid == NO_TILE) break;
     const uint32_t id = (narrow && (rnn || tile_of(tid, mt, n1, n2, L).kind == 1)) ? id128 : id256;
     const uint32_t acc = it & 1;
-    t0 = clock64();
+    t0 = pclk();
     mbar_wait(&m.tempty[acc], ((it >> 1) & 1) ^ 1);
-    w_tempty += clock64() - t0;
+    w_tempty += pclk() - t0;
     tc_fence_after();
     const uint32_t tm = tmem_base + acc * BN;
     for (uint32_t kc = 0; kc < KC; ++kc) {
-      t0 = clock64();
+      t0 = pclk();
       mbar_wait(&m.full[stage], phase);
-      w_full += clock64() - t0;
+      w_full += pclk() - t0;
       tc_fence_after();
       if (lane == 0) {
         const uint32_t a0 = smem_u32(m.sA + stage * A_BYTES), b0 = smem_u32(m.sB + stage * B_BYTES);
@@ -889,7 +899,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   const uint32_t ntiles = mt * (n1 + n2);
   const uint32_t tmem_base = *m.tmem_base;
   unsigned long long *prof = a.prof ? a.prof + blockIdx.x * 16 : nullptr;
-  const unsigned long long k_t0 = clock64();
+  const unsigned long long k_t0 = pclk();
   if (prof && threadIdx.x == 0) prof[14] = gtimer();
 
   if (warp == 0) {
@@ -907,9 +917,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
         const Tile x = tile_of(t, mt, n1, n2, L);
         const uint32_t m0 = x.m * BM;
         if (x.kind == 1 && a.diag != 4) {
-          t0 = clock64();
+          t0 = pclk();
           wait_phase1(a.done1 + x.m, target);
-          w_dep += clock64() - t0;
+          w_dep += pclk() - t0;
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         if (prof) prof[9 + x.kind] += 1;
@@ -918,9 +928,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
           // split modes: A part pa, weight part pw of this segment (column offsets into the part blocks)
           const int a_off = (int)(a.seg[sg].pa0 * (a.E + a.H)), b_off = (int)(a.seg[sg].pw * (a.E + a.H));
           const int rh_off = (int)(a.seg[sg].pa0 * a.H);
-          t0 = clock64();
+          t0 = pclk();
           mbar_wait(&m.empty[stage], phase ^ 1);
-          w_empty += clock64() - t0;
+          w_empty += pclk() - t0;
           if (a.diag == 2 || a.diag == 6) {
             mbar_arrive(&m.full[stage]);
             if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -955,10 +965,10 @@ __global__ void __maxnreg__(GRU_MAXREG)
       if (t == NO_TILE) break;
       const Tile x = tile_of(t, mt, n1, n2, L);
       const uint32_t acc = it & 1;
-      t0 = clock64();
+      t0 = pclk();
       mbar_wait(&m.tfull[acc], (it >> 1) & 1);
-      w_tfull += clock64() - t0;
-      t0 = clock64();
+      w_tfull += pclk() - t0;
+      t0 = pclk();
       tc_fence_after();
       const uint32_t row = x.m * BM + r_in;
       const bool valid = row < Q;
@@ -981,12 +991,12 @@ __global__ void __maxnreg__(GRU_MAXREG)
         epi_rnn(a, tbase, row, valid, x.j * a.bn2 + half * hw, hw, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
-        b1 += clock64() - t0;
+        b1 += pclk() - t0;
       } else if constexpr (LBR) {
         epi_lbr(a, tbase - half * (BN / 2), row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
-        b1 += clock64() - t0;
+        b1 += pclk() - t0;
       } else if (x.kind == 0) {
         epi_phase1<T>(a, tbase - half * hw, row, valid, half, x.j, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
@@ -998,13 +1008,13 @@ __global__ void __maxnreg__(GRU_MAXREG)
           __threadfence();
           atomicAdd(a.done1 + x.m, 1u);
         }
-        b1 += clock64() - t0;
+        b1 += pclk() - t0;
       } else {
         wait_phase1(a.done1 + x.m, target);               // acquire z of this M-tile
         epi_phase2(a, tbase, row, valid, x.j * a.bn2 + half * hw, hw, m.stg + (warp - 2) * STG_BYTES, lane);
         tc_fence_before();
         mbar_arrive(&m.tempty[acc]);
-        b2 += clock64() - t0;
+        b2 += pclk() - t0;
       }
     }
     if (prof && lane == 0 && (warp == 2 || warp == 6)) {
@@ -1012,7 +1022,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
       prof[o] = w_tfull; prof[o + 1] = b1; prof[o + 2] = b2;
     }
   }
-  if (prof && threadIdx.x == 0) prof[8] = clock64() - k_t0;
+  if (prof && threadIdx.x == 0) prof[8] = pclk() - k_t0;
   teardown(m, warp, tmem_base);
   if (prof && threadIdx.x == 0) prof[15] = gtimer();       // every warp of the CTA is done
 }
@@ -1174,7 +1184,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
   const uint32_t tempty0 = mapa(smem_u32(&m.tempty[0]), 0);
   const uint32_t qempty0 = mapa(smem_u32(&m.qempty[0]), 0);
   unsigned long long *prof = a.prof ? a.prof + blockIdx.x * 16 : nullptr;
-  const unsigned long long k_t0 = clock64();
+  const unsigned long long k_t0 = pclk();
   if (prof && threadIdx.x == 0) { prof[14] = gtimer(); prof[7] = t_entry; }
 
   // tile id of ring slot `it`; one lane releases the slot on the leader's qempty
@@ -1211,9 +1221,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
         const uint32_t bh = x.kind == 1 ? (uint32_t)(BN2 / 2) : (uint32_t)(BN / 2);   // B rows this CTA loads
         const uint32_t b0row = x.j * 2 * bh + rank * bh;
         if (x.kind == 1 && a.diag != 4) {
-          t0 = clock64();
+          t0 = pclk();
           wait_phase1(a.done1 + x.m, target);
-          w_dep += clock64() - t0;
+          w_dep += pclk() - t0;
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         if (prof) prof[9 + x.kind] += 1;
@@ -1226,9 +1236,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
           const uint32_t step = (NA == 3 && npa == 1 && a.pack) ? 2u : 1u;
           for (uint32_t kc = a.seg[sg].k0; kc < a.seg[sg].k1; kc += step) {
             const uint32_t nk = kc + step <= a.seg[sg].k1 ? step : 1u;   // K-chunks in this stage
-            t0 = clock64();
+            t0 = pclk();
             mbar_wait(&m.empty[stage], phase ^ 1);
-            w_empty += clock64() - t0;
+            w_empty += pclk() - t0;
             if (a.diag == 2 || a.diag == 6) {
               if (leader) mbar_arrive(&m.full[stage]);
               if (++stage == STP) { stage = 0; phase ^= 1; }
@@ -1289,9 +1299,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
                             : ((t >= p2_first || (p2_first == 0xFFFFFFFFu && tile_of(t, mt, n1, n2, L, a.gm).kind == 1))
                                    ? id2 : id1);
         const uint32_t acc = it & 1;
-        t0 = clock64();
+        t0 = pclk();
         mbar_wait_cl(&m.tempty[acc], ((it >> 1) & 1) ^ 1);   // arrivals from both CTAs
-        w_tempty += clock64() - t0;
+        w_tempty += pclk() - t0;
         tc_fence_after();
         const uint32_t tm = tmem_base + acc * BN;
         uint32_t kc = 0;                                  // stage count of this tile
@@ -1302,12 +1312,12 @@ __global__ void __maxnreg__(GRU_MAXREG)
           const uint32_t step = (NA == 3 && npa == 1 && a.pack) ? 2u : 1u;   // packed stages (producer)
           for (uint32_t c = c0; c < c1; c += step, ++kc) {
             const uint32_t nk = c + step <= c1 ? step : 1u;
-            t0 = clock64();
+            t0 = pclk();
             // both CTAs' bytes landed (complete_tx on this barrier); the MMA reads them
             // through the async proxy, so a CTA-scope wait suffices -- a cluster-scope
             // acquire would invalidate this SM's L1 (CCTL.IVALL) on every stage
             mbar_wait(&m.full[stage], phase);
-            w_full += clock64() - t0;
+            w_full += pclk() - t0;
             tc_fence_after();
             if (lane == 0) {
               const uint32_t a0 = smem_u32(m.sA + stage * NA * A_BYTES), b0 = smem_u32(m.sB + stage * BP_BYTES);
@@ -1349,10 +1359,10 @@ __global__ void __maxnreg__(GRU_MAXREG)
       if (t == NO_TILE) break;
       const Tile x = tile_of(t, mt, n1, n2, L, a.gm);
       const uint32_t acc = it & 1;
-      t0 = clock64();
+      t0 = pclk();
       mbar_wait(&m.tfull[acc], (it >> 1) & 1);
-      w_tfull += clock64() - t0;
-      t0 = clock64();
+      w_tfull += pclk() - t0;
+      t0 = pclk();
       tc_fence_after();
       const uint32_t row = x.m * 2 * BM + rank * BM + r_in;
       const bool valid = row < Q;
@@ -1382,9 +1392,9 @@ __global__ void __maxnreg__(GRU_MAXREG)
           __threadfence();
           atomicAdd(a.done1 + x.m, (uint32_t)EPI_WARPS);
         }
-        b1 += clock64() - t0;
+        b1 += pclk() - t0;
       } else {
-        b2 += clock64() - t0;
+        b2 += pclk() - t0;
       }
     }
     if (prof && lane == 0 && (warp == 2 || warp == 6)) {
@@ -1392,7 +1402,7 @@ __global__ void __maxnreg__(GRU_MAXREG)
       prof[o] = w_tfull; prof[o + 1] = b1; prof[o + 2] = b2;
     }
   }
-  if (prof && threadIdx.x == 0) prof[8] = clock64() - k_t0;
+  if (prof && threadIdx.x == 0) prof[8] = pclk() - k_t0;
   tc_fence_before();
   __syncthreads();
   if (prof && threadIdx.x == 0) prof[15] = gtimer();       // every warp of the CTA is done

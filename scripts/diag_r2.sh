@@ -4,7 +4,7 @@
 # DIAG 0 full, 3 no epilogue work, 5 cycle counters (valid results).
 set -u
 cd "${GRAFT_REPO_ROOT:-$(pwd)}"; mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+RNNLM_NVCC_FLAGS="-DRNNLM_TC_PROF=1" python -c "from paper_1801_09866_b200 import build; build.build(force=True)" > gpurun_out/build.log 2>&1   # cycle counters compiled in
 for math in ${MATHS:-bf16 bf16x3}; do for d in ${DIAGS:-0 3 5}; do
   RNNLM_TC_DIAG=$d timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-configs --also none \
     --sessions 5 --no-cache --math $math ${DIAG_ARGS:-} > gpurun_out/diag_${math}_d${d}.json 2> gpurun_out/diag_${math}_d${d}.err
@@ -19,3 +19,4 @@ except Exception as e:
 PY
   grep 'gru_tc prof' gpurun_out/diag_${math}_d${d}.err | tail -1
 done; done
+python -c "from paper_1801_09866_b200 import build; build.build(force=True)" > /dev/null 2>&1   # back to the default build
