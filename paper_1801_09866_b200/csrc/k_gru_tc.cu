@@ -352,10 +352,13 @@ __global__ void __launch_bounds__(256) k_gather_a1(TcArgs a) {
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 // Register cap of the fused kernels: three of its warps share an SM sub-partition,
-// and 3 x 152 x 32 registers leave room for one warp of k_score (48 registers)
-// per sub-partition, so the side-stream scoring runs beside the GRU.
+// and 3 x 160 x 32 registers leave 1,024 of the sub-partition's 16,384 for one
+// warp of k_score capped at 32 registers (k_score.cu), so the side-stream
+// scoring runs beside the GRU.  160 / 32 against 152 / 48: GRU 210.4 -> 207.9 us
+// (BF16X3), 143.0 -> 139.1 us (bf16), no spills left in the GRU
+// (profiles/ab_maxreg_r2.txt); 168 evicts the scoring warp altogether.
 #ifndef GRU_MAXREG
-#define GRU_MAXREG 152
+#define GRU_MAXREG 160
 #endif
 
 constexpr int TQ = 4;            // depth of the tile-id ring (producer -> MMA / epilogue)

@@ -20,7 +20,14 @@
 
 namespace rnnlm_dev {
 
-__global__ void __launch_bounds__(128) k_score(Params P, CallArgs A) {
+// register bound of the scoring kernel: it runs beside the fused GRU kernel,
+// one warp per SM sub-partition in the 1,024 registers the GRU's three warps
+// leave there (k_gru_tc.cu GRU_MAXREG)
+#ifndef RNNLM_SCORE_MAXREG
+#define RNNLM_SCORE_MAXREG 32
+#endif
+#define SCORE_BOUNDS __maxnreg__(RNNLM_SCORE_MAXREG)
+__global__ void SCORE_BOUNDS k_score(Params P, CallArgs A) {
   pdl_entry();
   const uint32_t total = P.counts[0];
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
