@@ -270,7 +270,9 @@ def burst_clocks(clk) -> bool:
     the burst peaks apply (the measured sustained peaks are for seconds-long
     power-capped runs)."""
     if not clk.get("sm_mhz") or not clk.get("sm_max_mhz"):
-        return False
+        # no clock sample landed in a few-ms region: the burst peak (the larger,
+        # i.e. the conservative denominator for a short timed region)
+        return True
     return clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"] and "sw_power_cap" not in clk.get("reasons", [])
 
 
@@ -471,7 +473,9 @@ def step_summary(args, bench, res, world, peaks, tf32_peak):
     tc = math != "fp32"
     gemv = bench.n <= 512
     k_ms = (timing["ms_gru_phase1"] + timing["ms_gru_phase2"]) if (tc and not gemv) else timing["ms_gru"]
-    peak, unit, bound, src = gru_peak(math, res["clocks_B"], peaks, tf32_peak, bench.eng.tf32x3_products() or 3)
+    # the roofline pass's clock samples, else the value pass's (same run, same frames' length)
+    clk_p = res["clocks_B"] if (res["clocks_B"] or {}).get("sm_mhz") else res["clocks"]
+    peak, unit, bound, src = gru_peak(math, clk_p, peaks, tf32_peak, bench.eng.tf32x3_products() or 3)
     achieved = flops / (k_ms / 1e3) / 1e12 if k_ms > 0 else 0.0
     pair = (math in ("bf16", "bf16x3") and args.cell == "gru" and dims.H % 256 == 0
             and os.environ.get("RNNLM_TC_PAIR", "1") != "0")
