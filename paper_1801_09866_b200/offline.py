@@ -18,6 +18,13 @@ larger GRU block -- the per-frame latency bound of the online path goes away.
 Host-side scheduling only: every step of the path still runs in the library's
 kernels; the gather / scatter of the batches' inputs and results are plain
 device tensor indexing (plumbing).
+
+Semantics: with lossless keys (off) every query gets bitwise its online score
+and state.  With lossy keys (sign / round) the first occupant of a
+hidden-cache key, and so which histories share a state, follows the LEVEL
+order, and handles are numbered in that order: results can differ from the
+online (frame-order) run; they equal the oracle replaying the same schedule
+(tests: test_offline_level_batches_vs_oracle, every key mode).
 """
 from __future__ import annotations
 
